@@ -1,0 +1,247 @@
+/*
+ * xgauss.h - C ABI of the B200-native DRR engine (libxgauss.so, sm_100a).
+ *
+ * Plain C: device pointers, sizes, POD structs and cudaStream_t (passed as
+ * void*).  No torch / C++ types cross this boundary.  Every entry point is
+ * stream-ordered, allocates nothing (caller-provided buffers and workspace)
+ * and returns an xg_status.  Data-dependent failures that the reference
+ * raises as exceptions (degenerate covariance, zero quaternion, non-finite
+ * features / gradients, entry-buffer overflow) are recorded as bits of a
+ * device status word (counters[XG_CTR_STATUS]) so that no entry point has
+ * to synchronise; the host maps them to the reference's exception classes.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   xg_preprocess_fwd   pkg/src/xsplat/rasterizer/frontend.py:104-158
+ *                       (project_splats: projection, cull, cov2D, conic,
+ *                       radius, tile rect) + gaussians.py:110-124,222-232
+ *   xg_bin_sort         frontend.py:160-173 (duplicate, np.lexsort by
+ *                       (tile, depth, index), np.searchsorted tile ranges)
+ *   xg_composite_fwd    rasterizer/_kernels.pyx:23-74 forward_tiles
+ *   xg_forward_tiles    rasterizer/_kernels.pyx:23-32 - the reference's own
+ *                       kernel-backend signature (backend.py:20-46)
+ *   xg_composite_bwd    rasterizer/_kernels.pyx:77-178 backward_tiles, with
+ *                       the L1 pixel gradient of trainer.py:117-121 fused
+ *   xg_backward_tiles   rasterizer/_kernels.pyx:77-87 - kernel-backend signature
+ *   xg_preprocess_bwd   rasterizer/backward.py:61-158 (+ trainer.py:185-188
+ *                       DensifyStats.accumulate fused)
+ *   xg_adam             trainer.py:147-170 adam_step (+ gaussians.py:234-235)
+ *   xg_densify_mark     trainer.py:206-225 densify masks and counts
+ *   xg_densify_apply    trainer.py:227-261 compaction, clone shift, split
+ *   xg_intensities      gaussians.py:230-232 GaussianCloud.intensities
+ */
+#ifndef XGAUSS_H
+#define XGAUSS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XG_ABI_VERSION 1
+
+typedef enum xg_status {
+  XG_OK = 0,
+  XG_ERR_INVALID = 1,    /* bad argument (null pointer, size)          */
+  XG_ERR_CUDA = 2,       /* CUDA launch / runtime failure              */
+  XG_ERR_WORKSPACE = 3   /* caller workspace smaller than required     */
+} xg_status;
+
+/* Device status word bits (counters[XG_CTR_STATUS]). */
+#define XG_ST_ZERO_QUAT        0x1u  /* InvalidParameterError  gaussians.py:56-57  */
+#define XG_ST_DEGENERATE       0x2u  /* NumericalDegeneracyError frontend.py:134-136 */
+#define XG_ST_NONFINITE_FEAT   0x4u  /* InvalidParameterError  gaussians.py:122-123 */
+#define XG_ST_ENTRY_OVERFLOW   0x8u  /* entry_capacity too small: re-run larger */
+#define XG_ST_GRAD_NONFINITE_SHIFT 8 /* bits 8..12: non-finite gradient per field
+                                        positions, rotations, log_scales,
+                                        raw_opacities, features (trainer.py:160-162) */
+
+/* counters[] layout (uint32, device). */
+#define XG_CTR_ACTIVE   0   /* splats surviving near-plane + on-screen cull  */
+#define XG_CTR_ENTRIES  1   /* (tile, splat) entries (may exceed capacity)    */
+#define XG_CTR_STATUS   2   /* status bits above                              */
+#define XG_CTR_TOUCH    3   /* scratch                                        */
+#define XG_NCOUNTERS    8
+
+/* Blend constants (rasterizer/kernels_py.py:13-19, frontend.py:36,
+ * gaussians.py:26, geometry.py:41). */
+#define XG_TILE_SIZE 16
+#define XG_POWER_CUTOFF (-30.0)
+#define XG_TRANSMITTANCE_FLOOR 1e-4
+#define XG_SIGMA_CLAMP 0.99
+#define XG_CUTOFF_SIGMA 7.5
+#define XG_COV2_LOWPASS 0.3
+
+/* One view (geometry.py:166-192): world->camera rotation (row-major) and
+ * translation of the 4x4 extrinsic, pixel focal length, principal point,
+ * near plane (0.01 * L_SO) and detector size.  All float64, as the
+ * reference's matrices. */
+typedef struct xg_camera {
+  double rot[9];
+  double trans[3];
+  double focal;
+  double cx, cy;
+  double near_plane;
+  int32_t width, height;
+} xg_camera;
+
+/* A Gaussian cloud: one flat float32 buffer
+ *   [positions N*3 | rotations N*4 (w,x,y,z) | log_scales N*3 |
+ *    raw_opacities N | features N*F]
+ * plus basis_weights[F] (gaussians.py:154-193). */
+typedef struct xg_cloud {
+  const float* params;
+  const float* basis;
+  int64_t n;
+  int32_t n_features;
+  int32_t _pad;
+} xg_cloud;
+
+/* Per-view screen-space buffers.  Per-Gaussian arrays are indexed by cloud
+ * row (culled rows have n_tiles == 0 and are never referenced). */
+typedef struct xg_splats {
+  double*   mean2d;       /* [N][2] projected mean, pixels                  */
+  float*    coef;         /* [N][4] A2,B2,C2,alpha: log2-density coefficients
+                             p2 = A2 dx^2 + B2 dx dy + C2 dy^2 (= power*log2 e)
+                             and opacity                                     */
+  float*    inten;        /* [N]    intensity sigmoid(F . lambda)           */
+  uint16_t* rect;         /* [N][4] tile rect tx0,ty0,tx1,ty1 (inclusive)   */
+  uint32_t* n_tiles;      /* [N]    tiles covered (0 = culled)              */
+  uint64_t* depth_key;    /* [N]    float64 bits of t_z (all ones if culled) */
+  uint32_t* order;        /* [N]    Gaussians sorted by (depth, index)      */
+  uint32_t* entry_splat;  /* [entry_capacity] Gaussian per (tile, splat) entry,
+                             sorted by (tile, depth, index)                  */
+  int64_t*  tile_ranges;  /* [n_tiles_x*n_tiles_y][2] [start, end)          */
+  uint32_t* counters;     /* [XG_NCOUNTERS]                                 */
+  int64_t   n;
+  int64_t   entry_capacity;
+} xg_splats;
+
+/* Optional float64 API outputs of the projection (frontend.py:58-74); any
+ * pointer may be NULL.  All [N]-row, written for active rows only. */
+typedef struct xg_splat_extras {
+  double* cov2d;   /* [N][3] xx, xy, yy of the low-pass-filtered covariance */
+  double* conic;   /* [N][3] its inverse                                    */
+  double* depth;   /* [N]                                                   */
+  double* t_cam;   /* [N][3]                                                */
+  double* radius;  /* [N]                                                   */
+  double* opacity; /* [N]                                                   */
+} xg_splat_extras;
+
+int32_t xg_abi_version(void);
+const char* xg_last_error(void);
+
+/* Tile grid of a camera. */
+int32_t xg_tiles_x(const xg_camera* cam);
+int32_t xg_tiles_y(const xg_camera* cam);
+
+/* Scratch bytes needed by xg_bin_sort. */
+size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles_total);
+
+/* K1: per-Gaussian projection (float64 arithmetic), writes mean2d, coef,
+ * inten, rect, n_tiles, depth_key, counters[ACTIVE], status bits.
+ * Resets counters[] first.  extras may be NULL. */
+xg_status xg_preprocess_fwd(const xg_cloud* cloud, const xg_camera* cam, xg_splats* sp,
+                            const xg_splat_extras* extras, void* stream);
+
+/* K2: depth sort (stable radix over the float64 bits of t_z, index
+ * tie-break: the reference's exact order, frontend.py:169), tile
+ * duplication (exclusive scan), stable radix sort by tile, tile ranges.
+ * Fills order, entry_splat, tile_ranges, counters[ENTRIES]. */
+xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* K3: front-to-back compositing.  Writes image[H][W], t_final[H][W] (final
+ * transmittance) and n_contrib[H][W] (1 + index of the last blended entry
+ * relative to the tile start, 0 if none).  If target != NULL also
+ * accumulates sum |image - target| into *l1_sum (double, device). */
+xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                           int32_t* n_contrib, const float* target, double* l1_sum, void* stream);
+
+/* K4a: reverse replay.  Per-pixel upstream gradient is dl_dimage[H][W], or,
+ * when dl_dimage == NULL, the fused L1 gradient l1_scale*sign(image-target).
+ * Accumulates (atomically) into grad_acc[N][8]:
+ *   {gx, gy, gxx, gxy, gyy, g_int, g_pow, 0}
+ * with gx = sum G*(2 A2 dx + B2 dy), gy = sum G*(B2 dx + 2 C2 dy),
+ * gxx/gxy/gyy = sum G*dx^2 / dx*dy / dy^2, g_pow = sum G,
+ * G = dL/dsigma * sigma on unclamped pairs (= the reference's g_power).
+ * grad_acc must be zeroed by the caller. */
+xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
+                           const int32_t* n_contrib, const float* dl_dimage, const float* image,
+                           const float* target, float l1_scale, float* grad_acc, void* stream);
+
+/* K4b: chain rule to every cloud field (float64 arithmetic).  Writes
+ * grads (flat, same layout as params; zero rows for culled Gaussians),
+ * screen_norms[N], visible[N]; flags non-finite fields in the status word.
+ * If norm_sum/obs_count/world_grad_sum are non-NULL they are accumulated
+ * (DensifyStats.accumulate, trainer.py:185-188).  g_mean_out / g_conic_out /
+ * g_int_out / g_alpha_out (optional, [N][2],[N][3],[N],[N] float64) receive
+ * the reference's kernel-level gradients (backward_tiles outputs). */
+xg_status xg_preprocess_bwd(const xg_cloud* cloud, const xg_camera* cam, const xg_splats* sp,
+                            const float* grad_acc, float* grads, float* screen_norms,
+                            uint8_t* visible, float* norm_sum, int32_t* obs_count,
+                            float* world_grad_sum, double* g_mean_out, double* g_conic_out,
+                            double* g_int_out, double* g_alpha_out, void* stream);
+
+/* Finite check of a flat gradient buffer: sets status bit 8+f for every
+ * field f holding a NaN/Inf. */
+xg_status xg_check_finite(const float* grads, int64_t n, int32_t n_features, uint32_t* counters,
+                          void* stream);
+
+/* K4c: fused Adam over all fields + quaternion renormalisation, in place.
+ * lr[5] per field (positions, rotations, log_scales, raw_opacities,
+ * features).  bc1 = 1-beta1^t, bc2 = 1-beta2^t.  Honours the non-finite bits
+ * in counters[STATUS] with the reference's partial-update semantics: fields
+ * before the first non-finite one are updated, the rest (and the renorm)
+ * are not. */
+xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq,
+                  int64_t n, int32_t n_features, const double* lr, double beta1, double beta2,
+                  double eps, double bc1, double bc2, const uint32_t* counters, void* stream);
+
+/* K4d (1): density-control masks.  flags[N] bit0 high-gradient, bit1 large,
+ * bit2 prune, bit3 clone, bit4 split; counts[4] = {prune, clone, split, keep}
+ * (counts zeroed by the callee). */
+xg_status xg_densify_mark(const float* params, int64_t n, int32_t n_features,
+                          const float* norm_sum, const int32_t* obs_count, double grad_threshold,
+                          double size_threshold, double prune_opacity, uint8_t* flags,
+                          uint32_t* counts, void* stream);
+
+/* K4d (2): compaction into new buffers laid out [keep | clone | split x2]
+ * (trainer.py:227-261).  allow_growth = 0 drops clone/split (cap reached).
+ * split_normals: [n_split][2][3] float64 standard normals (host PCG64 draw,
+ * uploaded).  new_params / new_exp_avg / new_exp_avg_sq sized n_new rows;
+ * moments of new rows are zeroed.  scratch: xg_densify_scratch_bytes(n). */
+size_t xg_densify_scratch_bytes(int64_t n);
+xg_status xg_densify_apply(const float* params, const float* exp_avg, const float* exp_avg_sq,
+                           int64_t n, int32_t n_features, const uint8_t* flags,
+                           const float* world_grad_sum, const double* split_normals,
+                           double log_split_factor, int32_t allow_growth, float* new_params,
+                           float* new_exp_avg, float* new_exp_avg_sq, int64_t n_new,
+                           uint32_t* scratch, void* stream);
+
+/* sigmoid(F . lambda) for all N (float32 out); flags non-finite features. */
+xg_status xg_intensities(const xg_cloud* cloud, float* out, uint32_t* counters, void* stream);
+
+/* The reference kernel-backend contract (_kernels.pyx:23-32, 77-87) on
+ * device buffers: n_splats active rows with float64 means2d[A][2],
+ * conics[A][3], intensities[A], opacities[A]; entry_splat[E] (row indices),
+ * tile_ranges[T][2].  image out float64 [h][w].  workspace >=
+ * xg_tiles_workspace_bytes(n_splats, h, w). */
+size_t xg_tiles_workspace_bytes(int64_t n_splats, int32_t h, int32_t w);
+xg_status xg_forward_tiles(int32_t h, int32_t w, const double* means2d, const double* conics,
+                           const double* intensities, const double* opacities,
+                           const int32_t* entry_splat, int64_t n_entries,
+                           const int64_t* tile_ranges, int64_t n_splats, double* image,
+                           void* workspace, size_t workspace_bytes, void* stream);
+xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const double* conics,
+                            const double* intensities, const double* opacities,
+                            const int32_t* entry_splat, int64_t n_entries,
+                            const int64_t* tile_ranges, int64_t n_splats, const double* dl_dimage,
+                            double* g_mean, double* g_conic, double* g_int, double* g_alpha,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XGAUSS_H */

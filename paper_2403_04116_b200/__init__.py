@@ -1,0 +1,57 @@
+"""B200-native Differentiable Radiative Rasterization (X-Gaussian, arXiv 2403.04116).
+
+A drop-in for the reference engine's hot path (``xsplat``): the same Python
+API - ``GaussianCloud``, ``render`` / ``render_view`` / ``project_splats`` /
+``render_backward``, ``adam_step`` / ``densify_and_prune`` / ``train`` - on
+hand-written sm_100a CUDA kernels behind the C ABI of ``include/xgauss.h``
+(libxgauss.so).  There is no CPU fallback.
+"""
+
+from .acui import CuboidSpec, init_alternative, init_cloud, sample_cuboid
+from .errors import (
+    ConfigError,
+    DatasetError,
+    InvalidParameterError,
+    NativeError,
+    NumericalDegeneracyError,
+    StaleSplatsError,
+    TooManyPointsError,
+    TrainingDivergenceError,
+    XSplatError,
+)
+from .gaussians import (
+    GaussianCloud,
+    RadiativeGaussian,
+    covariance_2d,
+    covariance_3d,
+    logit,
+    quaternions_to_rotations,
+    rirf,
+    sigmoid,
+)
+from .geometry import (
+    ExtrinsicMatrix,
+    IntrinsicMatrix,
+    ScannerConfig,
+    camera_to_image,
+    equal_interval_angles,
+    extrinsic_from_angle,
+    intrinsic_from_config,
+    projection_jacobian,
+    viewing_rotation,
+    world_to_camera,
+)
+from .rasterizer import (
+    Projection,
+    RenderGradients,
+    SplatList,
+    active_backend,
+    blend_pixel,
+    brute_force_render,
+    project_splats,
+    render,
+    render_backward,
+    render_view,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,583 @@
+// K3 / K4a: per-tile front-to-back compositing and its reverse replay.
+//
+// Reference semantics (rasterizer/_kernels.pyx:41-73, 121-177):
+//   per pixel, entries of its tile in (depth, index) order; stop once
+//   T < 1e-4 (tested BEFORE each entry); skip an entry if power > 0 or
+//   power < -30; sigma = min(alpha e^power, 0.99); acc += i sigma T;
+//   T *= 1 - sigma.  The pixel centre is the integer lattice point.
+//
+// B200 mapping.  One CTA per 16x16 tile, 4 warps, each warp owns an 8x8
+// sub-block with 2 vertically adjacent pixels per lane (they share dx and
+// the dx-only terms).  Entries are staged 128 at a time into shared memory
+// (one gather per thread: entry id -> 36 B splat record, mean re-based to
+// the tile origin in float64 so dx/dy keep ~1e-6 px precision).  Each warp
+// then culls the staged batch against its own 8x8 sub-block with an exact
+// ellipse/rectangle test (max of the concave log-density over the
+// rectangle vs the -30 cut-off, with margin) and walks only the survivors,
+// so ~half of the (pixel, entry) pairs the reference evaluates are never
+// touched.  Culling never changes results: a culled entry has power < -30
+// on every pixel of the sub-block, which the reference skips too.
+//
+// Power is evaluated on the log2 scale, p2 = A2 dx^2 + B2 dx dy + C2 dy^2
+// (= power * log2 e) with one MUFU.EX2 per pair; the transmittance update
+// T <- T - sigma T is a single fused multiply-add.
+#include "xg_internal.cuh"
+
+namespace xg {
+namespace {
+
+constexpr int kThreads = 128;   // 4 warps per tile
+constexpr int kBatch = 128;     // entries staged per round
+constexpr float kCullMargin = 0.05f;
+
+struct Rec {
+  float4 a;  // mx, my (tile-relative), A2, B2
+  float4 b;  // C2, alpha, intensity, 0
+};
+
+// Max of the concave p2 over the rectangle of pixel centres [xa,xb]x[ya,yb]
+// (tile-relative) compared against the cut-off.  The maximiser lies on the
+// edge facing the mean (or is the mean), so checking the two clamped edge
+// maxima is exact.
+__device__ __forceinline__ bool overlaps(const Rec& r, float xa, float xb, float ya, float yb) {
+  const float mx = r.a.x, my = r.a.y, A = r.a.z, B = r.a.w, C = r.b.x;
+  if (!(A < 0.f) || !(C < 0.f)) return true;
+  const float dx1 = fminf(fmaxf(mx, xa), xb) - mx;
+  const float dy1 = fminf(fmaxf(-B * dx1 / (2.f * C), ya - my), yb - my);
+  const float p1 = A * dx1 * dx1 + B * dx1 * dy1 + C * dy1 * dy1;
+  const float dy2 = fminf(fmaxf(my, ya), yb) - my;
+  const float dx2 = fminf(fmaxf(-B * dy2 / (2.f * A), xa - mx), xb - mx);
+  const float p2 = A * dx2 * dx2 + B * dx2 * dy2 + C * dy2 * dy2;
+  return fmaxf(p1, p2) >= kCut2 - kCullMargin;
+}
+
+__device__ __forceinline__ void stage(Rec* s_rec, uint32_t* s_gid, long long k, long long end,
+                                      const uint32_t* __restrict__ entry,
+                                      const double2* __restrict__ mean2d,
+                                      const float4* __restrict__ coef,
+                                      const float* __restrict__ inten, double x0, double y0) {
+  const int t = threadIdx.x;
+  if (k < end) {
+    const uint32_t g = __ldg(entry + k);
+    const double2 m = __ldg(mean2d + g);
+    const float4 c = __ldg(coef + g);
+    const float it = __ldg(inten + g);
+    Rec r;
+    r.a = make_float4((float)(m.x - x0), (float)(m.y - y0), c.x, c.y);
+    r.b = make_float4(c.z, c.w, it, 0.f);
+    s_rec[t] = r;
+    if (s_gid) s_gid[t] = g;
+  }
+}
+
+// Compacts this warp's survivors of the staged batch into list (ascending).
+__device__ __forceinline__ int cull_batch(const Rec* s_rec, uint8_t* list, int nb, float xa,
+                                          float xb, float ya, float yb) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  int cnt = 0;
+#pragma unroll
+  for (int r = 0; r < kBatch / 32; ++r) {
+    const int j = r * 32 + lane;
+    const bool keep = j < nb && overlaps(s_rec[j], xa, xb, ya, yb);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) list[cnt + __popc(bal & lt)] = (uint8_t)j;
+    cnt += __popc(bal);
+  }
+  __syncwarp();
+  return cnt;
+}
+
+struct TileGeom {
+  int x0, y0;
+  int px, py0;     // pixel of this lane (second pixel is py0 + 1)
+  float fx, fy0, fy1;
+  float xa, xb, ya, yb;  // warp sub-block, tile-relative pixel centres
+  bool in0, in1;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(int tile, int ntx, int w, int h) {
+  TileGeom g;
+  const int tx = tile % ntx, ty = tile / ntx;
+  g.x0 = tx * kTile;
+  g.y0 = ty * kTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sx = (warp & 1) * 8, sy = (warp >> 1) * 8;
+  const int lx = sx + (lane & 7), ly = sy + 2 * (lane >> 3);
+  g.px = g.x0 + lx;
+  g.py0 = g.y0 + ly;
+  g.fx = (float)lx;
+  g.fy0 = (float)ly;
+  g.fy1 = (float)(ly + 1);
+  g.xa = (float)sx;
+  g.xb = (float)(sx + 7);
+  g.ya = (float)sy;
+  g.yb = (float)(sy + 7);
+  g.in0 = g.px < w && g.py0 < h;
+  g.in1 = g.px < w && g.py0 + 1 < h;
+  return g;
+}
+
+struct FwdArgs {
+  const double2* mean2d;
+  const float4* coef;
+  const float* inten;
+  const uint32_t* entry;
+  const long long* ranges;
+  float* image;
+  float* t_final;
+  int* n_contrib;
+  const float* target;
+  double* l1_sum;
+  int ntx, w, h;
+};
+
+// One pixel, one entry: the blend step of _kernels.pyx:57-72.
+__device__ __forceinline__ void blend(float dy, float bdx, float adx2, const Rec& r, int krel,
+                                      float& T, float& acc, int& last) {
+  const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
+  const float dens = ex2_approx(p2);
+  float sg = fminf(__fmul_rn(r.b.y, dens), kClamp);
+  const bool ok = (p2 <= 0.f) & (p2 >= kCut2) & (T >= kFloor);
+  sg = ok ? sg : 0.f;
+  const float w = __fmul_rn(sg, T);
+  acc = __fmaf_rn(r.b.z, w, acc);
+  T = __fmaf_rn(-sg, T, T);
+  last = ok ? krel : last;
+}
+
+__global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
+  __shared__ Rec s_rec[kBatch];
+  __shared__ uint8_t s_list[kThreads / 32][kBatch];
+  __shared__ float s_l1[kThreads / 32];
+  const int tile = blockIdx.x;
+  const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
+  const int warp = threadIdx.x >> 5;
+  const long long start = a.ranges[2 * tile], end = a.ranges[2 * tile + 1];
+  float T0 = g.in0 ? 1.f : 0.f, T1 = g.in1 ? 1.f : 0.f;
+  float acc0 = 0.f, acc1 = 0.f;
+  int last0 = -1, last1 = -1;
+  bool warp_alive = __any_sync(0xffffffffu, g.in0 || g.in1);
+  for (long long b0 = start; b0 < end; b0 += kBatch) {
+    stage(s_rec, nullptr, b0 + threadIdx.x, end, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
+    __syncthreads();
+    if (warp_alive) {
+      const int nb = (int)min((long long)kBatch, end - b0);
+      const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
+      const int kbase = (int)(b0 - start);
+      for (int q = 0; q < cnt; ++q) {
+        const int j = s_list[warp][q];
+        const Rec r = s_rec[j];
+        const float dx = __fsub_rn(g.fx, r.a.x);
+        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+        const float bdx = __fmul_rn(r.a.w, dx);
+        blend(__fsub_rn(g.fy0, r.a.y), bdx, adx2, r, kbase + j, T0, acc0, last0);
+        blend(__fsub_rn(g.fy1, r.a.y), bdx, adx2, r, kbase + j, T1, acc1, last1);
+      }
+      warp_alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
+    }
+    if (!__syncthreads_or(warp_alive)) break;
+  }
+  const long long o0 = (long long)g.py0 * a.w + g.px;
+  float l1 = 0.f;
+  if (g.in0) {
+    a.image[o0] = acc0;
+    if (a.t_final) a.t_final[o0] = T0;
+    if (a.n_contrib) a.n_contrib[o0] = last0 + 1;
+    if (a.target) l1 += fabsf(acc0 - a.target[o0]);
+  }
+  if (g.in1) {
+    const long long o1 = o0 + a.w;
+    a.image[o1] = acc1;
+    if (a.t_final) a.t_final[o1] = T1;
+    if (a.n_contrib) a.n_contrib[o1] = last1 + 1;
+    if (a.target) l1 += fabsf(acc1 - a.target[o1]);
+  }
+  if (a.target && a.l1_sum) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    if ((threadIdx.x & 31) == 0) s_l1[warp] = l1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) t += (double)s_l1[w];
+      atomicAdd(a.l1_sum, t);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward
+// ---------------------------------------------------------------------------
+struct BwdArgs {
+  const double2* mean2d;
+  const float4* coef;
+  const float* inten;
+  const uint32_t* entry;
+  const long long* ranges;
+  const float* t_final;
+  const int* n_contrib;
+  const float* dl;       // upstream dL/dI, or null -> fused L1
+  const float* image;
+  const float* target;
+  float l1_scale;
+  float* grad_acc;       // [N][8]
+  int ntx, w, h;
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Reverse step for one pixel and one entry: the gradient pass of
+// _kernels.pyx:142-177 run back to front, with the suffix sum accumulated
+// directly (no acc - prefix - contrib cancellation) and T restored by
+// division by (1 - sigma).
+__device__ __forceinline__ void unblend(float dy, float bdx, float adx2, float a2dx, float dx,
+                                        const Rec& r, bool act, float g, float& T, float& S,
+                                        float (&acc)[7]) {
+  const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
+  const float dens = ex2_approx(p2);
+  const float sraw = __fmul_rn(r.b.y, dens);
+  const bool valid = act & (p2 <= 0.f) & (p2 >= kCut2);
+  const bool clamped = sraw >= kClamp;
+  float sg = fminf(sraw, kClamp);
+  sg = valid ? sg : 0.f;
+  const float rc = rcp_approx(1.f - sg);
+  const float Tb = T * rc;
+  const float w = sg * Tb;
+  const float it = r.b.z;
+  const float dsig = g * (it * Tb - S * rc);
+  const float G = (valid && !clamped) ? dsig * sg : 0.f;
+  acc[5] = fmaf(g, w, acc[5]);                 // g_int
+  acc[6] += G;                                 // sum G  (-> g_alpha, g_raw)
+  acc[0] = fmaf(G, fmaf(r.a.w, dy, a2dx), acc[0]);           // G (2A dx + B dy)
+  acc[1] = fmaf(G, fmaf(2.f * r.b.x, dy, bdx), acc[1]);      // G (B dx + 2C dy)
+  acc[2] = fmaf(G, dx * dx, acc[2]);
+  acc[3] = fmaf(G, dx * dy, acc[3]);
+  acc[4] = fmaf(G, dy * dy, acc[4]);
+  S = fmaf(it, w, S);
+  T = valid ? Tb : T;
+}
+
+// Sum 8 per-lane values over the warp; returns the total of value
+// index ((lane>>2)&7) in every lane (transpose-reduce: 9 shuffles).
+__device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = up ? v[i] : v[i + 4];
+      const float keep = up ? v[i + 4] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = up ? v[i] : v[i + 2];
+      const float keep = up ? v[i + 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  {
+    const bool up = lane & 4;
+    const float send = up ? v[0] : v[1];
+    const float keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+__global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
+  __shared__ Rec s_rec[kBatch];
+  __shared__ uint32_t s_gid[kBatch];
+  __shared__ uint8_t s_list[kThreads / 32][kBatch];
+  __shared__ float4 s_acc[kThreads / 32][kBatch][2];
+  __shared__ int s_last;
+  const int tile = blockIdx.x;
+  const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long start = a.ranges[2 * tile], end = a.ranges[2 * tile + 1];
+  const long long o0 = (long long)g.py0 * a.w + g.px, o1 = o0 + a.w;
+  float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
+  int last0 = -1, last1 = -1;
+  if (g.in0) {
+    T0 = a.t_final[o0];
+    last0 = a.n_contrib[o0] - 1;
+    g0 = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
+  }
+  if (g.in1) {
+    T1 = a.t_final[o1];
+    last1 = a.n_contrib[o1] - 1;
+    g1 = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
+  }
+  if (g0 == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
+  if (g1 == 0.f) last1 = -1;
+  int wl = max(last0, last1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+  if (threadIdx.x == 0) s_last = -1;
+  __syncthreads();
+  if (lane == 0) atomicMax(&s_last, wl);
+  __syncthreads();
+  const long long hi = start + s_last + 1;  // one past the last entry any pixel needs
+  float S0 = 0.f, S1 = 0.f;
+  for (long long b1 = hi; b1 > start; b1 -= kBatch) {
+    const long long b0 = b1 - kBatch > start ? b1 - kBatch : start;
+    const int nb = (int)(b1 - b0);
+    stage(s_rec, s_gid, b0 + threadIdx.x, b1, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
+    {
+      float4* z = &s_acc[0][0][0];
+      for (int i = threadIdx.x; i < (kThreads / 32) * kBatch * 2; i += kThreads)
+        z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    const int kbase = (int)(b0 - start);
+    if (wl >= kbase) {
+      const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
+      for (int q = cnt - 1; q >= 0; --q) {
+        const int j = s_list[warp][q];
+        const int krel = kbase + j;
+        if (krel > wl) continue;  // warp-uniform
+        const Rec r = s_rec[j];
+        const float dx = __fsub_rn(g.fx, r.a.x);
+        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+        const float bdx = __fmul_rn(r.a.w, dx);
+        const float a2dx = 2.f * r.a.z * dx;
+        float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        unblend(__fsub_rn(g.fy0, r.a.y), bdx, adx2, a2dx, dx, r, krel <= last0, g0, T0, S0, acc);
+        unblend(__fsub_rn(g.fy1, r.a.y), bdx, adx2, a2dx, dx, r, krel <= last1, g1, T1, S1, acc);
+        float v[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], 0.f};
+        const float tot = warp_reduce8(v);
+        if ((lane & 3) == 0) {
+          const int idx = (lane >> 2) & 7;
+          reinterpret_cast<float*>(&s_acc[warp][j][0])[idx] = tot;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      float4 u = s_acc[0][threadIdx.x][0], v = s_acc[0][threadIdx.x][1];
+#pragma unroll
+      for (int w = 1; w < kThreads / 32; ++w) {
+        const float4 u2 = s_acc[w][threadIdx.x][0], v2 = s_acc[w][threadIdx.x][1];
+        u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
+        v.x += v2.x; v.y += v2.y; v.z += v2.z;
+      }
+      if (u.x != 0.f || u.y != 0.f || u.z != 0.f || u.w != 0.f || v.x != 0.f || v.y != 0.f ||
+          v.z != 0.f) {
+        float* dst = a.grad_acc + 8 * (long long)s_gid[threadIdx.x];
+        red_add_v4(dst, u.x, u.y, u.z, u.w);
+        red_add_v4(dst + 4, v.x, v.y, v.z, 0.f);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reference kernel-backend adapters (forward_tiles / backward_tiles).
+// ---------------------------------------------------------------------------
+__global__ void k_rows_to_records(long long n, const double* means, const double* conics,
+                                  const double* inten, const double* opac, double2* mean2d,
+                                  float4* coef, float* it) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  mean2d[i] = make_double2(means[2 * i], means[2 * i + 1]);
+  coef[i] = make_float4((float)(-0.5 * kLog2e * conics[3 * i]), (float)(-kLog2e * conics[3 * i + 1]),
+                        (float)(-0.5 * kLog2e * conics[3 * i + 2]), (float)opac[i]);
+  it[i] = (float)inten[i];
+}
+
+__global__ void k_f32_to_f64(const float* a, double* b, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (double)a[i];
+}
+
+__global__ void k_f64_to_f32(const double* a, float* b, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
+}
+
+__global__ void k_acc_to_reference(long long n, const float* acc, const double* opac, double* g_mean,
+                                   double* g_conic, double* g_int, double* g_alpha) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* a = acc + 8 * i;
+  g_mean[2 * i] = -kLn2 * (double)a[0];
+  g_mean[2 * i + 1] = -kLn2 * (double)a[1];
+  g_conic[3 * i] = -0.5 * (double)a[2];
+  g_conic[3 * i + 1] = -(double)a[3];
+  g_conic[3 * i + 2] = -0.5 * (double)a[4];
+  g_int[i] = (double)a[5];
+  g_alpha[i] = opac[i] > 0.0 ? (double)a[6] / opac[i] : 0.0;
+}
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct TilesWs {
+  double2* mean2d;
+  float4* coef;
+  float* inten;
+  float* image;
+  float* t_final;
+  int* n_contrib;
+  float* dl;
+  float* acc;
+};
+
+size_t tiles_ws(int64_t n, int32_t h, int32_t w, TilesWs* out, char* base) {
+  const size_t hw = (size_t)h * (size_t)w;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += al(bytes);
+    return p;
+  };
+  TilesWs t;
+  t.mean2d = (double2*)take(16 * (size_t)n);
+  t.coef = (float4*)take(16 * (size_t)n);
+  t.inten = (float*)take(4 * (size_t)n);
+  t.image = (float*)take(4 * hw);
+  t.t_final = (float*)take(4 * hw);
+  t.n_contrib = (int*)take(4 * hw);
+  t.dl = (float*)take(4 * hw);
+  t.acc = (float*)take(32 * (size_t)n);
+  if (out) *out = t;
+  return off + 256;
+}
+
+}  // namespace
+}  // namespace xg
+
+using namespace xg;
+
+extern "C" {
+
+xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                           int32_t* n_contrib, const float* target, double* l1_sum, void* stream) {
+  if (!cam || !sp || !image || !sp->entry_splat || !sp->tile_ranges || !sp->mean2d || !sp->coef ||
+      !sp->inten) {
+    set_error_msg("xg_composite_fwd: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+            (const long long*)sp->tile_ranges, image, t_final, n_contrib, target, l1_sum,
+            tiles_x(*cam), cam->width, cam->height};
+  const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
+  k_composite_fwd<<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("k_composite_fwd");
+}
+
+xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
+                           const int32_t* n_contrib, const float* dl_dimage, const float* image,
+                           const float* target, float l1_scale, float* grad_acc, void* stream) {
+  if (!cam || !sp || !t_final || !n_contrib || !grad_acc || (!dl_dimage && (!image || !target))) {
+    set_error_msg("xg_composite_bwd: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+            (const long long*)sp->tile_ranges, t_final, n_contrib, dl_dimage, image, target,
+            l1_scale, grad_acc, tiles_x(*cam), cam->width, cam->height};
+  const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
+  k_composite_bwd<<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("k_composite_bwd");
+}
+
+size_t xg_tiles_workspace_bytes(int64_t n_splats, int32_t h, int32_t w) {
+  return tiles_ws(n_splats > 0 ? n_splats : 1, h, w, nullptr, nullptr);
+}
+
+static xg_status tiles_common(int32_t h, int32_t w, const double* means2d, const double* conics,
+                              const double* intensities, const double* opacities,
+                              const int32_t* entry_splat, const int64_t* tile_ranges,
+                              int64_t n_splats, void* workspace, size_t workspace_bytes,
+                              cudaStream_t s, TilesWs& t, xg_camera& cam, xg_splats& sp) {
+  if (h < 1 || w < 1 || n_splats < 0 || !tile_ranges || !workspace ||
+      (n_splats > 0 && (!means2d || !conics || !intensities || !opacities || !entry_splat))) {
+    set_error_msg("xg_*_tiles: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  if (workspace_bytes < xg_tiles_workspace_bytes(n_splats, h, w)) {
+    set_error_msg("xg_*_tiles: workspace too small");
+    return XG_ERR_WORKSPACE;
+  }
+  tiles_ws(n_splats > 0 ? n_splats : 1, h, w, &t, (char*)workspace);
+  cam = xg_camera{};
+  cam.width = w;
+  cam.height = h;
+  if (n_splats > 0) {
+    k_rows_to_records<<<div_up(n_splats, 256), 256, 0, s>>>(n_splats, means2d, conics, intensities,
+                                                            opacities, t.mean2d, t.coef, t.inten);
+    xg_status st = check_launch("k_rows_to_records");
+    if (st != XG_OK) return st;
+  }
+  sp = xg_splats{};
+  sp.mean2d = (double*)t.mean2d;
+  sp.coef = (float*)t.coef;
+  sp.inten = t.inten;
+  sp.entry_splat = (uint32_t*)entry_splat;
+  sp.tile_ranges = (int64_t*)tile_ranges;
+  sp.n = n_splats;
+  return XG_OK;
+}
+
+xg_status xg_forward_tiles(int32_t h, int32_t w, const double* means2d, const double* conics,
+                           const double* intensities, const double* opacities,
+                           const int32_t* entry_splat, int64_t n_entries,
+                           const int64_t* tile_ranges, int64_t n_splats, double* image,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  (void)n_entries;
+  cudaStream_t s = (cudaStream_t)stream;
+  TilesWs t;
+  xg_camera cam;
+  xg_splats sp;
+  xg_status st = tiles_common(h, w, means2d, conics, intensities, opacities, entry_splat, tile_ranges,
+                              n_splats, workspace, workspace_bytes, s, t, cam, sp);
+  if (st != XG_OK) return st;
+  if ((st = xg_composite_fwd(&cam, &sp, t.image, nullptr, nullptr, nullptr, nullptr, stream)) != XG_OK)
+    return st;
+  k_f32_to_f64<<<div_up((int64_t)h * w, 256), 256, 0, s>>>(t.image, image, (long long)h * w);
+  return check_launch("k_f32_to_f64");
+}
+
+xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const double* conics,
+                            const double* intensities, const double* opacities,
+                            const int32_t* entry_splat, int64_t n_entries,
+                            const int64_t* tile_ranges, int64_t n_splats, const double* dl_dimage,
+                            double* g_mean, double* g_conic, double* g_int, double* g_alpha,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  (void)n_entries;
+  cudaStream_t s = (cudaStream_t)stream;
+  TilesWs t;
+  xg_camera cam;
+  xg_splats sp;
+  xg_status st = tiles_common(h, w, means2d, conics, intensities, opacities, entry_splat, tile_ranges,
+                              n_splats, workspace, workspace_bytes, s, t, cam, sp);
+  if (st != XG_OK) return st;
+  if (n_splats == 0) return XG_OK;
+  if (!dl_dimage || !g_mean || !g_conic || !g_int || !g_alpha) {
+    set_error_msg("xg_backward_tiles: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  if ((st = xg_composite_fwd(&cam, &sp, t.image, t.t_final, t.n_contrib, nullptr, nullptr, stream)) != XG_OK)
+    return st;
+  const long long hw = (long long)h * w;
+  k_f64_to_f32<<<div_up(hw, 256), 256, 0, s>>>(dl_dimage, t.dl, hw);
+  cudaMemsetAsync(t.acc, 0, 32 * (size_t)n_splats, s);
+  if ((st = xg_composite_bwd(&cam, &sp, t.t_final, t.n_contrib, t.dl, nullptr, nullptr, 0.f, t.acc,
+                             stream)) != XG_OK)
+    return st;
+  k_acc_to_reference<<<div_up(n_splats, 256), 256, 0, s>>>(n_splats, t.acc, opacities, g_mean, g_conic,
+                                                           g_int, g_alpha);
+  return check_launch("k_acc_to_reference");
+}
+
+}  // extern "C"

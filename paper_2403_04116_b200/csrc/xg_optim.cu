@@ -1,0 +1,320 @@
+// K4c fused Adam and K4d density control (trainer.py:147-268).
+//
+// Adam: one thread per Gaussian walks its 11 + N_f parameters (all fields
+// live in one flat buffer, so the per-field rows are contiguous and a warp
+// touches contiguous cache lines), updates moments and parameters, and
+// renormalises the quaternion in the same pass - one read of p, m, v, g
+// and one write of p, m, v per element, the HBM minimum (28 B/element).
+// Arithmetic is float64 in registers (the reference is float64 end to end).
+//
+// Density control: a mark kernel evaluates the clone / split / prune masks
+// (float64 comparisons, so identical to the reference on the same inputs)
+// and counts them; the host then applies the cap rule and calls apply,
+// which scans the three masks and scatters keep / clone / split-child rows
+// into the new [keep | clone | split x2] layout.
+#include <math.h>
+
+#include "xg_sort.cuh"
+
+namespace xg {
+namespace {
+
+constexpr int kFields = 5;
+
+struct Layout {
+  long long off[kFields];
+  int width[kFields];
+};
+
+__host__ Layout make_layout(long long n, int nf) {
+  Layout L;
+  const int w[kFields] = {3, 4, 3, 1, nf};
+  long long o = 0;
+  for (int f = 0; f < kFields; ++f) {
+    L.off[f] = o;
+    L.width[f] = w[f];
+    o += n * w[f];
+  }
+  return L;
+}
+
+struct AdamArgs {
+  float* p;
+  const float* g;
+  float* m;
+  float* v;
+  long long n;
+  Layout L;
+  double lr[kFields];
+  double b1, b2, eps, bc1, bc2;
+  const uint32_t* counters;
+};
+
+__global__ void k_adam(AdamArgs a) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const uint32_t bad = a.counters ? (a.counters[XG_CTR_STATUS] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f : 0u;
+  for (int f = 0; f < kFields; ++f) {
+    if (bad & ((2u << f) - 1u)) return;  // a field <= f diverged: stop (reference raises here)
+    const long long base = a.L.off[f] + i * a.L.width[f];
+    const double lr = a.lr[f];
+    for (int c = 0; c < a.L.width[f]; ++c) {
+      const long long e = base + c;
+      const double g = a.g[e];
+      double m = a.m[e], v = a.v[e];
+      m = a.b1 * m + (1.0 - a.b1) * g;
+      v = a.b2 * v + (1.0 - a.b2) * g * g;
+      a.m[e] = (float)m;
+      a.v[e] = (float)v;
+      a.p[e] = (float)((double)a.p[e] - lr * (m / a.bc1) / (sqrt(v / a.bc2) + a.eps));
+    }
+  }
+  // normalize_rotations (gaussians.py:234-235)
+  float* q = a.p + a.L.off[1] + 4 * i;
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  const double nrm = sqrt(((w * w + x * x) + y * y) + z * z);
+  q[0] = (float)(w / nrm);
+  q[1] = (float)(x / nrm);
+  q[2] = (float)(y / nrm);
+  q[3] = (float)(z / nrm);
+}
+
+__device__ __forceinline__ double sigmoid64(double x) { return det_sigmoid(x); }
+
+__global__ void k_densify_mark(const float* p, long long n, Layout L, const float* norm_sum,
+                               const int32_t* obs, double gthr, double sthr, double pthr,
+                               uint8_t* flags, uint32_t* counts) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  uint8_t fl = 0;
+  if (i < n) {
+    const int o = obs[i];
+    const double avg = (double)norm_sum[i] / (double)(o > 1 ? o : 1);
+    const bool high = avg >= gthr;
+    const float* ls = p + L.off[2] + 3 * i;
+    double mx = det_exp((double)ls[0]);
+    mx = fmax(mx, det_exp((double)ls[1]));
+    mx = fmax(mx, det_exp((double)ls[2]));
+    const bool large = mx > sthr;
+    const bool prune = sigmoid64((double)p[L.off[3] + i]) < pthr;
+    const bool clone = high && !large && !prune;
+    const bool split = high && large && !prune;
+    fl = (uint8_t)(high | (large << 1) | (prune << 2) | (clone << 3) | (split << 4));
+    flags[i] = fl;
+  }
+  const unsigned bp = __ballot_sync(0xffffffffu, fl & 4), bc = __ballot_sync(0xffffffffu, fl & 8),
+                 bs = __ballot_sync(0xffffffffu, fl & 16);
+  if (lane_id() == 0) {
+    if (bp) atomicAdd(&counts[0], __popc(bp));
+    if (bc) atomicAdd(&counts[1], __popc(bc));
+    if (bs) atomicAdd(&counts[2], __popc(bs));
+  }
+}
+
+// class masks for the scans: keep = !prune && !split (when growth is
+// disabled split rows are kept, matching clone[:] = split[:] = False).
+__global__ void k_class_masks(const uint8_t* flags, long long n, int allow, uint32_t* mk, uint32_t* mc,
+                              uint32_t* ms) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t f = flags[i];
+  const bool prune = f & 4;
+  const bool clone = allow && (f & 8);
+  const bool split = allow && (f & 16);
+  mk[i] = (!prune && !split) ? 1u : 0u;
+  mc[i] = clone ? 1u : 0u;
+  ms[i] = split ? 1u : 0u;
+}
+
+__device__ __forceinline__ void rot_of(const float* q4, double* r) {
+  double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
+  const double nrm = sqrt(((w * w + x * x) + y * y) + z * z);
+  w /= nrm; x /= nrm; y /= nrm; z /= nrm;
+  r[0] = 1.0 - 2.0 * (y * y + z * z); r[1] = 2.0 * (x * y - w * z); r[2] = 2.0 * (x * z + w * y);
+  r[3] = 2.0 * (x * y + w * z); r[4] = 1.0 - 2.0 * (x * x + z * z); r[5] = 2.0 * (y * z - w * x);
+  r[6] = 2.0 * (x * z - w * y); r[7] = 2.0 * (y * z + w * x); r[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+struct ApplyArgs {
+  const float *p, *m, *v;
+  long long n, n_new;
+  Layout L, Ln;
+  const uint32_t *mk, *mc, *ms;       // masks
+  const uint32_t *sk, *sc, *ss;       // exclusive scans
+  const uint32_t *tot;                // totals [keep, clone, split]
+  const float* wgs;                   // world_grad_sum [n][3]
+  const double* normals;              // [n_split][2][3]
+  double log_split;
+  float *np_, *nm, *nv;
+};
+
+__device__ __forceinline__ void copy_row(const ApplyArgs& a, long long src, long long dst, bool moments) {
+  for (int f = 0; f < kFields; ++f) {
+    const int w = a.L.width[f];
+    const float* ps = a.p + a.L.off[f] + src * w;
+    float* pd = a.np_ + a.Ln.off[f] + dst * w;
+    for (int c = 0; c < w; ++c) pd[c] = ps[c];
+    float* md = a.nm + a.Ln.off[f] + dst * w;
+    float* vd = a.nv + a.Ln.off[f] + dst * w;
+    if (moments) {
+      const float* ms = a.m + a.L.off[f] + src * w;
+      const float* vs = a.v + a.L.off[f] + src * w;
+      for (int c = 0; c < w; ++c) md[c] = ms[c], vd[c] = vs[c];
+    } else {
+      for (int c = 0; c < w; ++c) md[c] = 0.f, vd[c] = 0.f;
+    }
+  }
+}
+
+__global__ void k_densify_apply(ApplyArgs a) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const long long n_keep = a.tot[0], n_clone = a.tot[1];
+  if (a.mk[i]) copy_row(a, i, a.sk[i], true);
+  if (a.mc[i]) {
+    // clone nudged half a mean scale against the accumulated gradient
+    const long long d = n_keep + a.sc[i];
+    copy_row(a, i, d, false);
+    const double gx = a.wgs[3 * i], gy = a.wgs[3 * i + 1], gz = a.wgs[3 * i + 2];
+    const double nrm = sqrt(gx * gx + gy * gy + gz * gz);
+    const float* ls = a.p + a.L.off[2] + 3 * i;
+    const double step = 0.5 * ((det_exp((double)ls[0]) + det_exp((double)ls[1])) + det_exp((double)ls[2])) / 3.0;
+    if (nrm > 0.0) {
+      float* pd = a.np_ + a.Ln.off[0] + 3 * d;
+      const float* ps = a.p + a.L.off[0] + 3 * i;
+      pd[0] = (float)((double)ps[0] - step * (gx / nrm));
+      pd[1] = (float)((double)ps[1] - step * (gy / nrm));
+      pd[2] = (float)((double)ps[2] - step * (gz / nrm));
+    }
+  }
+  if (a.ms[i]) {
+    // two children sampling the parent's own distribution: mu + R (z * s)
+    const long long k = a.ss[i];
+    const long long d0 = n_keep + n_clone + 2 * k;
+    double r[9];
+    rot_of(a.p + a.L.off[1] + 4 * i, r);
+    const float* ls = a.p + a.L.off[2] + 3 * i;
+    const double s[3] = {det_exp((double)ls[0]), det_exp((double)ls[1]), det_exp((double)ls[2])};
+    const float* ps = a.p + a.L.off[0] + 3 * i;
+    for (int c = 0; c < 2; ++c) {
+      const long long d = d0 + c;
+      copy_row(a, i, d, false);
+      const double* z = a.normals + 6 * k + 3 * c;
+      const double lz[3] = {z[0] * s[0], z[1] * s[1], z[2] * s[2]};
+      float* pd = a.np_ + a.Ln.off[0] + 3 * d;
+      for (int row = 0; row < 3; ++row) {
+        const double off = (r[3 * row] * lz[0] + r[3 * row + 1] * lz[1]) + r[3 * row + 2] * lz[2];
+        pd[row] = (float)((double)ps[row] + off);
+      }
+      float* ld = a.np_ + a.Ln.off[2] + 3 * d;
+      for (int q = 0; q < 3; ++q) ld[q] = (float)((double)ls[q] - a.log_split);
+    }
+  }
+}
+
+__global__ void k_totals(const uint32_t* sk, const uint32_t* mk, const uint32_t* sc, const uint32_t* mc,
+                         const uint32_t* ss, const uint32_t* ms, long long n, uint32_t* tot) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    tot[0] = sk[n - 1] + mk[n - 1];
+    tot[1] = sc[n - 1] + mc[n - 1];
+    tot[2] = ss[n - 1] + ms[n - 1];
+  }
+}
+
+}  // namespace
+}  // namespace xg
+
+using namespace xg;
+
+extern "C" {
+
+xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,
+                  int32_t n_features, const double* lr, double beta1, double beta2, double eps,
+                  double bc1, double bc2, const uint32_t* counters, void* stream) {
+  if (!params || !grads || !exp_avg || !exp_avg_sq || !lr || n < 1 || n_features < 1) {
+    set_error_msg("xg_adam: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  AdamArgs a;
+  a.p = params;
+  a.g = grads;
+  a.m = exp_avg;
+  a.v = exp_avg_sq;
+  a.n = n;
+  a.L = make_layout(n, n_features);
+  for (int f = 0; f < kFields; ++f) a.lr[f] = lr[f];
+  a.b1 = beta1;
+  a.b2 = beta2;
+  a.eps = eps;
+  a.bc1 = bc1;
+  a.bc2 = bc2;
+  a.counters = counters;
+  k_adam<<<div_up(n, 128), 128, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("k_adam");
+}
+
+xg_status xg_densify_mark(const float* params, int64_t n, int32_t n_features, const float* norm_sum,
+                          const int32_t* obs_count, double grad_threshold, double size_threshold,
+                          double prune_opacity, uint8_t* flags, uint32_t* counts, void* stream) {
+  if (!params || !norm_sum || !obs_count || !flags || !counts || n < 1) {
+    set_error_msg("xg_densify_mark: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(counts, 0, 4 * sizeof(uint32_t), s);
+  k_densify_mark<<<div_up(n, 128), 128, 0, s>>>(params, n, make_layout(n, n_features), norm_sum,
+                                                obs_count, grad_threshold, size_threshold,
+                                                prune_opacity, flags, counts);
+  return check_launch("k_densify_mark");
+}
+
+xg_status xg_densify_apply(const float* params, const float* exp_avg, const float* exp_avg_sq,
+                           int64_t n, int32_t n_features, const uint8_t* flags,
+                           const float* world_grad_sum, const double* split_normals,
+                           double log_split_factor, int32_t allow_growth, float* new_params,
+                           float* new_exp_avg, float* new_exp_avg_sq, int64_t n_new,
+                           uint32_t* scratch, void* stream) {
+  if (!params || !exp_avg || !exp_avg_sq || !flags || !world_grad_sum || !new_params ||
+      !new_exp_avg || !new_exp_avg_sq || !scratch || n < 1 || n_new < 1) {
+    set_error_msg("xg_densify_apply: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // scratch layout: 3 masks, 3 scans (n each), 3 totals, then scan workspace
+  uint32_t* mk = scratch;
+  uint32_t* mc = mk + n;
+  uint32_t* ms = mc + n;
+  uint32_t* sk = ms + n;
+  uint32_t* sc = sk + n;
+  uint32_t* ss = sc + n;
+  uint32_t* tot = ss + n;
+  void* sws = (void*)(((uintptr_t)(tot + 4) + 255) & ~(uintptr_t)255);
+  const size_t sws_bytes = scan_workspace_bytes(n);
+  k_class_masks<<<div_up(n, 256), 256, 0, s>>>(flags, n, allow_growth, mk, mc, ms);
+  xg_status st = check_launch("k_class_masks");
+  if (st != XG_OK) return st;
+  if ((st = scan_u32(mk, nullptr, sk, n, nullptr, n, nullptr, sws, sws_bytes, s)) != XG_OK) return st;
+  if ((st = scan_u32(mc, nullptr, sc, n, nullptr, n, nullptr, sws, sws_bytes, s)) != XG_OK) return st;
+  if ((st = scan_u32(ms, nullptr, ss, n, nullptr, n, nullptr, sws, sws_bytes, s)) != XG_OK) return st;
+  k_totals<<<1, 32, 0, s>>>(sk, mk, sc, mc, ss, ms, n, tot);
+  ApplyArgs a;
+  a.p = params;
+  a.m = exp_avg;
+  a.v = exp_avg_sq;
+  a.n = n;
+  a.n_new = n_new;
+  a.L = make_layout(n, n_features);
+  a.Ln = make_layout(n_new, n_features);
+  a.mk = mk; a.mc = mc; a.ms = ms;
+  a.sk = sk; a.sc = sc; a.ss = ss;
+  a.tot = tot;
+  a.wgs = world_grad_sum;
+  a.normals = split_normals;
+  a.log_split = log_split_factor;
+  a.np_ = new_params;
+  a.nm = new_exp_avg;
+  a.nv = new_exp_avg_sq;
+  k_densify_apply<<<div_up(n, 128), 128, 0, s>>>(a);
+  return check_launch("k_densify_apply");
+}
+
+}  // extern "C"

@@ -1,0 +1,27 @@
+// Device-wide primitives used by binning and density control (internal).
+#pragma once
+#include "xg_internal.cuh"
+
+namespace xg {
+
+// Exclusive prefix sum of uint32 (optionally gathered: x[i] = in[gather[i]]).
+// The item count is read on the device from *n_dev when n_dev != nullptr
+// (else n_host); grids are sized for `cap`.  If total != nullptr the sum is
+// written there (device).  Single pass, decoupled look-back.
+size_t scan_workspace_bytes(int64_t cap);
+xg_status scan_u32(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64_t cap,
+                   const uint32_t* n_dev, int64_t n_host, uint32_t* total, void* ws, size_t ws_bytes,
+                   cudaStream_t s);
+
+// Stable LSD radix sort of (key, value) uint32 pairs over key bits
+// [begin_bit, end_bit).  Input in keys[0]/vals[0]; the result ends in
+// keys[*result]/vals[*result].  Count read on device from *n_dev.
+size_t radix_workspace_bytes(int64_t cap);
+xg_status radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                           int begin_bit, int end_bit, void* ws, size_t ws_bytes, cudaStream_t s,
+                           int* result);
+xg_status radix_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int64_t cap,
+                             const uint32_t* n_dev, int begin_bit, int end_bit, void* ws, size_t ws_bytes,
+                             cudaStream_t s, int* result);
+
+}  // namespace xg

@@ -1,0 +1,184 @@
+"""Per-view device buffers and the stream-ordered call sequence of one render.
+
+``Frame`` owns every buffer one view needs (per-Gaussian screen-space
+records, the sorted entry list, tile ranges, image / final transmittance /
+contributor counts, the binning workspace) and drives the C-ABI:
+
+    xg_preprocess_fwd -> xg_bin_sort -> xg_composite_fwd
+    xg_composite_bwd  -> xg_preprocess_bwd
+
+Nothing here synchronises except :meth:`Frame.read_counters`.  The entry
+buffer is sized from a capacity; an overflow is reported by the device
+status word and the frame is re-binned with the exact size
+(:meth:`Frame.ensure_binned`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as nat
+from .geometry import XgCamera
+
+TILE_SIZE = 16
+
+
+def tile_grid(h: int, w: int) -> tuple[int, int]:
+    return (h + TILE_SIZE - 1) // TILE_SIZE, (w + TILE_SIZE - 1) // TILE_SIZE
+
+
+class Frame:
+    """Device buffers of one view for a cloud of ``n`` Gaussians."""
+
+    def __init__(self, n: int, h: int, w: int, device, entry_capacity: int | None = None,
+                 extras: bool = False):
+        self.n, self.h, self.w = int(n), int(h), int(w)
+        self.device = torch.device(device)
+        nty, ntx = tile_grid(h, w)
+        self.n_tiles = ntx * nty
+        dev = self.device
+        self.mean2d = torch.empty((n, 2), dtype=torch.float64, device=dev)
+        self.coef = torch.empty((n, 4), dtype=torch.float32, device=dev)
+        self.inten = torch.empty(n, dtype=torch.float32, device=dev)
+        self.rect = torch.empty((n, 4), dtype=torch.int16, device=dev)
+        self.tiles_touched = torch.empty(n, dtype=torch.int32, device=dev)
+        self.depth_key = torch.empty(n, dtype=torch.int64, device=dev)
+        self.order = torch.empty(n, dtype=torch.int32, device=dev)
+        self.tile_ranges = torch.empty((self.n_tiles, 2), dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(nat.XG_NCOUNTERS, dtype=torch.int32, device=dev)
+        self.image = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
+        self.extras = None
+        if extras:
+            self.extras = {
+                "cov2d": torch.empty((n, 3), dtype=torch.float64, device=dev),
+                "conic": torch.empty((n, 3), dtype=torch.float64, device=dev),
+                "depth": torch.empty(n, dtype=torch.float64, device=dev),
+                "t_cam": torch.empty((n, 3), dtype=torch.float64, device=dev),
+                "radius": torch.empty(n, dtype=torch.float64, device=dev),
+                "opacity": torch.empty(n, dtype=torch.float64, device=dev),
+            }
+        self.entry_capacity = 0
+        self.entry_splat = None
+        self.workspace = None
+        self.set_capacity(entry_capacity if entry_capacity else max(16 * n, 1024))
+        self.cam = None
+        self.has_forward = False
+
+    def set_capacity(self, cap: int) -> None:
+        cap = int(cap)
+        if cap <= self.entry_capacity and self.entry_splat is not None:
+            return
+        self.entry_capacity = cap
+        self.entry_splat = torch.empty(cap, dtype=torch.int32, device=self.device)
+        ws = nat.lib().xg_bin_workspace_bytes(self.n, cap, self.n_tiles)
+        self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
+
+    def splats_struct(self) -> nat.XgSplats:
+        s = nat.XgSplats()
+        s.mean2d = self.mean2d.data_ptr()
+        s.coef = self.coef.data_ptr()
+        s.inten = self.inten.data_ptr()
+        s.rect = self.rect.data_ptr()
+        s.n_tiles = self.tiles_touched.data_ptr()
+        s.depth_key = self.depth_key.data_ptr()
+        s.order = self.order.data_ptr()
+        s.entry_splat = self.entry_splat.data_ptr()
+        s.tile_ranges = self.tile_ranges.data_ptr()
+        s.counters = self.counters.data_ptr()
+        s.n = self.n
+        s.entry_capacity = self.entry_capacity
+        return s
+
+    # --- stages -------------------------------------------------------------
+    def preprocess(self, cloud, cam: XgCamera) -> None:
+        if cloud.n_points != self.n:
+            raise ValueError("frame was allocated for a different cloud size")
+        self.cam = cam
+        cs = nat.cloud_struct(cloud)
+        sp = self.splats_struct()
+        ex = None
+        if self.extras is not None:
+            ex = nat.XgSplatExtras(**{k: v.data_ptr() for k, v in self.extras.items()})
+        nat.check(
+            nat.lib().xg_preprocess_fwd(
+                ctypes.byref(cs), ctypes.byref(cam), ctypes.byref(sp),
+                ctypes.byref(ex) if ex is not None else None, nat.stream(),
+            ),
+            "xg_preprocess_fwd",
+        )
+        self.has_forward = False
+
+    def bin(self) -> None:
+        sp = self.splats_struct()
+        nat.check(
+            nat.lib().xg_bin_sort(
+                ctypes.byref(self.cam), ctypes.byref(sp), self.workspace.data_ptr(),
+                self.workspace.numel(), nat.stream(),
+            ),
+            "xg_bin_sort",
+        )
+
+    def composite(self, target: torch.Tensor | None = None, l1_sum: torch.Tensor | None = None) -> None:
+        sp = self.splats_struct()
+        nat.check(
+            nat.lib().xg_composite_fwd(
+                ctypes.byref(self.cam), ctypes.byref(sp), self.image.data_ptr(),
+                self.t_final.data_ptr(), self.n_contrib.data_ptr(), nat.ptr(target, "target"),
+                nat.ptr(l1_sum, "l1_sum"), nat.stream(),
+            ),
+            "xg_composite_fwd",
+        )
+        self.has_forward = True
+
+    def read_counters(self) -> tuple[int, int, int]:
+        c = self.counters.cpu()
+        return int(c[nat.XG_CTR_ACTIVE]), int(c[nat.XG_CTR_ENTRIES]), int(c[nat.XG_CTR_STATUS]) & 0xFFFFFFFF
+
+    def ensure_binned(self, check_status: bool = True) -> tuple[int, int, int]:
+        """bin(), then one sync to read (active, entries, status); re-bin with
+        the exact capacity if the entry buffer overflowed."""
+        self.bin()
+        active, entries, status = self.read_counters()
+        if check_status:
+            nat.raise_for_status(status & ~nat.XG_ST_ENTRY_OVERFLOW)
+        if entries > self.entry_capacity:
+            self.set_capacity(int(entries * 1.25) + 1024)
+            self.counters[nat.XG_CTR_STATUS] = status & ~nat.XG_ST_ENTRY_OVERFLOW
+            self.bin()
+            active, entries, status = self.read_counters()
+        return active, entries, status
+
+    def backward(self, cloud, grad_acc: torch.Tensor, grads_flat: torch.Tensor, screen_norms, visible,
+                 dl_dimage: torch.Tensor | None = None, target: torch.Tensor | None = None,
+                 l1_scale: float = 0.0, stats=None, kernel_grads=None) -> None:
+        sp = self.splats_struct()
+        grad_acc.zero_()
+        nat.check(
+            nat.lib().xg_composite_bwd(
+                ctypes.byref(self.cam), ctypes.byref(sp), self.t_final.data_ptr(),
+                self.n_contrib.data_ptr(), nat.ptr(dl_dimage, "dl_dimage"),
+                self.image.data_ptr() if dl_dimage is None else None,
+                nat.ptr(target, "target") if dl_dimage is None else None,
+                ctypes.c_float(l1_scale), grad_acc.data_ptr(), nat.stream(),
+            ),
+            "xg_composite_bwd",
+        )
+        cs = nat.cloud_struct(cloud)
+        ns = oc = wg = None
+        if stats is not None:
+            ns, oc, wg = stats.norm_sum.data_ptr(), stats.obs_count.data_ptr(), stats.world_grad_sum.data_ptr()
+        km = kc = ki = ka = None
+        if kernel_grads is not None:
+            km, kc, ki, ka = (kernel_grads[k].data_ptr() for k in ("g_mean", "g_conic", "g_int", "g_alpha"))
+        nat.check(
+            nat.lib().xg_preprocess_bwd(
+                ctypes.byref(cs), ctypes.byref(self.cam), ctypes.byref(sp), grad_acc.data_ptr(),
+                grads_flat.data_ptr(), nat.ptr(screen_norms), nat.ptr(visible), ns, oc, wg, km, kc, ki,
+                ka, nat.stream(),
+            ),
+            "xg_preprocess_bwd",
+        )

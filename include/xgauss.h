@@ -131,6 +131,8 @@ typedef struct xg_splat_extras {
 
 int32_t xg_abi_version(void);
 const char* xg_last_error(void);
+/* Running count of kernels this library has launched (process-wide). */
+uint64_t xg_kernel_launches(void);
 
 /* Tile grid of a camera. */
 int32_t xg_tiles_x(const xg_camera* cam);

@@ -72,6 +72,7 @@ class XgSplatExtras(ctypes.Structure):
 SIGNATURES = {
     "xg_abi_version": (c_i32, []),
     "xg_last_error": (ctypes.c_char_p, []),
+    "xg_kernel_launches": (ctypes.c_uint64, []),
     "xg_tiles_x": (c_i32, [c_void_p]),
     "xg_tiles_y": (c_i32, [c_void_p]),
     "xg_bin_workspace_bytes": (c_size, [c_i64, c_i64, c_i32]),
@@ -205,6 +206,10 @@ def raise_for_status(word: int, where: str = "") -> None:
         for f, name in enumerate(PARAM_FIELDS):
             if grad & (1 << f):
                 raise TrainingDivergenceError(name)
+
+
+def kernel_launches() -> int:
+    return int(lib().xg_kernel_launches())
 
 
 def intensities(cloud) -> torch.Tensor:

@@ -19,8 +19,12 @@ constexpr float kClamp = (float)XG_SIGMA_CLAMP;
 // Remember the last error for xg_last_error().
 void set_error(const char* what, cudaError_t err);
 void set_error_msg(const char* what);
+void note_launch();
 
+// Called once after every kernel launch: error check + launch accounting
+// (xg_kernel_launches(), used by bench.py's gpu_launches).
 inline xg_status check_launch(const char* what) {
+  note_launch();
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
     set_error(what, err);

@@ -122,11 +122,15 @@ class Frame:
             "xg_bin_sort",
         )
 
-    def composite(self, target: torch.Tensor | None = None, l1_sum: torch.Tensor | None = None) -> None:
+    def composite(self, target: torch.Tensor | None = None, l1_sum: torch.Tensor | None = None,
+                  image_out: torch.Tensor | None = None) -> None:
+        """K3.  ``image_out`` (float32 [H, W], contiguous) receives the image
+        instead of the frame's own buffer (e.g. a slot of a sweep stack)."""
         sp = self.splats_struct()
+        img = self.image if image_out is None else image_out
         nat.check(
             nat.lib().xg_composite_fwd(
-                ctypes.byref(self.cam), ctypes.byref(sp), self.image.data_ptr(),
+                ctypes.byref(self.cam), ctypes.byref(sp), img.data_ptr(),
                 self.t_final.data_ptr(), self.n_contrib.data_ptr(), nat.ptr(target, "target"),
                 nat.ptr(l1_sum, "l1_sum"), nat.stream(),
             ),

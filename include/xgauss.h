@@ -62,6 +62,7 @@ typedef enum xg_status {
 #define XG_CTR_ENTRIES  1   /* (tile, splat) entries (may exceed capacity)    */
 #define XG_CTR_STATUS   2   /* status bits above                              */
 #define XG_CTR_TOUCH    3   /* scratch                                        */
+#define XG_CTR_STICKY   4   /* caller-owned, never reset by the library       */
 #define XG_NCOUNTERS    8
 
 /* Blend constants (rasterizer/kernels_py.py:13-19, frontend.py:36,
@@ -143,7 +144,8 @@ size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles
 
 /* K1: per-Gaussian projection (float64 arithmetic), writes mean2d, coef,
  * inten, rect, n_tiles, depth_key, counters[ACTIVE], status bits.
- * Resets counters[] first.  extras may be NULL. */
+ * Resets counters[0..3] first (counters[4..7] are left to the caller).
+ * extras may be NULL. */
 xg_status xg_preprocess_fwd(const xg_cloud* cloud, const xg_camera* cam, xg_splats* sp,
                             const xg_splat_extras* extras, void* stream);
 
@@ -194,12 +196,12 @@ xg_status xg_check_finite(const float* grads, int64_t n, int32_t n_features, uin
 /* K4c: fused Adam over all fields + quaternion renormalisation, in place.
  * lr[5] per field (positions, rotations, log_scales, raw_opacities,
  * features).  bc1 = 1-beta1^t, bc2 = 1-beta2^t.  Honours the non-finite bits
- * in counters[STATUS] with the reference's partial-update semantics: fields
- * before the first non-finite one are updated, the rest (and the renorm)
- * are not. */
+ * in the device word *status (if non-NULL) with the reference's
+ * partial-update semantics: fields before the first non-finite one are
+ * updated, the rest (and the renorm) are not.  lr is HOST memory. */
 xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq,
                   int64_t n, int32_t n_features, const double* lr, double beta1, double beta2,
-                  double eps, double bc1, double bc2, const uint32_t* counters, void* stream);
+                  double eps, double bc1, double bc2, const uint32_t* status, void* stream);
 
 /* K4d (1): density-control masks.  flags[N] bit0 high-gradient, bit1 large,
  * bit2 prune, bit3 clone, bit4 split; counts[4] = {prune, clone, split, keep}

@@ -47,13 +47,13 @@ struct AdamArgs {
   Layout L;
   double lr[kFields];
   double b1, b2, eps, bc1, bc2;
-  const uint32_t* counters;
+  const uint32_t* status;
 };
 
 __global__ void k_adam(AdamArgs a) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  const uint32_t bad = a.counters ? (a.counters[XG_CTR_STATUS] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f : 0u;
+  const uint32_t bad = a.status ? (a.status[0] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f : 0u;
   for (int f = 0; f < kFields; ++f) {
     if (bad & ((2u << f) - 1u)) return;  // a field <= f diverged: stop (reference raises here)
     const long long base = a.L.off[f] + i * a.L.width[f];
@@ -229,7 +229,7 @@ extern "C" {
 
 xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,
                   int32_t n_features, const double* lr, double beta1, double beta2, double eps,
-                  double bc1, double bc2, const uint32_t* counters, void* stream) {
+                  double bc1, double bc2, const uint32_t* status, void* stream) {
   if (!params || !grads || !exp_avg || !exp_avg_sq || !lr || n < 1 || n_features < 1) {
     set_error_msg("xg_adam: invalid argument");
     return XG_ERR_INVALID;
@@ -247,7 +247,7 @@ xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_
   a.eps = eps;
   a.bc1 = bc1;
   a.bc2 = bc2;
-  a.counters = counters;
+  a.status = status;
   k_adam<<<div_up(n, 128), 128, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_adam");
 }

@@ -452,7 +452,7 @@ xg_status xg_preprocess_fwd(const xg_cloud* cloud, const xg_camera* cam, xg_spla
     return XG_ERR_INVALID;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  cudaMemsetAsync(sp->counters, 0, XG_NCOUNTERS * sizeof(uint32_t), s);
+  cudaMemsetAsync(sp->counters, 0, XG_CTR_STICKY * sizeof(uint32_t), s);
   xg_splat_extras ex = {};
   if (extras) ex = *extras;
   const int block = 128;

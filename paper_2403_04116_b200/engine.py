@@ -139,12 +139,14 @@ class Frame:
         self.has_forward = True
 
     def read_counters(self) -> tuple[int, int, int]:
-        c = self.counters.cpu()
-        return int(c[nat.XG_CTR_ACTIVE]), int(c[nat.XG_CTR_ENTRIES]), int(c[nat.XG_CTR_STATUS]) & 0xFFFFFFFF
+        c = self.counters.cpu().numpy().astype("int64") & 0xFFFFFFFF
+        self.last_counters = c
+        return int(c[nat.XG_CTR_ACTIVE]), int(c[nat.XG_CTR_ENTRIES]), int(c[nat.XG_CTR_STATUS])
 
     def ensure_binned(self, check_status: bool = True) -> tuple[int, int, int]:
         """bin(), then one sync to read (active, entries, status); re-bin with
-        the exact capacity if the entry buffer overflowed."""
+        the exact capacity if the entry buffer overflowed.  All eight
+        counters read are kept in ``last_counters``."""
         self.bin()
         active, entries, status = self.read_counters()
         if check_status:

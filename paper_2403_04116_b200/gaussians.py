@@ -136,7 +136,7 @@ class RadiativeGaussian:
 def _as_f32(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.detach().to(device=device, dtype=torch.float32)
-    return torch.as_tensor(np.asarray(x, dtype=np.float64), dtype=torch.float32, device=device)
+    return torch.as_tensor(np.array(x, dtype=np.float64), dtype=torch.float32, device=device)
 
 
 class GaussianCloud:

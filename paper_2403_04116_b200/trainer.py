@@ -325,111 +325,154 @@ class _IterationEngine:
         self.vis = torch.empty(n, dtype=torch.uint8, device=cloud.device)
 
 
+class Trainer:
+    """The train loop of trainer.py:330-438 as a resumable object: ``step()``
+    runs one iteration; ``run()`` runs to ``cfg.iterations``.  ``train()``
+    is ``Trainer(...).run()``."""
+
+    def __init__(self, dataset: ProjectionSet, cloud: GaussianCloud, cfg: TrainConfig, out_dir=None,
+                 verbose: bool = False, targets_on_host: bool = False):
+        if dataset.train_indices.size < 1:
+            raise InvalidParameterError("dataset has no training projections")
+        nat.require_cuda(cloud.flat, "cloud")
+        self.dataset, self.cfg, self.verbose = dataset, cfg, verbose
+        self.cloud = cloud.copy()
+        self.dev = dev = self.cloud.device
+        self.state = OptimizerState(self.cloud)
+        self.rng = np.random.default_rng(cfg.rng_seed)
+        self.stats = DensifyStats.zeros(self.cloud.n_points, dev)
+        pos = self.cloud.positions
+        span = float((pos.max(0).values - pos.min(0).values).max())
+        self.size_threshold = (cfg.densify_size_threshold if cfg.densify_size_threshold is not None
+                               else 0.01 * max(span, 1.0))
+        sc = dataset.scanner
+        intr = intrinsic_from_config(sc)
+        self.h, self.w = h, w = sc.detector_height, sc.detector_width
+        self.cams = {int(i): camera_pod(extrinsic_from_angle(sc, float(dataset.angles[i])), intr, (h, w))
+                     for i in dataset.train_indices}
+        # targets resident in HBM (default), or kept in pinned host memory and
+        # copied per iteration (end-to-end measurement)
+        self.targets_on_host = targets_on_host
+        if targets_on_host:
+            self.targets = {int(i): torch.as_tensor(dataset.images[i], dtype=torch.float32).pin_memory()
+                            for i in dataset.train_indices}
+            self.tgt_dev = torch.empty((h, w), dtype=torch.float32, device=dev)
+            self.loss_host = torch.zeros(1, dtype=torch.float64).pin_memory()
+        else:
+            self.targets = {int(i): torch.as_tensor(dataset.images[i], dtype=torch.float32, device=dev).contiguous()
+                            for i in dataset.train_indices}
+        self.out_path = Path(out_dir) if out_dir is not None else None
+        self.log = None
+        if self.out_path is not None:
+            self.out_path.mkdir(parents=True, exist_ok=True)
+            self.log = open(self.out_path / "metrics.tsv", "w")
+            self.log.write(METRICS_HEADER)
+        self.eng = _IterationEngine(self.cloud, h, w)
+        self.metrics: list = []
+        self.order: list = []
+        self.it = 0
+        self.t0 = time.perf_counter()
+        self.grad_mask = 0x1F << nat.XG_ST_GRAD_SHIFT
+        self.densify_events = 0
+
+    def step(self) -> None:
+        cfg, eng = self.cfg, self.eng
+        self.it += 1
+        it = self.it
+        h, w = self.h, self.w
+        if not self.order:
+            self.order = [int(i) for i in self.rng.permutation(self.dataset.train_indices)]
+        view = self.order.pop()
+        fr = eng.frame
+        fr.preprocess(self.cloud, self.cams[view])
+        fr.ensure_binned(check_status=False)
+        c = fr.last_counters
+        nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))  # divergence of the previous step
+        nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
+        if self.targets_on_host:
+            self.tgt_dev.copy_(self.targets[view], non_blocking=True)
+            tgt = self.tgt_dev
+        else:
+            tgt = self.targets[view]
+        eng.l1.zero_()
+        fr.composite(target=tgt, l1_sum=eng.l1)
+        if self.targets_on_host:
+            self.loss_host.copy_(eng.l1, non_blocking=True)  # the step's scalar result, to the host
+        value = None
+        if cfg.gamma == 0.0:
+            fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
+                        l1_scale=1.0 / (h * w), stats=self.stats)
+        else:
+            value, dl = loss(fr.image, tgt, cfg.gamma)
+            fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis,
+                        dl_dimage=dl.float().contiguous(), stats=self.stats)
+        # carry this step's non-finite flags into the sticky word Adam reads
+        fr.counters[nat.XG_CTR_STICKY : nat.XG_CTR_STICKY + 1].bitwise_or_(
+            fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1] & self.grad_mask)
+        lr_table = {"positions": position_learning_rate(cfg, it - 1), "rotations": cfg.lr_rotation,
+                    "log_scales": cfg.lr_scaling, "raw_opacities": cfg.lr_opacity, "features": cfg.lr_feature}
+        self.state.step += 1
+        _adam_launch(self.cloud, eng.grads.flat, self.state, lr_table, cfg,
+                     fr.counters.data_ptr() + 4 * nat.XG_CTR_STICKY)
+
+        densify_now = cfg.densify_from_iter < it <= cfg.densify_until_iter and it % cfg.densify_interval == 0
+        log_now = it % cfg.log_interval == 0 or it == cfg.iterations
+        ckpt_now = self.out_path is not None and it in cfg.checkpoint_iterations
+        if densify_now or log_now or ckpt_now or it == cfg.iterations:
+            nat.raise_for_status(int(fr.counters[nat.XG_CTR_STICKY].item()) & 0xFFFFFFFF)
+        if densify_now:
+            self.cloud, self.state, rep = densify_and_prune(self.cloud, self.state, self.stats, cfg,
+                                                            self.size_threshold, self.rng)
+            self.stats = DensifyStats.zeros(self.cloud.n_points, self.dev)
+            eng.resize(self.cloud)
+            self.densify_events += 1
+            if self.verbose:
+                print(f"[{it}] density control: {rep}")
+        if cfg.opacity_reset_interval and it % cfg.opacity_reset_interval == 0:
+            self.cloud.raw_opacities.clamp_(max=logit(0.01))
+            self.state.exp_avg["raw_opacities"].zero_()
+            self.state.exp_avg_sq["raw_opacities"].zero_()
+        if log_now:
+            if value is None:
+                value = float(eng.l1.item()) / (h * w)
+            row = {"iteration": it, "loss": value, "train_psnr": psnr(fr.image, tgt), "test_psnr": None,
+                   "test_ssim": None, "n_points": self.cloud.n_points}
+            if it % cfg.eval_interval == 0 or it == cfg.iterations:
+                rep = evaluate(self.cloud, self.dataset, self.dataset.test_indices)
+                row["test_psnr"], row["test_ssim"] = rep.psnr, rep.ssim
+                if self.verbose:
+                    print(f"[{it}] loss {value:.5f} test PSNR {rep.psnr:.2f} dB SSIM {rep.ssim:.4f} "
+                          f"N {self.cloud.n_points} ({time.perf_counter() - self.t0:.1f}s)")
+            self.metrics.append(row)
+            if self.log is not None:
+                self.log.write(_metrics_row(row))
+                self.log.flush()
+        if ckpt_now:
+            save_cloud(self.cloud, self.out_path / f"ckpt_{it:06d}.ply")
+
+    def close(self) -> None:
+        if self.log is not None:
+            self.log.close()
+            self.log = None
+
+    def run(self) -> TrainResult:
+        try:
+            while self.it < self.cfg.iterations:
+                self.step()
+        finally:
+            self.close()
+        if self.out_path is not None:
+            save_cloud(self.cloud, self.out_path / "cloud_final.ply")
+        return TrainResult(cloud=self.cloud, metrics=self.metrics, out_dir=self.out_path)
+
+
 def train(dataset: ProjectionSet, cloud: GaussianCloud, cfg: TrainConfig, out_dir=None,
           verbose: bool = False) -> TrainResult:
     """Optimise the cloud against the training projections (trainer.py:330-438)."""
-    if dataset.train_indices.size < 1:
-        raise InvalidParameterError("dataset has no training projections")
-    nat.require_cuda(cloud.flat, "cloud")
-    cloud = cloud.copy()
-    dev = cloud.device
-    state = OptimizerState(cloud)
-    rng = np.random.default_rng(cfg.rng_seed)
-    stats = DensifyStats.zeros(cloud.n_points, dev)
-    pos = cloud.positions
-    span = float((pos.max(0).values - pos.min(0).values).max())
-    size_threshold = cfg.densify_size_threshold if cfg.densify_size_threshold is not None else 0.01 * max(span, 1.0)
-    sc = dataset.scanner
-    intr = intrinsic_from_config(sc)
-    h, w = sc.detector_height, sc.detector_width
-    cams = {int(i): camera_pod(extrinsic_from_angle(sc, float(dataset.angles[i])), intr, (h, w))
-            for i in dataset.train_indices}
-    targets = {int(i): torch.as_tensor(dataset.images[i], dtype=torch.float32, device=dev).contiguous()
-               for i in dataset.train_indices}
-    out_path = Path(out_dir) if out_dir is not None else None
-    log = None
-    if out_path is not None:
-        out_path.mkdir(parents=True, exist_ok=True)
-        log = open(out_path / "metrics.tsv", "w")
-        log.write(METRICS_HEADER)
-    eng = _IterationEngine(cloud, h, w)
-    metrics: list = []
-    order: list = []
-    t0 = time.perf_counter()
-    grad_mask = 0x1F << nat.XG_ST_GRAD_SHIFT
-    try:
-        for it in range(1, cfg.iterations + 1):
-            if not order:
-                order = [int(i) for i in rng.permutation(dataset.train_indices)]
-            view = order.pop()
-            fr = eng.frame
-            fr.preprocess(cloud, cams[view])
-            fr.ensure_binned(check_status=False)
-            c = fr.last_counters
-            nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))  # divergence of the previous step
-            nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
-            tgt = targets[view]
-            eng.l1.zero_()
-            fr.composite(target=tgt, l1_sum=eng.l1)
-            if cfg.gamma == 0.0:
-                fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
-                            l1_scale=1.0 / (h * w), stats=stats)
-                value = None
-            else:
-                value, dl = loss(fr.image, tgt, cfg.gamma)
-                fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis,
-                            dl_dimage=dl.float().contiguous(), stats=stats)
-            # carry this step's non-finite flags into the sticky word Adam reads
-            fr.counters[nat.XG_CTR_STICKY : nat.XG_CTR_STICKY + 1].bitwise_or_(
-                fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1] & grad_mask)
-            lr_table = {"positions": position_learning_rate(cfg, it - 1), "rotations": cfg.lr_rotation,
-                        "log_scales": cfg.lr_scaling, "raw_opacities": cfg.lr_opacity,
-                        "features": cfg.lr_feature}
-            state.step += 1
-            _adam_launch(cloud, eng.grads.flat, state, lr_table, cfg,
-                         fr.counters.data_ptr() + 4 * nat.XG_CTR_STICKY)
-
-            densify_now = cfg.densify_from_iter < it <= cfg.densify_until_iter and it % cfg.densify_interval == 0
-            log_now = it % cfg.log_interval == 0 or it == cfg.iterations
-            ckpt_now = out_path is not None and it in cfg.checkpoint_iterations
-            if densify_now or log_now or ckpt_now or it == cfg.iterations:
-                nat.raise_for_status(int(fr.counters[nat.XG_CTR_STICKY].item()) & 0xFFFFFFFF)
-            if densify_now:
-                cloud, state, rep = densify_and_prune(cloud, state, stats, cfg, size_threshold, rng)
-                stats = DensifyStats.zeros(cloud.n_points, dev)
-                eng.resize(cloud)
-                if verbose:
-                    print(f"[{it}] density control: {rep}")
-            if cfg.opacity_reset_interval and it % cfg.opacity_reset_interval == 0:
-                cloud.raw_opacities.clamp_(max=logit(0.01))
-                state.exp_avg["raw_opacities"].zero_()
-                state.exp_avg_sq["raw_opacities"].zero_()
-            if log_now:
-                if value is None:
-                    value = float(eng.l1.item()) / (h * w)
-                row = {"iteration": it, "loss": value, "train_psnr": psnr(fr.image, tgt), "test_psnr": None,
-                       "test_ssim": None, "n_points": cloud.n_points}
-                if it % cfg.eval_interval == 0 or it == cfg.iterations:
-                    rep = evaluate(cloud, dataset, dataset.test_indices)
-                    row["test_psnr"], row["test_ssim"] = rep.psnr, rep.ssim
-                    if verbose:
-                        print(f"[{it}] loss {value:.5f} test PSNR {rep.psnr:.2f} dB SSIM {rep.ssim:.4f} "
-                              f"N {cloud.n_points} ({time.perf_counter() - t0:.1f}s)")
-                metrics.append(row)
-                if log is not None:
-                    log.write(_metrics_row(row))
-                    log.flush()
-            if ckpt_now:
-                save_cloud(cloud, out_path / f"ckpt_{it:06d}.ply")
-    finally:
-        if log is not None:
-            log.close()
-    if out_path is not None:
-        save_cloud(cloud, out_path / "cloud_final.ply")
-    return TrainResult(cloud=cloud, metrics=metrics, out_dir=out_path)
+    return Trainer(dataset, cloud, cfg, out_dir, verbose).run()
 
 
 __all__ = [
-    "PARAM_FIELDS", "DensifyStats", "OptimizerState", "TrainConfig", "TrainResult", "adam_step",
+    "PARAM_FIELDS", "DensifyStats", "OptimizerState", "TrainConfig", "TrainResult", "Trainer", "adam_step",
     "densify_and_prune", "evaluate", "loss", "position_learning_rate", "train", "render",
 ]

@@ -62,7 +62,8 @@ typedef enum xg_status {
 #define XG_CTR_ENTRIES  1   /* (tile, splat) entries (may exceed capacity)    */
 #define XG_CTR_STATUS   2   /* status bits above                              */
 #define XG_CTR_TOUCH    3   /* scratch                                        */
-#define XG_CTR_STICKY   4   /* caller-owned, never reset by the library       */
+#define XG_CTR_STICKY   4   /* caller-owned, never written by the library     */
+#define XG_CTR_QUEUE    5   /* tile work-queue head of the compositing kernels */
 #define XG_NCOUNTERS    8
 
 /* Blend constants (rasterizer/kernels_py.py:13-19, frontend.py:36,
@@ -117,6 +118,9 @@ typedef struct xg_splats {
   uint32_t* counters;     /* [XG_NCOUNTERS]                                 */
   int64_t   n;
   int64_t   entry_capacity;
+  int32_t*  tile_order;   /* [n_tiles_x*n_tiles_y] tiles by descending entry
+                             count (compositing schedule; written by
+                             xg_bin_sort)                                   */
 } xg_splats;
 
 /* Optional float64 API outputs of the projection (frontend.py:58-74); any
@@ -144,7 +148,7 @@ size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles
 
 /* K1: per-Gaussian projection (float64 arithmetic), writes mean2d, coef,
  * inten, rect, n_tiles, depth_key, counters[ACTIVE], status bits.
- * Resets counters[0..3] first (counters[4..7] are left to the caller).
+ * Resets counters[0..3] first (counters[4] is left to the caller).
  * extras may be NULL. */
 xg_status xg_preprocess_fwd(const xg_cloud* cloud, const xg_camera* cam, xg_splats* sp,
                             const xg_splat_extras* extras, void* stream);
@@ -152,7 +156,7 @@ xg_status xg_preprocess_fwd(const xg_cloud* cloud, const xg_camera* cam, xg_spla
 /* K2: depth sort (stable radix over the float64 bits of t_z, index
  * tie-break: the reference's exact order, frontend.py:169), tile
  * duplication (exclusive scan), stable radix sort by tile, tile ranges.
- * Fills order, entry_splat, tile_ranges, counters[ENTRIES]. */
+ * Fills order, entry_splat, tile_ranges, tile_order, counters[ENTRIES]. */
 xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size_t workspace_bytes,
                       void* stream);
 
@@ -166,9 +170,8 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
 /* K4a: reverse replay.  Per-pixel upstream gradient is dl_dimage[H][W], or,
  * when dl_dimage == NULL, the fused L1 gradient l1_scale*sign(image-target).
  * Accumulates (atomically) into grad_acc[N][8]:
- *   {gx, gy, gxx, gxy, gyy, g_int, g_pow, 0}
- * with gx = sum G*(2 A2 dx + B2 dy), gy = sum G*(B2 dx + 2 C2 dy),
- * gxx/gxy/gyy = sum G*dx^2 / dx*dy / dy^2, g_pow = sum G,
+ *   {sum G dx, sum G dy, sum G dx^2, sum G dx dy, sum G dy^2, sum g w, sum G, 0}
+ * over (pixel, entry) pairs, dx = px - mx, w = sigma T, g = dL/dI,
  * G = dL/dsigma * sigma on unclamped pairs (= the reference's g_power).
  * grad_acc must be zeroed by the caller. */
 xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,

@@ -31,7 +31,7 @@ XG_ST_DEGENERATE = 0x2
 XG_ST_NONFINITE_FEAT = 0x4
 XG_ST_ENTRY_OVERFLOW = 0x8
 XG_ST_GRAD_SHIFT = 8
-XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY = 0, 1, 2, 4
+XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
 XG_NCOUNTERS = 8
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
 
@@ -61,6 +61,7 @@ class XgSplats(ctypes.Structure):
         ("counters", c_void_p),
         ("n", c_i64),
         ("entry_capacity", c_i64),
+        ("tile_order", c_void_p),
     ]
 
 

@@ -172,7 +172,9 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   // 5. ranges
   k_tile_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(keys[res], sp->counters, cap, n_tiles,
                                                       (long long*)sp->tile_ranges);
-  return check_launch("k_tile_ranges");
+  if ((st = check_launch("k_tile_ranges")) != XG_OK) return st;
+  if (!sp->tile_order) return XG_OK;
+  return launch_tile_order(sp->tile_ranges, n_tiles, sp->tile_order, s);
 }
 
 }  // extern "C"

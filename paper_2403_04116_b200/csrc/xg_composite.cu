@@ -124,6 +124,9 @@ struct FwdArgs {
   const float* inten;
   const uint32_t* entry;
   const long long* ranges;
+  const int* order;        // tiles, heaviest first
+  uint32_t* work;          // queue head (zeroed before launch)
+  int n_tiles;
   float* image;
   float* t_final;
   int* n_contrib;
@@ -146,64 +149,109 @@ __device__ __forceinline__ void blend(float dy, float bdx, float adx2, const Rec
   last = ok ? krel : last;
 }
 
+// Next tile for this CTA from the heaviest-first queue (-1: queue drained).
+__device__ __forceinline__ int next_tile(const int* order, uint32_t* work, int n_tiles, int* s_tile) {
+  if (threadIdx.x == 0) {
+    const uint32_t k = atomicAdd(work, 1u);
+    *s_tile = k < (uint32_t)n_tiles ? order[k] : -1;
+  }
+  __syncthreads();
+  return *s_tile;
+}
+
+// Persistent CTAs (one wave sized by occupancy) pull tiles from a queue
+// ordered by descending entry count, so the heavy central tiles start first
+// and the tail is made of light tiles (LPT scheduling).
 __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
   __shared__ Rec s_rec[kBatch];
   __shared__ uint8_t s_list[kThreads / 32][kBatch];
   __shared__ float s_l1[kThreads / 32];
-  const int tile = blockIdx.x;
-  const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
+  __shared__ int s_tile;
   const int warp = threadIdx.x >> 5;
-  const long long start = a.ranges[2 * tile], end = a.ranges[2 * tile + 1];
-  float T0 = g.in0 ? 1.f : 0.f, T1 = g.in1 ? 1.f : 0.f;
-  float acc0 = 0.f, acc1 = 0.f;
-  int last0 = -1, last1 = -1;
-  bool warp_alive = __any_sync(0xffffffffu, g.in0 || g.in1);
-  for (long long b0 = start; b0 < end; b0 += kBatch) {
-    stage(s_rec, nullptr, b0 + threadIdx.x, end, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
-    __syncthreads();
-    if (warp_alive) {
-      const int nb = (int)min((long long)kBatch, end - b0);
-      const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
-      const int kbase = (int)(b0 - start);
-      for (int q = 0; q < cnt; ++q) {
-        const int j = s_list[warp][q];
-        const Rec r = s_rec[j];
-        const float dx = __fsub_rn(g.fx, r.a.x);
-        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-        const float bdx = __fmul_rn(r.a.w, dx);
-        blend(__fsub_rn(g.fy0, r.a.y), bdx, adx2, r, kbase + j, T0, acc0, last0);
-        blend(__fsub_rn(g.fy1, r.a.y), bdx, adx2, r, kbase + j, T1, acc1, last1);
+  for (;;) {
+    const int tile = next_tile(a.order, a.work, a.n_tiles, &s_tile);
+    if (tile < 0) break;
+    const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
+    const long long start = a.ranges[2 * tile], end = a.ranges[2 * tile + 1];
+    float T0 = g.in0 ? 1.f : 0.f, T1 = g.in1 ? 1.f : 0.f;
+    float acc0 = 0.f, acc1 = 0.f;
+    int last0 = -1, last1 = -1;
+    bool warp_alive = __any_sync(0xffffffffu, g.in0 || g.in1);
+    for (long long b0 = start; b0 < end; b0 += kBatch) {
+      stage(s_rec, nullptr, b0 + threadIdx.x, end, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
+      __syncthreads();
+      if (warp_alive) {
+        const int nb = (int)min((long long)kBatch, end - b0);
+        const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
+        const int kbase = (int)(b0 - start);
+        for (int q = 0; q < cnt; ++q) {
+          const int j = s_list[warp][q];
+          const Rec r = s_rec[j];
+          const float dx = __fsub_rn(g.fx, r.a.x);
+          const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+          const float bdx = __fmul_rn(r.a.w, dx);
+          blend(__fsub_rn(g.fy0, r.a.y), bdx, adx2, r, kbase + j, T0, acc0, last0);
+          blend(__fsub_rn(g.fy1, r.a.y), bdx, adx2, r, kbase + j, T1, acc1, last1);
+        }
+        warp_alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
       }
-      warp_alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
+      if (!__syncthreads_or(warp_alive)) break;
     }
-    if (!__syncthreads_or(warp_alive)) break;
-  }
-  const long long o0 = (long long)g.py0 * a.w + g.px;
-  float l1 = 0.f;
-  if (g.in0) {
-    a.image[o0] = acc0;
-    if (a.t_final) a.t_final[o0] = T0;
-    if (a.n_contrib) a.n_contrib[o0] = last0 + 1;
-    if (a.target) l1 += fabsf(acc0 - a.target[o0]);
-  }
-  if (g.in1) {
-    const long long o1 = o0 + a.w;
-    a.image[o1] = acc1;
-    if (a.t_final) a.t_final[o1] = T1;
-    if (a.n_contrib) a.n_contrib[o1] = last1 + 1;
-    if (a.target) l1 += fabsf(acc1 - a.target[o1]);
-  }
-  if (a.target && a.l1_sum) {
+    const long long o0 = (long long)g.py0 * a.w + g.px;
+    float l1 = 0.f;
+    if (g.in0) {
+      a.image[o0] = acc0;
+      if (a.t_final) a.t_final[o0] = T0;
+      if (a.n_contrib) a.n_contrib[o0] = last0 + 1;
+      if (a.target) l1 += fabsf(acc0 - a.target[o0]);
+    }
+    if (g.in1) {
+      const long long o1 = o0 + a.w;
+      a.image[o1] = acc1;
+      if (a.t_final) a.t_final[o1] = T1;
+      if (a.n_contrib) a.n_contrib[o1] = last1 + 1;
+      if (a.target) l1 += fabsf(acc1 - a.target[o1]);
+    }
+    if (a.target && a.l1_sum) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-    if ((threadIdx.x & 31) == 0) s_l1[warp] = l1;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) t += (double)s_l1[w];
-      atomicAdd(a.l1_sum, t);
+      for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      if ((threadIdx.x & 31) == 0) s_l1[warp] = l1;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) t += (double)s_l1[w];
+        atomicAdd(a.l1_sum, t);
+      }
+    }
+    __syncthreads();  // s_tile / shared buffers are reused by the next tile
+  }
+}
+
+// Tiles by descending entry count (64 log-spaced buckets; order within a
+// bucket is arbitrary - it only affects scheduling, never results).
+__global__ void __launch_bounds__(1024) k_tile_order(const long long* __restrict__ ranges, int n_tiles,
+                                                     int* __restrict__ order) {
+  constexpr int NB = 64;
+  __shared__ int hist[NB];
+  __shared__ int off[NB];
+  if (threadIdx.x < NB) hist[threadIdx.x] = 0;
+  __syncthreads();
+  auto key = [&](int t) {
+    const long long len = ranges[2 * t + 1] - ranges[2 * t];
+    const int b = len > 0 ? (int)(4.f * __log2f((float)len + 1.f)) : 0;
+    return NB - 1 - min(b, NB - 1);
+  };
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[key(t)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int b = 0; b < NB; ++b) {
+      off[b] = run;
+      run += hist[b];
     }
   }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&off[key(t)], 1)] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -215,6 +263,9 @@ struct BwdArgs {
   const float* inten;
   const uint32_t* entry;
   const long long* ranges;
+  const int* order;
+  uint32_t* work;
+  int n_tiles;
   const float* t_final;
   const int* n_contrib;
   const float* dl;       // upstream dL/dI, or null -> fused L1
@@ -234,30 +285,23 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // Reverse step for one pixel and one entry: the gradient pass of
 // _kernels.pyx:142-177 run back to front, with the suffix sum accumulated
 // directly (no acc - prefix - contrib cancellation) and T restored by
-// division by (1 - sigma).
-__device__ __forceinline__ void unblend(float dy, float bdx, float adx2, float a2dx, float dx,
-                                        const Rec& r, bool act, float g, float& T, float& S,
-                                        float (&acc)[7]) {
+// division by (1 - sigma).  Returns G = dL/dsigma * sigma on unclamped
+// pairs (the reference's g_power) and g * w (the intensity gradient).
+__device__ __forceinline__ void unblend(float dy, float bdx, float adx2, const Rec& r, bool act, float g,
+                                        float& T, float& S, float& G, float& gw) {
   const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
   const float dens = ex2_approx(p2);
   const float sraw = __fmul_rn(r.b.y, dens);
   const bool valid = act & (p2 <= 0.f) & (p2 >= kCut2);
   const bool clamped = sraw >= kClamp;
-  float sg = fminf(sraw, kClamp);
-  sg = valid ? sg : 0.f;
+  const float sg = valid ? fminf(sraw, kClamp) : 0.f;
   const float rc = rcp_approx(1.f - sg);
   const float Tb = T * rc;
   const float w = sg * Tb;
   const float it = r.b.z;
-  const float dsig = g * (it * Tb - S * rc);
-  const float G = (valid && !clamped) ? dsig * sg : 0.f;
-  acc[5] = fmaf(g, w, acc[5]);                 // g_int
-  acc[6] += G;                                 // sum G  (-> g_alpha, g_raw)
-  acc[0] = fmaf(G, fmaf(r.a.w, dy, a2dx), acc[0]);           // G (2A dx + B dy)
-  acc[1] = fmaf(G, fmaf(2.f * r.b.x, dy, bdx), acc[1]);      // G (B dx + 2C dy)
-  acc[2] = fmaf(G, dx * dx, acc[2]);
-  acc[3] = fmaf(G, dx * dy, acc[3]);
-  acc[4] = fmaf(G, dy * dy, acc[4]);
+  gw = g * w;
+  const float dsig = g * fmaf(-S, rc, it * Tb);
+  G = (valid && !clamped) ? dsig * sg : 0.f;
   S = fmaf(it, w, S);
   T = valid ? Tb : T;
 }
@@ -295,91 +339,117 @@ __device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
   return v[0];
 }
 
+// Per-splat accumulators (grad_acc[N][8]), per (pixel, entry) pair with
+// G = dL/dsigma * sigma (unclamped pairs) and w = sigma T:
+//   {sum G dx, sum G dy, sum G dx^2, sum G dx dy, sum G dy^2, sum g w, sum G, 0}
+// xg_preprocess_bwd turns them into the reference's g_mean / g_conic /
+// g_int / g_alpha using the splat's own (A2, B2, C2, alpha).
 __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   __shared__ Rec s_rec[kBatch];
   __shared__ uint32_t s_gid[kBatch];
   __shared__ uint8_t s_list[kThreads / 32][kBatch];
   __shared__ float4 s_acc[kThreads / 32][kBatch][2];
   __shared__ int s_last;
-  const int tile = blockIdx.x;
-  const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
+  __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long start = a.ranges[2 * tile], end = a.ranges[2 * tile + 1];
-  const long long o0 = (long long)g.py0 * a.w + g.px, o1 = o0 + a.w;
-  float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
-  int last0 = -1, last1 = -1;
-  if (g.in0) {
-    T0 = a.t_final[o0];
-    last0 = a.n_contrib[o0] - 1;
-    g0 = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
-  }
-  if (g.in1) {
-    T1 = a.t_final[o1];
-    last1 = a.n_contrib[o1] - 1;
-    g1 = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
-  }
-  if (g0 == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
-  if (g1 == 0.f) last1 = -1;
-  int wl = max(last0, last1);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
-  if (threadIdx.x == 0) s_last = -1;
-  __syncthreads();
-  if (lane == 0) atomicMax(&s_last, wl);
-  __syncthreads();
-  const long long hi = start + s_last + 1;  // one past the last entry any pixel needs
-  float S0 = 0.f, S1 = 0.f;
-  for (long long b1 = hi; b1 > start; b1 -= kBatch) {
-    const long long b0 = b1 - kBatch > start ? b1 - kBatch : start;
-    const int nb = (int)(b1 - b0);
-    stage(s_rec, s_gid, b0 + threadIdx.x, b1, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
-    {
-      float4* z = &s_acc[0][0][0];
-      for (int i = threadIdx.x; i < (kThreads / 32) * kBatch * 2; i += kThreads)
-        z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (;;) {
+    const int tile = next_tile(a.order, a.work, a.n_tiles, &s_tile);
+    if (tile < 0) break;
+    const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
+    const long long start = a.ranges[2 * tile];
+    const long long o0 = (long long)g.py0 * a.w + g.px, o1 = o0 + a.w;
+    float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
+    int last0 = -1, last1 = -1;
+    if (g.in0) {
+      T0 = a.t_final[o0];
+      last0 = a.n_contrib[o0] - 1;
+      g0 = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
     }
+    if (g.in1) {
+      T1 = a.t_final[o1];
+      last1 = a.n_contrib[o1] - 1;
+      g1 = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
+    }
+    if (g0 == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
+    if (g1 == 0.f) last1 = -1;
+    int wl = max(last0, last1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+    if (threadIdx.x == 0) s_last = -1;
     __syncthreads();
-    const int kbase = (int)(b0 - start);
-    if (wl >= kbase) {
-      const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
-      for (int q = cnt - 1; q >= 0; --q) {
-        const int j = s_list[warp][q];
-        const int krel = kbase + j;
-        if (krel > wl) continue;  // warp-uniform
-        const Rec r = s_rec[j];
-        const float dx = __fsub_rn(g.fx, r.a.x);
-        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-        const float bdx = __fmul_rn(r.a.w, dx);
-        const float a2dx = 2.f * r.a.z * dx;
-        float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        unblend(__fsub_rn(g.fy0, r.a.y), bdx, adx2, a2dx, dx, r, krel <= last0, g0, T0, S0, acc);
-        unblend(__fsub_rn(g.fy1, r.a.y), bdx, adx2, a2dx, dx, r, krel <= last1, g1, T1, S1, acc);
-        float v[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], 0.f};
-        const float tot = warp_reduce8(v);
-        if ((lane & 3) == 0) {
-          const int idx = (lane >> 2) & 7;
-          reinterpret_cast<float*>(&s_acc[warp][j][0])[idx] = tot;
+    if (lane == 0) atomicMax(&s_last, wl);
+    __syncthreads();
+    const long long hi = start + s_last + 1;  // one past the last entry any pixel needs
+    float S0 = 0.f, S1 = 0.f;
+    for (long long b1 = hi; b1 > start; b1 -= kBatch) {
+      const long long b0 = b1 - kBatch > start ? b1 - kBatch : start;
+      const int nb = (int)(b1 - b0);
+      stage(s_rec, s_gid, b0 + threadIdx.x, b1, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
+      {
+        float4* z = &s_acc[0][0][0];
+        for (int i = threadIdx.x; i < (kThreads / 32) * kBatch * 2; i += kThreads)
+          z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      __syncthreads();
+      const int kbase = (int)(b0 - start);
+      if (wl >= kbase) {
+        const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
+        for (int q = cnt - 1; q >= 0; --q) {
+          const int j = s_list[warp][q];
+          const int krel = kbase + j;
+          if (krel > wl) continue;  // warp-uniform
+          const Rec r = s_rec[j];
+          const float dx = __fsub_rn(g.fx, r.a.x);
+          const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+          const float bdx = __fmul_rn(r.a.w, dx);
+          const float dy0 = __fsub_rn(g.fy0, r.a.y), dy1 = __fsub_rn(g.fy1, r.a.y);
+          float G0, G1, gw0, gw1;
+          unblend(dy0, bdx, adx2, r, krel <= last0, g0, T0, S0, G0, gw0);
+          unblend(dy1, bdx, adx2, r, krel <= last1, g1, T1, S1, G1, gw1);
+          const float Gs = G0 + G1, gws = gw0 + gw1;
+          if (!__any_sync(0xffffffffu, (Gs != 0.f) | (gws != 0.f))) continue;
+          const float Gdy0 = G0 * dy0, Gdy1 = G1 * dy1;
+          const float Gdys = Gdy0 + Gdy1;
+          float v[8] = {Gs * dx, Gdys, Gs * (dx * dx), Gdys * dx, fmaf(Gdy0, dy0, Gdy1 * dy1), gws, Gs, 0.f};
+          const float tot = warp_reduce8(v);
+          if ((lane & 3) == 0) reinterpret_cast<float*>(&s_acc[warp][j][0])[(lane >> 2) & 7] = tot;
         }
       }
-    }
-    __syncthreads();
-    if (threadIdx.x < nb) {
-      float4 u = s_acc[0][threadIdx.x][0], v = s_acc[0][threadIdx.x][1];
+      __syncthreads();
+      if (threadIdx.x < nb) {
+        float4 u = s_acc[0][threadIdx.x][0], v = s_acc[0][threadIdx.x][1];
 #pragma unroll
-      for (int w = 1; w < kThreads / 32; ++w) {
-        const float4 u2 = s_acc[w][threadIdx.x][0], v2 = s_acc[w][threadIdx.x][1];
-        u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
-        v.x += v2.x; v.y += v2.y; v.z += v2.z;
+        for (int w = 1; w < kThreads / 32; ++w) {
+          const float4 u2 = s_acc[w][threadIdx.x][0], v2 = s_acc[w][threadIdx.x][1];
+          u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
+          v.x += v2.x; v.y += v2.y; v.z += v2.z;
+        }
+        if (u.x != 0.f || u.y != 0.f || u.z != 0.f || u.w != 0.f || v.x != 0.f || v.y != 0.f ||
+            v.z != 0.f) {
+          float* dst = a.grad_acc + 8 * (long long)s_gid[threadIdx.x];
+          red_add_v4(dst, u.x, u.y, u.z, u.w);
+          red_add_v4(dst + 4, v.x, v.y, v.z, 0.f);
+        }
       }
-      if (u.x != 0.f || u.y != 0.f || u.z != 0.f || u.w != 0.f || v.x != 0.f || v.y != 0.f ||
-          v.z != 0.f) {
-        float* dst = a.grad_acc + 8 * (long long)s_gid[threadIdx.x];
-        red_add_v4(dst, u.x, u.y, u.z, u.w);
-        red_add_v4(dst + 4, v.x, v.y, v.z, 0.f);
-      }
+      __syncthreads();
     }
-    __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Launch configuration: one wave of persistent CTAs.
+// ---------------------------------------------------------------------------
+template <typename K>
+int persistent_grid(K kernel, int n_tiles) {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+    cached = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return n_tiles < cached ? n_tiles : cached;
 }
 
 // ---------------------------------------------------------------------------
@@ -406,13 +476,15 @@ __global__ void k_f64_to_f32(const double* a, float* b, long long n) {
   if (i < n) b[i] = (float)a[i];
 }
 
-__global__ void k_acc_to_reference(long long n, const float* acc, const double* opac, double* g_mean,
-                                   double* g_conic, double* g_int, double* g_alpha) {
+__global__ void k_acc_to_reference(long long n, const float* acc, const float4* coef, const double* opac,
+                                   double* g_mean, double* g_conic, double* g_int, double* g_alpha) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float* a = acc + 8 * i;
-  g_mean[2 * i] = -kLn2 * (double)a[0];
-  g_mean[2 * i + 1] = -kLn2 * (double)a[1];
+  const float4 c = coef[i];
+  const double sdx = a[0], sdy = a[1];
+  g_mean[2 * i] = -kLn2 * (2.0 * c.x * sdx + (double)c.y * sdy);
+  g_mean[2 * i + 1] = -kLn2 * ((double)c.y * sdx + 2.0 * c.z * sdy);
   g_conic[3 * i] = -0.5 * (double)a[2];
   g_conic[3 * i + 1] = -(double)a[3];
   g_conic[3 * i + 2] = -0.5 * (double)a[4];
@@ -431,6 +503,8 @@ struct TilesWs {
   int* n_contrib;
   float* dl;
   float* acc;
+  int32_t* order;
+  uint32_t* counters;
 };
 
 size_t tiles_ws(int64_t n, int32_t h, int32_t w, TilesWs* out, char* base) {
@@ -450,11 +524,19 @@ size_t tiles_ws(int64_t n, int32_t h, int32_t w, TilesWs* out, char* base) {
   t.n_contrib = (int*)take(4 * hw);
   t.dl = (float*)take(4 * hw);
   t.acc = (float*)take(32 * (size_t)n);
+  t.order = (int32_t*)take(4 * (size_t)(((w + kTile - 1) / kTile) * ((h + kTile - 1) / kTile)));
+  t.counters = (uint32_t*)take(4 * XG_NCOUNTERS);
   if (out) *out = t;
   return off + 256;
 }
 
 }  // namespace
+
+xg_status launch_tile_order(const int64_t* ranges, int n_tiles, int32_t* order, cudaStream_t s) {
+  k_tile_order<<<1, 1024, 0, s>>>((const long long*)ranges, n_tiles, order);
+  return check_launch("k_tile_order");
+}
+
 }  // namespace xg
 
 using namespace xg;
@@ -468,11 +550,17 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
     set_error_msg("xg_composite_fwd: invalid argument");
     return XG_ERR_INVALID;
   }
-  FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
-            (const long long*)sp->tile_ranges, image, t_final, n_contrib, target, l1_sum,
-            tiles_x(*cam), cam->width, cam->height};
+  if (!sp->tile_order || !sp->counters) {
+    set_error_msg("xg_composite_fwd: tile_order / counters missing (run xg_bin_sort first)");
+    return XG_ERR_INVALID;
+  }
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
-  k_composite_fwd<<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+  uint32_t* work = sp->counters + XG_CTR_QUEUE;
+  cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
+  FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+            (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
+            target, l1_sum, tiles_x(*cam), cam->width, cam->height};
+  k_composite_fwd<<<persistent_grid(k_composite_fwd, n_tiles), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
 }
 
@@ -483,11 +571,17 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
     set_error_msg("xg_composite_bwd: invalid argument");
     return XG_ERR_INVALID;
   }
-  BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
-            (const long long*)sp->tile_ranges, t_final, n_contrib, dl_dimage, image, target,
-            l1_scale, grad_acc, tiles_x(*cam), cam->width, cam->height};
+  if (!sp->tile_order || !sp->counters) {
+    set_error_msg("xg_composite_bwd: tile_order / counters missing (run xg_bin_sort first)");
+    return XG_ERR_INVALID;
+  }
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
-  k_composite_bwd<<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+  uint32_t* work = sp->counters + XG_CTR_QUEUE;
+  cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
+  BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+            (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, t_final, n_contrib, dl_dimage,
+            image, target, l1_scale, grad_acc, tiles_x(*cam), cam->width, cam->height};
+  k_composite_bwd<<<persistent_grid(k_composite_bwd, n_tiles), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
 }
 
@@ -526,7 +620,9 @@ static xg_status tiles_common(int32_t h, int32_t w, const double* means2d, const
   sp.entry_splat = (uint32_t*)entry_splat;
   sp.tile_ranges = (int64_t*)tile_ranges;
   sp.n = n_splats;
-  return XG_OK;
+  sp.tile_order = t.order;
+  sp.counters = t.counters;
+  return launch_tile_order(tile_ranges, tiles_x(cam) * tiles_y(cam), t.order, s);
 }
 
 xg_status xg_forward_tiles(int32_t h, int32_t w, const double* means2d, const double* conics,
@@ -575,8 +671,8 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
   if ((st = xg_composite_bwd(&cam, &sp, t.t_final, t.n_contrib, t.dl, nullptr, nullptr, 0.f, t.acc,
                              stream)) != XG_OK)
     return st;
-  k_acc_to_reference<<<div_up(n_splats, 256), 256, 0, s>>>(n_splats, t.acc, opacities, g_mean, g_conic,
-                                                           g_int, g_alpha);
+  k_acc_to_reference<<<div_up(n_splats, 256), 256, 0, s>>>(n_splats, t.acc, t.coef, opacities, g_mean,
+                                                           g_conic, g_int, g_alpha);
   return check_launch("k_acc_to_reference");
 }
 

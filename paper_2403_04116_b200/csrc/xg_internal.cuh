@@ -33,6 +33,9 @@ inline xg_status check_launch(const char* what) {
   return XG_OK;
 }
 
+// Heaviest-first tile schedule from the tile ranges (xg_composite.cu).
+xg_status launch_tile_order(const int64_t* ranges, int n_tiles, int32_t* order, cudaStream_t s);
+
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 inline int tiles_x(const xg_camera& c) { return (c.width + kTile - 1) / kTile; }

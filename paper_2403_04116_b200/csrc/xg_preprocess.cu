@@ -290,9 +290,13 @@ __global__ void k_preprocess_bwd(CloudPtrs c, Cam k, xg_splats sp, const float* 
       project_one(c, k, i, p);
       const float4 a0 = reinterpret_cast<const float4*>(acc)[2 * i];
       const float4 a1 = reinterpret_cast<const float4*>(acc)[2 * i + 1];
-      // kernel accumulators -> reference kernel outputs (xgauss.h, K4a)
-      const double gmx = -kLn2 * (double)a0.x;
-      const double gmy = -kLn2 * (double)a0.y;
+      // kernel accumulators -> reference kernel outputs (xgauss.h, K4a):
+      // sum G (2 A2 dx + B2 dy) = 2 A2 sum G dx + B2 sum G dy, and the mean
+      // gradient is -ln2 times that (p2 = power * log2 e, dx = px - mx)
+      const float4 cf = reinterpret_cast<const float4*>(sp.coef)[i];
+      const double sdx = a0.x, sdy = a0.y;
+      const double gmx = -kLn2 * (2.0 * (double)cf.x * sdx + (double)cf.y * sdy);
+      const double gmy = -kLn2 * ((double)cf.y * sdx + 2.0 * (double)cf.z * sdy);
       const double gca = -0.5 * (double)a0.z;
       const double gcb = -(double)a0.w;
       const double gcc = -0.5 * (double)a1.x;

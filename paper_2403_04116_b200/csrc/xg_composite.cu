@@ -6,28 +6,33 @@
 //   power < -30; sigma = min(alpha e^power, 0.99); acc += i sigma T;
 //   T *= 1 - sigma.  The pixel centre is the integer lattice point.
 //
-// B200 mapping.  One CTA per 16x16 tile, 4 warps, each warp owns an 8x8
-// sub-block with 2 vertically adjacent pixels per lane (they share dx and
-// the dx-only terms).  Entries are staged 128 at a time into shared memory
-// (one gather per thread: entry id -> 36 B splat record, mean re-based to
-// the tile origin in float64 so dx/dy keep ~1e-6 px precision).  Each warp
-// then culls the staged batch against its own 8x8 sub-block with an exact
-// ellipse/rectangle test (max of the concave log-density over the
-// rectangle vs the -30 cut-off, with margin) and walks only the survivors,
-// so ~half of the (pixel, entry) pairs the reference evaluates are never
-// touched.  Culling never changes results: a culled entry has power < -30
-// on every pixel of the sub-block, which the reference skips too.
+// B200 mapping (warp-centric).  The unit of work is one 8x8 quarter of a
+// 16x16 tile, owned by ONE warp (2 vertically adjacent pixels per lane,
+// sharing dx and the dx-only terms).  Warps are persistent and pull units
+// from a heaviest-tile-first queue, so the load balances at quarter-tile
+// granularity and no warp ever waits for a sibling (no __syncthreads).
+// A warp walks its tile's entry list 32 at a time: each lane gathers one
+// entry's 36 B splat record (mean re-based to the tile origin in float64,
+// so dx/dy keep ~1e-6 px precision), tests it against the warp's 8x8
+// sub-block with an exact ellipse/rectangle bound (max of the concave
+// log-density over the rectangle vs the -30 cut-off, with margin), and the
+// survivors are ballot-compacted into the warp's shared-memory slice; the
+// next batch's gathers are issued before the current batch is blended.
+// Culling never changes results: a culled entry has power < -30 on every
+// pixel of the sub-block, which the reference skips too.
 //
 // Power is evaluated on the log2 scale, p2 = A2 dx^2 + B2 dx dy + C2 dy^2
 // (= power * log2 e) with one MUFU.EX2 per pair; the transmittance update
 // T <- T - sigma T is a single fused multiply-add.
+#include <stdlib.h>
+
 #include "xg_internal.cuh"
 
 namespace xg {
 namespace {
 
-constexpr int kThreads = 128;   // 4 warps per tile
-constexpr int kBatch = 128;     // entries staged per round
+constexpr int kWarps = 8;             // independent warps per CTA
+constexpr int kThreads = 32 * kWarps;
 constexpr float kCullMargin = 0.05f;
 
 struct Rec {
@@ -51,71 +56,95 @@ __device__ __forceinline__ bool overlaps(const Rec& r, float xa, float xb, float
   return fmaxf(p1, p2) >= kCut2 - kCullMargin;
 }
 
-__device__ __forceinline__ void stage(Rec* s_rec, uint32_t* s_gid, long long k, long long end,
-                                      const uint32_t* __restrict__ entry,
-                                      const double2* __restrict__ mean2d,
-                                      const float4* __restrict__ coef,
-                                      const float* __restrict__ inten, double x0, double y0) {
-  const int t = threadIdx.x;
-  if (k < end) {
-    const uint32_t g = __ldg(entry + k);
-    const double2 m = __ldg(mean2d + g);
-    const float4 c = __ldg(coef + g);
-    const float it = __ldg(inten + g);
-    Rec r;
-    r.a = make_float4((float)(m.x - x0), (float)(m.y - y0), c.x, c.y);
-    r.b = make_float4(c.z, c.w, it, 0.f);
-    s_rec[t] = r;
-    if (s_gid) s_gid[t] = g;
-  }
-}
-
-// Compacts this warp's survivors of the staged batch into list (ascending).
-__device__ __forceinline__ int cull_batch(const Rec* s_rec, uint8_t* list, int nb, float xa,
-                                          float xb, float ya, float yb) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  int cnt = 0;
-#pragma unroll
-  for (int r = 0; r < kBatch / 32; ++r) {
-    const int j = r * 32 + lane;
-    const bool keep = j < nb && overlaps(s_rec[j], xa, xb, ya, yb);
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (keep) list[cnt + __popc(bal & lt)] = (uint8_t)j;
-    cnt += __popc(bal);
-  }
-  __syncwarp();
-  return cnt;
-}
-
-struct TileGeom {
-  int x0, y0;
-  int px, py0;     // pixel of this lane (second pixel is py0 + 1)
-  float fx, fy0, fy1;
-  float xa, xb, ya, yb;  // warp sub-block, tile-relative pixel centres
-  bool in0, in1;
+// One lane's gathered entry (raw, before re-basing).
+struct Raw {
+  double2 m;
+  float4 c;
+  float it;
+  uint32_t g;
+  bool valid;
 };
 
-__device__ __forceinline__ TileGeom tile_geom(int tile, int ntx, int w, int h) {
-  TileGeom g;
+__device__ __forceinline__ Raw gather(long long k, long long lo, long long hi,
+                                      const uint32_t* __restrict__ entry,
+                                      const double2* __restrict__ mean2d,
+                                      const float4* __restrict__ coef, const float* __restrict__ inten) {
+  Raw r;
+  r.valid = k >= lo && k < hi;
+  if (r.valid) {
+    r.g = __ldg(entry + k);
+    r.m = __ldg(mean2d + r.g);
+    r.c = __ldg(coef + r.g);
+    r.it = __ldg(inten + r.g);
+  }
+  return r;
+}
+
+// Re-base, cull against the warp's sub-block and ballot-compact the
+// survivors (ascending entry order) into the warp's shared slice.  Returns
+// the survivor count.
+__device__ __forceinline__ int compact(const Raw& raw, int krel, double x0, double y0, float xa, float xb,
+                                       float ya, float yb, Rec* s_rec, int* s_k, uint32_t* s_gid) {
+  Rec r;
+  bool keep = false;
+  if (raw.valid) {
+    r.a = make_float4((float)(raw.m.x - x0), (float)(raw.m.y - y0), raw.c.x, raw.c.y);
+    r.b = make_float4(raw.c.z, raw.c.w, raw.it, 0.f);
+    keep = overlaps(r, xa, xb, ya, yb);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (keep) {
+    const int pos = __popc(bal & lanemask_lt());
+    s_rec[pos] = r;
+    s_k[pos] = krel;
+    if (s_gid) s_gid[pos] = raw.g;
+  }
+  __syncwarp();
+  return __popc(bal);
+}
+
+struct Unit {
+  int x0, y0;            // tile origin
+  int px, py0;           // this lane's pixels (px, py0) and (px, py0 + 1)
+  float fx, fy0, fy1;    // tile-relative pixel centres
+  float xa, xb, ya, yb;  // the warp's 8x8 sub-block (tile-relative)
+  bool in0, in1;
+  long long start, end;
+};
+
+__device__ __forceinline__ Unit make_unit(int tile, int quad, int ntx, int w, int h, const long long* ranges) {
+  Unit u;
   const int tx = tile % ntx, ty = tile / ntx;
-  g.x0 = tx * kTile;
-  g.y0 = ty * kTile;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sx = (warp & 1) * 8, sy = (warp >> 1) * 8;
+  u.x0 = tx * kTile;
+  u.y0 = ty * kTile;
+  const int lane = threadIdx.x & 31;
+  const int sx = (quad & 1) * 8, sy = (quad >> 1) * 8;
   const int lx = sx + (lane & 7), ly = sy + 2 * (lane >> 3);
-  g.px = g.x0 + lx;
-  g.py0 = g.y0 + ly;
-  g.fx = (float)lx;
-  g.fy0 = (float)ly;
-  g.fy1 = (float)(ly + 1);
-  g.xa = (float)sx;
-  g.xb = (float)(sx + 7);
-  g.ya = (float)sy;
-  g.yb = (float)(sy + 7);
-  g.in0 = g.px < w && g.py0 < h;
-  g.in1 = g.px < w && g.py0 + 1 < h;
-  return g;
+  u.px = u.x0 + lx;
+  u.py0 = u.y0 + ly;
+  u.fx = (float)lx;
+  u.fy0 = (float)ly;
+  u.fy1 = (float)(ly + 1);
+  u.xa = (float)sx;
+  u.xb = (float)(sx + 7);
+  u.ya = (float)sy;
+  u.yb = (float)(sy + 7);
+  u.in0 = u.px < w && u.py0 < h;
+  u.in1 = u.px < w && u.py0 + 1 < h;
+  u.start = ranges[2 * tile];
+  u.end = ranges[2 * tile + 1];
+  return u;
+}
+
+// Next (tile, quarter) unit for this warp from the heaviest-first queue.
+__device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int n_tiles, int& tile, int& quad) {
+  uint32_t k = 0;
+  if ((threadIdx.x & 31) == 0) k = atomicAdd(work, 1u);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  if (k >= 4u * (uint32_t)n_tiles) return false;
+  tile = order[k >> 2];
+  quad = (int)(k & 3u);
+  return true;
 }
 
 struct FwdArgs {
@@ -149,63 +178,46 @@ __device__ __forceinline__ void blend(float dy, float bdx, float adx2, const Rec
   last = ok ? krel : last;
 }
 
-// Next tile for this CTA from the heaviest-first queue (-1: queue drained).
-__device__ __forceinline__ int next_tile(const int* order, uint32_t* work, int n_tiles, int* s_tile) {
-  if (threadIdx.x == 0) {
-    const uint32_t k = atomicAdd(work, 1u);
-    *s_tile = k < (uint32_t)n_tiles ? order[k] : -1;
-  }
-  __syncthreads();
-  return *s_tile;
-}
-
-// Persistent CTAs (one wave sized by occupancy) pull tiles from a queue
-// ordered by descending entry count, so the heavy central tiles start first
-// and the tail is made of light tiles (LPT scheduling).
 __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
-  __shared__ Rec s_rec[kBatch];
-  __shared__ uint8_t s_list[kThreads / 32][kBatch];
-  __shared__ float s_l1[kThreads / 32];
-  __shared__ int s_tile;
-  const int warp = threadIdx.x >> 5;
-  for (;;) {
-    const int tile = next_tile(a.order, a.work, a.n_tiles, &s_tile);
-    if (tile < 0) break;
-    const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
-    const long long start = a.ranges[2 * tile], end = a.ranges[2 * tile + 1];
-    float T0 = g.in0 ? 1.f : 0.f, T1 = g.in1 ? 1.f : 0.f;
+  __shared__ Rec s_rec[kWarps][32];
+  __shared__ int s_k[kWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Rec* rec = s_rec[warp];
+  int* kk = s_k[warp];
+  int tile, quad;
+  while (next_unit(a.order, a.work, a.n_tiles, tile, quad)) {
+    const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
+    float T0 = u.in0 ? 1.f : 0.f, T1 = u.in1 ? 1.f : 0.f;
     float acc0 = 0.f, acc1 = 0.f;
     int last0 = -1, last1 = -1;
-    bool warp_alive = __any_sync(0xffffffffu, g.in0 || g.in1);
-    for (long long b0 = start; b0 < end; b0 += kBatch) {
-      stage(s_rec, nullptr, b0 + threadIdx.x, end, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
-      __syncthreads();
-      if (warp_alive) {
-        const int nb = (int)min((long long)kBatch, end - b0);
-        const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
-        const int kbase = (int)(b0 - start);
-        for (int q = 0; q < cnt; ++q) {
-          const int j = s_list[warp][q];
-          const Rec r = s_rec[j];
-          const float dx = __fsub_rn(g.fx, r.a.x);
-          const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-          const float bdx = __fmul_rn(r.a.w, dx);
-          blend(__fsub_rn(g.fy0, r.a.y), bdx, adx2, r, kbase + j, T0, acc0, last0);
-          blend(__fsub_rn(g.fy1, r.a.y), bdx, adx2, r, kbase + j, T1, acc1, last1);
-        }
-        warp_alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
+    bool alive = __any_sync(0xffffffffu, u.in0 || u.in1);
+    Raw nxt = gather(u.start + lane, u.start, u.end, a.entry, a.mean2d, a.coef, a.inten);
+    for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
+      const Raw cur = nxt;
+      const int cnt = compact(cur, (int)(b0 - u.start) + lane, u.x0, u.y0, u.xa, u.xb, u.ya, u.yb, rec, kk,
+                              nullptr);
+      nxt = gather(b0 + 32 + lane, u.start, u.end, a.entry, a.mean2d, a.coef, a.inten);  // prefetch
+      for (int q = 0; q < cnt; ++q) {
+        const Rec r = rec[q];
+        const int krel = kk[q];
+        const float dx = __fsub_rn(u.fx, r.a.x);
+        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+        const float bdx = __fmul_rn(r.a.w, dx);
+        blend(__fsub_rn(u.fy0, r.a.y), bdx, adx2, r, krel, T0, acc0, last0);
+        blend(__fsub_rn(u.fy1, r.a.y), bdx, adx2, r, krel, T1, acc1, last1);
       }
-      if (!__syncthreads_or(warp_alive)) break;
+      __syncwarp();
+      alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
     }
-    const long long o0 = (long long)g.py0 * a.w + g.px;
+    const long long o0 = (long long)u.py0 * a.w + u.px;
     float l1 = 0.f;
-    if (g.in0) {
+    if (u.in0) {
       a.image[o0] = acc0;
       if (a.t_final) a.t_final[o0] = T0;
       if (a.n_contrib) a.n_contrib[o0] = last0 + 1;
       if (a.target) l1 += fabsf(acc0 - a.target[o0]);
     }
-    if (g.in1) {
+    if (u.in1) {
       const long long o1 = o0 + a.w;
       a.image[o1] = acc1;
       if (a.t_final) a.t_final[o1] = T1;
@@ -215,15 +227,8 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
     if (a.target && a.l1_sum) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-      if ((threadIdx.x & 31) == 0) s_l1[warp] = l1;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) t += (double)s_l1[w];
-        atomicAdd(a.l1_sum, t);
-      }
+      if (lane == 0) atomicAdd(a.l1_sum, (double)l1);
     }
-    __syncthreads();  // s_tile / shared buffers are reused by the next tile
   }
 }
 
@@ -343,29 +348,28 @@ __device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
 // G = dL/dsigma * sigma (unclamped pairs) and w = sigma T:
 //   {sum G dx, sum G dy, sum G dx^2, sum G dx dy, sum G dy^2, sum g w, sum G, 0}
 // xg_preprocess_bwd turns them into the reference's g_mean / g_conic /
-// g_int / g_alpha using the splat's own (A2, B2, C2, alpha).
+// g_int / g_alpha using the splat's own (A2, B2, C2, alpha).  Each warp
+// reduces its 64 pixels per splat and issues two vector reductions.
 __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
-  __shared__ Rec s_rec[kBatch];
-  __shared__ uint32_t s_gid[kBatch];
-  __shared__ uint8_t s_list[kThreads / 32][kBatch];
-  __shared__ float4 s_acc[kThreads / 32][kBatch][2];
-  __shared__ int s_last;
-  __shared__ int s_tile;
+  __shared__ Rec s_rec[kWarps][32];
+  __shared__ int s_k[kWarps][32];
+  __shared__ uint32_t s_gid[kWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (;;) {
-    const int tile = next_tile(a.order, a.work, a.n_tiles, &s_tile);
-    if (tile < 0) break;
-    const TileGeom g = tile_geom(tile, a.ntx, a.w, a.h);
-    const long long start = a.ranges[2 * tile];
-    const long long o0 = (long long)g.py0 * a.w + g.px, o1 = o0 + a.w;
+  Rec* rec = s_rec[warp];
+  int* kk = s_k[warp];
+  uint32_t* gid = s_gid[warp];
+  int tile, quad;
+  while (next_unit(a.order, a.work, a.n_tiles, tile, quad)) {
+    const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
+    const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
     float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
     int last0 = -1, last1 = -1;
-    if (g.in0) {
+    if (u.in0) {
       T0 = a.t_final[o0];
       last0 = a.n_contrib[o0] - 1;
       g0 = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
     }
-    if (g.in1) {
+    if (u.in1) {
       T1 = a.t_final[o1];
       last1 = a.n_contrib[o1] - 1;
       g1 = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
@@ -375,63 +379,38 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
     int wl = max(last0, last1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
-    if (threadIdx.x == 0) s_last = -1;
-    __syncthreads();
-    if (lane == 0) atomicMax(&s_last, wl);
-    __syncthreads();
-    const long long hi = start + s_last + 1;  // one past the last entry any pixel needs
+    const long long hi = u.start + wl + 1;  // one past the last entry this warp needs
     float S0 = 0.f, S1 = 0.f;
-    for (long long b1 = hi; b1 > start; b1 -= kBatch) {
-      const long long b0 = b1 - kBatch > start ? b1 - kBatch : start;
-      const int nb = (int)(b1 - b0);
-      stage(s_rec, s_gid, b0 + threadIdx.x, b1, a.entry, a.mean2d, a.coef, a.inten, g.x0, g.y0);
-      {
-        float4* z = &s_acc[0][0][0];
-        for (int i = threadIdx.x; i < (kThreads / 32) * kBatch * 2; i += kThreads)
-          z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // batches of 32 walked back to front: [b1 - 32, b1)
+    Raw nxt = gather(hi - 32 + lane, u.start, hi, a.entry, a.mean2d, a.coef, a.inten);
+    for (long long b1 = hi; b1 > u.start; b1 -= 32) {
+      const Raw cur = nxt;
+      const int cnt = compact(cur, (int)(b1 - 32 - u.start) + lane, u.x0, u.y0, u.xa, u.xb, u.ya, u.yb, rec,
+                              kk, gid);
+      nxt = gather(b1 - 64 + lane, u.start, hi, a.entry, a.mean2d, a.coef, a.inten);  // prefetch
+      for (int q = cnt - 1; q >= 0; --q) {
+        const Rec r = rec[q];
+        const int krel = kk[q];
+        const float dx = __fsub_rn(u.fx, r.a.x);
+        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+        const float bdx = __fmul_rn(r.a.w, dx);
+        const float dy0 = __fsub_rn(u.fy0, r.a.y), dy1 = __fsub_rn(u.fy1, r.a.y);
+        float G0, G1, gw0, gw1;
+        unblend(dy0, bdx, adx2, r, krel <= last0, g0, T0, S0, G0, gw0);
+        unblend(dy1, bdx, adx2, r, krel <= last1, g1, T1, S1, G1, gw1);
+        const float Gs = G0 + G1, gws = gw0 + gw1;
+        if (!__any_sync(0xffffffffu, (Gs != 0.f) | (gws != 0.f))) continue;
+        const float Gdy0 = G0 * dy0, Gdy1 = G1 * dy1;
+        const float Gdys = Gdy0 + Gdy1;
+        float v[8] = {Gs * dx, Gdys, Gs * (dx * dx), Gdys * dx, fmaf(Gdy0, dy0, Gdy1 * dy1), gws, Gs, 0.f};
+        const float tot = warp_reduce8(v);
+        // value i sits in lane 4i: gather 0..3 into lane 0 and 4..7 into lane 16
+        const float t1 = __shfl_down_sync(0xffffffffu, tot, 4);
+        const float t2 = __shfl_down_sync(0xffffffffu, tot, 8);
+        const float t3 = __shfl_down_sync(0xffffffffu, tot, 12);
+        if ((lane & 15) == 0) red_add_v4(a.grad_acc + 8 * (long long)gid[q] + (lane >> 2), tot, t1, t2, t3);
       }
-      __syncthreads();
-      const int kbase = (int)(b0 - start);
-      if (wl >= kbase) {
-        const int cnt = cull_batch(s_rec, s_list[warp], nb, g.xa, g.xb, g.ya, g.yb);
-        for (int q = cnt - 1; q >= 0; --q) {
-          const int j = s_list[warp][q];
-          const int krel = kbase + j;
-          if (krel > wl) continue;  // warp-uniform
-          const Rec r = s_rec[j];
-          const float dx = __fsub_rn(g.fx, r.a.x);
-          const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-          const float bdx = __fmul_rn(r.a.w, dx);
-          const float dy0 = __fsub_rn(g.fy0, r.a.y), dy1 = __fsub_rn(g.fy1, r.a.y);
-          float G0, G1, gw0, gw1;
-          unblend(dy0, bdx, adx2, r, krel <= last0, g0, T0, S0, G0, gw0);
-          unblend(dy1, bdx, adx2, r, krel <= last1, g1, T1, S1, G1, gw1);
-          const float Gs = G0 + G1, gws = gw0 + gw1;
-          if (!__any_sync(0xffffffffu, (Gs != 0.f) | (gws != 0.f))) continue;
-          const float Gdy0 = G0 * dy0, Gdy1 = G1 * dy1;
-          const float Gdys = Gdy0 + Gdy1;
-          float v[8] = {Gs * dx, Gdys, Gs * (dx * dx), Gdys * dx, fmaf(Gdy0, dy0, Gdy1 * dy1), gws, Gs, 0.f};
-          const float tot = warp_reduce8(v);
-          if ((lane & 3) == 0) reinterpret_cast<float*>(&s_acc[warp][j][0])[(lane >> 2) & 7] = tot;
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x < nb) {
-        float4 u = s_acc[0][threadIdx.x][0], v = s_acc[0][threadIdx.x][1];
-#pragma unroll
-        for (int w = 1; w < kThreads / 32; ++w) {
-          const float4 u2 = s_acc[w][threadIdx.x][0], v2 = s_acc[w][threadIdx.x][1];
-          u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
-          v.x += v2.x; v.y += v2.y; v.z += v2.z;
-        }
-        if (u.x != 0.f || u.y != 0.f || u.z != 0.f || u.w != 0.f || v.x != 0.f || v.y != 0.f ||
-            v.z != 0.f) {
-          float* dst = a.grad_acc + 8 * (long long)s_gid[threadIdx.x];
-          red_add_v4(dst, u.x, u.y, u.z, u.w);
-          red_add_v4(dst + 4, v.x, v.y, v.z, 0.f);
-        }
-      }
-      __syncthreads();
+      __syncwarp();
     }
   }
 }
@@ -439,17 +418,19 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
 // ---------------------------------------------------------------------------
 // Launch configuration: one wave of persistent CTAs.
 // ---------------------------------------------------------------------------
+// CTAs per SM: the occupancy limit, or XG_*_CTAS_PER_SM (tuning knob) if set lower.
 template <typename K>
-int persistent_grid(K kernel, int n_tiles) {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-    cached = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  return n_tiles < cached ? n_tiles : cached;
+int persistent_grid(K kernel, int n_units, const char* env) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const char* e = getenv(env);
+  if (e && atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
+  const int grid = sms * per_sm;
+  const int need = (n_units + kWarps - 1) / kWarps;
+  return need < grid ? need : grid;
 }
 
 // ---------------------------------------------------------------------------
@@ -560,7 +541,7 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
   FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
             target, l1_sum, tiles_x(*cam), cam->width, cam->height};
-  k_composite_fwd<<<persistent_grid(k_composite_fwd, n_tiles), kThreads, 0, (cudaStream_t)stream>>>(a);
+  k_composite_fwd<<<persistent_grid(k_composite_fwd, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
 }
 
@@ -581,7 +562,7 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, t_final, n_contrib, dl_dimage,
             image, target, l1_scale, grad_acc, tiles_x(*cam), cam->width, cam->height};
-  k_composite_bwd<<<persistent_grid(k_composite_bwd, n_tiles), kThreads, 0, (cudaStream_t)stream>>>(a);
+  k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
 }
 

@@ -121,11 +121,7 @@ typedef struct xg_splats {
   int32_t*  tile_order;   /* [n_tiles_x*n_tiles_y] tiles by descending entry
                              count (compositing schedule; written by
                              xg_bin_sort)                                   */
-  uint32_t* sched;        /* [XG_SCHED_SLOTS] per-SM work-queue heads of the
-                             compositing kernels (scratch)                  */
 } xg_splats;
-
-#define XG_SCHED_SLOTS 1024
 
 /* Optional float64 API outputs of the projection (frontend.py:58-74); any
  * pointer may be NULL.  All [N]-row, written for active rows only. */

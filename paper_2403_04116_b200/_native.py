@@ -33,7 +33,6 @@ XG_ST_ENTRY_OVERFLOW = 0x8
 XG_ST_GRAD_SHIFT = 8
 XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
 XG_NCOUNTERS = 8
-XG_SCHED_SLOTS = 1024
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
 
 c_void_p = ctypes.c_void_p
@@ -63,7 +62,6 @@ class XgSplats(ctypes.Structure):
         ("n", c_i64),
         ("entry_capacity", c_i64),
         ("tile_order", c_void_p),
-        ("sched", c_void_p),
     ]
 
 

@@ -136,42 +136,15 @@ __device__ __forceinline__ Unit make_unit(int tile, int quad, int ntx, int w, in
   return u;
 }
 
-// Work distribution.  Tiles sorted heaviest-first are dealt to nq per-SM
-// queues in boustrophedon order (round j hands tile j*nq + q, or
-// j*nq + nq-1-q on odd rounds, to queue q), so every SM starts with an
-// even share of heavy and light tiles; each tile is 4 units (its 8x8
-// quarters, kept on one SM for L1 reuse of the splat records).  A warp
-// drains the queue of the SM it runs on, then steals from the others.
-__device__ __forceinline__ unsigned smid() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-
-struct Sched {
-  const int* order;
-  uint32_t* heads;  // [nq]
-  int nq;
-  int n_tiles;
-};
-
-__device__ __forceinline__ bool next_unit(const Sched& sc, int& q, int& tried, int& tile, int& quad) {
-  const int lane = threadIdx.x & 31;
-  while (tried < sc.nq) {
-    uint32_t c = 0;
-    if (lane == 0) c = atomicAdd(sc.heads + q, 1u);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    const uint32_t j = c >> 2;
-    const long long i = (long long)j * sc.nq + ((j & 1u) ? sc.nq - 1 - q : q);
-    if (i < sc.n_tiles) {
-      tile = sc.order[i];
-      quad = (int)(c & 3u);
-      return true;
-    }
-    q = q + 1 == sc.nq ? 0 : q + 1;  // this queue is drained: steal from the next
-    ++tried;
-  }
-  return false;
+// Next (tile, quarter) unit for this warp from the heaviest-first queue.
+__device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int n_tiles, int& tile, int& quad) {
+  uint32_t k = 0;
+  if ((threadIdx.x & 31) == 0) k = atomicAdd(work, 1u);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  if (k >= 4u * (uint32_t)n_tiles) return false;
+  tile = order[k >> 2];
+  quad = (int)(k & 3u);
+  return true;
 }
 
 struct FwdArgs {
@@ -180,7 +153,9 @@ struct FwdArgs {
   const float* inten;
   const uint32_t* entry;
   const long long* ranges;
-  Sched sched;
+  const int* order;        // tiles, heaviest first
+  uint32_t* work;          // queue head (zeroed before launch)
+  int n_tiles;
   float* image;
   float* t_final;
   int* n_contrib;
@@ -203,14 +178,14 @@ __device__ __forceinline__ void blend(float dy, float bdx, float adx2, const Rec
   last = ok ? krel : last;
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_composite_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
   __shared__ Rec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Rec* rec = s_rec[warp];
   int* kk = s_k[warp];
-  int tile, quad, tried = 0, q = (int)(smid() % (unsigned)a.sched.nq);
-  while (next_unit(a.sched, q, tried, tile, quad)) {
+  int tile, quad;
+  while (next_unit(a.order, a.work, a.n_tiles, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     float T0 = u.in0 ? 1.f : 0.f, T1 = u.in1 ? 1.f : 0.f;
     float acc0 = 0.f, acc1 = 0.f;
@@ -293,7 +268,9 @@ struct BwdArgs {
   const float* inten;
   const uint32_t* entry;
   const long long* ranges;
-  Sched sched;
+  const int* order;
+  uint32_t* work;
+  int n_tiles;
   const float* t_final;
   const int* n_contrib;
   const float* dl;       // upstream dL/dI, or null -> fused L1
@@ -373,7 +350,7 @@ __device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
 // xg_preprocess_bwd turns them into the reference's g_mean / g_conic /
 // g_int / g_alpha using the splat's own (A2, B2, C2, alpha).  Each warp
 // reduces its 64 pixels per splat and issues two vector reductions.
-__global__ void __launch_bounds__(kThreads, 3) k_composite_bwd(BwdArgs a) {
+__global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   __shared__ Rec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   __shared__ uint32_t s_gid[kWarps][32];
@@ -381,8 +358,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_composite_bwd(BwdArgs a) {
   Rec* rec = s_rec[warp];
   int* kk = s_k[warp];
   uint32_t* gid = s_gid[warp];
-  int tile, quad, tried = 0, q = (int)(smid() % (unsigned)a.sched.nq);
-  while (next_unit(a.sched, q, tried, tile, quad)) {
+  int tile, quad;
+  while (next_unit(a.order, a.work, a.n_tiles, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
     float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
@@ -441,13 +418,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_composite_bwd(BwdArgs a) {
 // ---------------------------------------------------------------------------
 // Launch configuration: one wave of persistent CTAs.
 // ---------------------------------------------------------------------------
-int sm_count() {
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms > 0 ? (sms < XG_SCHED_SLOTS ? sms : XG_SCHED_SLOTS) : 1;
-}
-
 // CTAs per SM: the occupancy limit, or XG_*_CTAS_PER_SM (tuning knob) if set lower.
 template <typename K>
 int persistent_grid(K kernel, int n_units, const char* env) {
@@ -458,10 +428,9 @@ int persistent_grid(K kernel, int n_units, const char* env) {
   if (per_sm < 1) per_sm = 1;
   const char* e = getenv(env);
   if (e && atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
-  // a full, even wave (every SM drains its own queue); tiny problems launch less
   const int grid = sms * per_sm;
   const int need = (n_units + kWarps - 1) / kWarps;
-  return need < sms ? need : grid;
+  return need < grid ? need : grid;
 }
 
 // ---------------------------------------------------------------------------
@@ -517,7 +486,6 @@ struct TilesWs {
   float* acc;
   int32_t* order;
   uint32_t* counters;
-  uint32_t* sched;
 };
 
 size_t tiles_ws(int64_t n, int32_t h, int32_t w, TilesWs* out, char* base) {
@@ -539,7 +507,6 @@ size_t tiles_ws(int64_t n, int32_t h, int32_t w, TilesWs* out, char* base) {
   t.acc = (float*)take(32 * (size_t)n);
   t.order = (int32_t*)take(4 * (size_t)(((w + kTile - 1) / kTile) * ((h + kTile - 1) / kTile)));
   t.counters = (uint32_t*)take(4 * XG_NCOUNTERS);
-  t.sched = (uint32_t*)take(4 * XG_SCHED_SLOTS);
   if (out) *out = t;
   return off + 256;
 }
@@ -564,15 +531,15 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
     set_error_msg("xg_composite_fwd: invalid argument");
     return XG_ERR_INVALID;
   }
-  if (!sp->tile_order || !sp->sched) {
-    set_error_msg("xg_composite_fwd: tile_order / sched missing (run xg_bin_sort first)");
+  if (!sp->tile_order || !sp->counters) {
+    set_error_msg("xg_composite_fwd: tile_order / counters missing (run xg_bin_sort first)");
     return XG_ERR_INVALID;
   }
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
-  const Sched sc{sp->tile_order, sp->sched, sm_count(), n_tiles};
-  cudaMemsetAsync(sp->sched, 0, sizeof(uint32_t) * sc.nq, (cudaStream_t)stream);
+  uint32_t* work = sp->counters + XG_CTR_QUEUE;
+  cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
   FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
-            (const long long*)sp->tile_ranges, sc, image, t_final, n_contrib,
+            (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
             target, l1_sum, tiles_x(*cam), cam->width, cam->height};
   k_composite_fwd<<<persistent_grid(k_composite_fwd, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
@@ -585,15 +552,15 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
     set_error_msg("xg_composite_bwd: invalid argument");
     return XG_ERR_INVALID;
   }
-  if (!sp->tile_order || !sp->sched) {
-    set_error_msg("xg_composite_bwd: tile_order / sched missing (run xg_bin_sort first)");
+  if (!sp->tile_order || !sp->counters) {
+    set_error_msg("xg_composite_bwd: tile_order / counters missing (run xg_bin_sort first)");
     return XG_ERR_INVALID;
   }
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
-  const Sched sc{sp->tile_order, sp->sched, sm_count(), n_tiles};
-  cudaMemsetAsync(sp->sched, 0, sizeof(uint32_t) * sc.nq, (cudaStream_t)stream);
+  uint32_t* work = sp->counters + XG_CTR_QUEUE;
+  cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
   BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
-            (const long long*)sp->tile_ranges, sc, t_final, n_contrib, dl_dimage,
+            (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, t_final, n_contrib, dl_dimage,
             image, target, l1_scale, grad_acc, tiles_x(*cam), cam->width, cam->height};
   k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
@@ -636,7 +603,6 @@ static xg_status tiles_common(int32_t h, int32_t w, const double* means2d, const
   sp.n = n_splats;
   sp.tile_order = t.order;
   sp.counters = t.counters;
-  sp.sched = t.sched;
   return launch_tile_order(tile_ranges, tiles_x(cam) * tiles_y(cam), t.order, s);
 }
 

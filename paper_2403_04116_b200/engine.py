@@ -48,7 +48,6 @@ class Frame:
         self.order = torch.empty(n, dtype=torch.int32, device=dev)
         self.tile_ranges = torch.empty((self.n_tiles, 2), dtype=torch.int64, device=dev)
         self.tile_order = torch.empty(self.n_tiles, dtype=torch.int32, device=dev)
-        self.sched = torch.zeros(nat.XG_SCHED_SLOTS, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(nat.XG_NCOUNTERS, dtype=torch.int32, device=dev)
         self.image = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
@@ -94,7 +93,6 @@ class Frame:
         s.n = self.n
         s.entry_capacity = self.entry_capacity
         s.tile_order = self.tile_order.data_ptr()
-        s.sched = self.sched.data_ptr()
         return s
 
     # --- stages -------------------------------------------------------------

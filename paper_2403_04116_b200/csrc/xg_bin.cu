@@ -13,6 +13,8 @@
 // Sorting the N Gaussians once (64-bit keys, L2-resident) and then only the
 // ~10 tile bits of the E entries replaces a 74-bit (tile|depth64) sort of E
 // keys: two passes over E instead of ten.
+#include <limits.h>
+
 #include "xg_sort.cuh"
 
 namespace xg {
@@ -26,51 +28,109 @@ __global__ void k_iota(uint32_t* v, long long n, uint32_t* n_dev) {
   if (i == 0) *n_dev = (uint32_t)n;
 }
 
+// One warp per 32 consecutive depth-sorted Gaussians.  Their entries are
+// contiguous ([offsets[s0], offsets[s0] + total)), so the warp writes them
+// cooperatively - lane e of each round writes entry base + e - which keeps
+// every store coalesced regardless of how many tiles each Gaussian covers.
 __global__ void k_duplicate(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
                             const ushort4* __restrict__ rect, const uint32_t* __restrict__ offsets,
                             long long n, int ntx, long long cap, uint32_t* __restrict__ keys,
                             uint32_t* __restrict__ vals, uint32_t* counters) {
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  bool overflow = false;
+  const int lane = threadIdx.x & 31;
+  uint32_t g = 0, cnt = 0;
+  ushort4 r = make_ushort4(0, 0, 0, 0);
+  long long off = 0;
   if (s < n) {
-    const uint32_t g = order[s];
-    const uint32_t cnt = n_tiles[g];
-    if (cnt) {
-      const long long off = offsets[s];
-      if (off + cnt > cap) {
-        overflow = true;
-      } else {
-        const ushort4 r = rect[g];
-        long long o = off;
-        for (int ty = r.y; ty <= r.w; ++ty)
-          for (int tx = r.x; tx <= r.z; ++tx, ++o) {
-            keys[o] = (uint32_t)(ty * ntx + tx);
-            vals[o] = g;
-          }
-      }
+    g = order[s];
+    cnt = n_tiles[g];
+    off = offsets[s];
+    if (cnt) r = rect[g];
+  }
+  // inclusive warp scan of the counts
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t excl = incl - cnt;
+  const long long base = __shfl_sync(0xffffffffu, off - (long long)excl, 0);  // offsets[s0]
+  if (total == 0) return;
+  if (base + total > cap) {
+    if (lane == 0) atomicOr(&counters[XG_CTR_STATUS], XG_ST_ENTRY_OVERFLOW);
+    return;
+  }
+  const int w = cnt ? (int)(r.z - r.x + 1) : 1;
+  for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+    const uint32_t e = e0 + lane;
+    // owner: the last lane whose exclusive prefix is <= e (binary search via shuffles)
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int cand = lo + step;
+      const uint32_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+      if (cand < 32 && ex <= e) lo = cand;
+    }
+    const uint32_t j = e - __shfl_sync(0xffffffffu, excl, lo);
+    const int ow = __shfl_sync(0xffffffffu, w, lo);
+    const int ox = __shfl_sync(0xffffffffu, (int)r.x, lo);
+    const int oy = __shfl_sync(0xffffffffu, (int)r.y, lo);
+    const uint32_t og = __shfl_sync(0xffffffffu, g, lo);
+    if (e < total) {
+      const int ty = oy + (int)(j / (uint32_t)ow), tx = ox + (int)(j % (uint32_t)ow);
+      keys[base + e] = (uint32_t)(ty * ntx + tx);
+      vals[base + e] = og;
     }
   }
-  if (__ballot_sync(0xffffffffu, overflow) && lane_id() == 0)
-    atomicOr(&counters[XG_CTR_STATUS], XG_ST_ENTRY_OVERFLOW);
 }
 
-__device__ __forceinline__ long long lower_bound(const uint32_t* a, long long n, uint32_t v) {
-  long long lo = 0, hi = n;
-  while (lo < hi) {
-    const long long mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t* counters,
-                              long long cap, int n_tiles, long long* __restrict__ ranges) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
+// Tile ranges from the tile-sorted keys: a boundary pass writes the start /
+// end of every non-empty tile, then empty tiles get start = end = the start
+// of the next non-empty tile (np.searchsorted semantics, frontend.py:171-173).
+__global__ void k_tile_bounds(const uint32_t* __restrict__ keys, const uint32_t* counters, long long cap,
+                              long long* __restrict__ ranges) {
   long long e = counters[XG_CTR_ENTRIES];
   if (e > cap) e = cap;
-  ranges[2 * t] = lower_bound(keys, e, (uint32_t)t);
-  ranges[2 * t + 1] = lower_bound(keys, e, (uint32_t)t + 1);
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < e;
+       k += (long long)gridDim.x * blockDim.x) {
+    const uint32_t t = keys[k];
+    if (k == 0 || keys[k - 1] != t) ranges[2 * t] = k;
+    if (k == e - 1 || keys[k + 1] != t) ranges[2 * t + 1] = k + 1;
+  }
+}
+
+// Fill empty tiles (pre-set to -1) with the start of the next non-empty
+// tile: a suffix-min over tiles, in chunks of 1024 from the back.
+__global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, long long cap, int n_tiles,
+                                                    long long* __restrict__ ranges) {
+  __shared__ long long s_val[1024];
+  __shared__ long long s_next;
+  long long e = counters[XG_CTR_ENTRIES];
+  if (e > cap) e = cap;
+  if (threadIdx.x == 0) s_next = e;
+  for (int hi = n_tiles; hi > 0; hi -= 1024) {
+    const int t = hi - 1024 + (int)threadIdx.x;
+    const long long st = t >= 0 ? ranges[2 * t] : -1;
+    s_val[threadIdx.x] = st >= 0 ? st : LLONG_MAX;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix min (Hillis-Steele)
+      const long long other = threadIdx.x + o < 1024 ? s_val[threadIdx.x + o] : LLONG_MAX;
+      __syncthreads();
+      if (other < s_val[threadIdx.x]) s_val[threadIdx.x] = other;
+      __syncthreads();
+    }
+    if (t >= 0 && st < 0) {
+      long long cand = threadIdx.x + 1 < 1024 ? s_val[threadIdx.x + 1] : LLONG_MAX;
+      if (cand == LLONG_MAX) cand = s_next;
+      ranges[2 * t] = cand;
+      ranges[2 * t + 1] = cand;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_val[0] != LLONG_MAX) s_next = s_val[0];
+    __syncthreads();
+  }
 }
 
 struct BinWs {
@@ -153,7 +213,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                      w.tail, w.tail_bytes, s)) != XG_OK)
     return st;
   // 3. duplicate
-  k_duplicate<<<div_up(n, 128), 128, 0, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, w.offN,
+  k_duplicate<<<div_up(n, 256), 256, 0, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, w.offN,
                                              n, ntx, cap, w.keyE0, sp->entry_splat, sp->counters);
   if ((st = check_launch("k_duplicate")) != XG_OK) return st;
   // 4. stable sort by tile id
@@ -170,9 +230,11 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   if (res == 1)
     cudaMemcpyAsync(sp->entry_splat, w.valE1, sizeof(uint32_t) * cap, cudaMemcpyDeviceToDevice, s);
   // 5. ranges
-  k_tile_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(keys[res], sp->counters, cap, n_tiles,
-                                                      (long long*)sp->tile_ranges);
-  if ((st = check_launch("k_tile_ranges")) != XG_OK) return st;
+  cudaMemsetAsync(sp->tile_ranges, 0xff, sizeof(int64_t) * 2 * (size_t)n_tiles, s);
+  k_tile_bounds<<<4 * 148, 256, 0, s>>>(keys[res], sp->counters, cap, (long long*)sp->tile_ranges);
+  if ((st = check_launch("k_tile_bounds")) != XG_OK) return st;
+  k_tile_fill<<<1, 1024, 0, s>>>(sp->counters, cap, n_tiles, (long long*)sp->tile_ranges);
+  if ((st = check_launch("k_tile_fill")) != XG_OK) return st;
   if (!sp->tile_order) return XG_OK;
   return launch_tile_order(sp->tile_ranges, n_tiles, sp->tile_order, s);
 }

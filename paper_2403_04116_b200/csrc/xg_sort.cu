@@ -198,14 +198,19 @@ __global__ void __launch_bounds__(kSortThreads)
   K key[kSortRounds];
   uint32_t val[kSortRounds], pos[kSortRounds];
   const long long seg = base + (long long)warp * (kSortTile / kSortWarps);
+  // all loads first (16 independent coalesced loads in flight per thread)
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
     const long long idx = seg + r * 32 + lane;
     const bool valid = idx < n;
-    const K k = valid ? keys_in[idx] : (K)0;
-    key[r] = k;
+    key[r] = valid ? keys_in[idx] : (K)0;
     val[r] = valid ? vals_in[idx] : 0u;
-    const uint32_t d = valid ? ((uint32_t)(k >> shift) & (BINS - 1)) : (uint32_t)BINS;
+  }
+#pragma unroll
+  for (int r = 0; r < kSortRounds; ++r) {
+    const long long idx = seg + r * 32 + lane;
+    const bool valid = idx < n;
+    const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & (BINS - 1)) : (uint32_t)BINS;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const uint32_t before = wh[warp][valid ? d : 0];
     pos[r] = before + __popc(peers & lt);

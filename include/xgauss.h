@@ -195,6 +195,9 @@ xg_status xg_preprocess_bwd(const xg_cloud* cloud, const xg_camera* cam, const x
  * field f holding a NaN/Inf. */
 xg_status xg_check_finite(const float* grads, int64_t n, int32_t n_features, uint32_t* counters,
                           void* stream);
+/* Same over flat elements [elem_begin, elem_end) (one gradient bucket). */
+xg_status xg_check_finite_range(const float* grads, int64_t n, int32_t n_features, int64_t elem_begin,
+                                int64_t elem_end, uint32_t* counters, void* stream);
 
 /* K4c: fused Adam over all fields + quaternion renormalisation, in place.
  * lr[5] per field (positions, rotations, log_scales, raw_opacities,
@@ -205,6 +208,17 @@ xg_status xg_check_finite(const float* grads, int64_t n, int32_t n_features, uin
 xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq,
                   int64_t n, int32_t n_features, const double* lr, double beta1, double beta2,
                   double eps, double bc1, double bc2, const uint32_t* status, void* stream);
+
+/* The two halves of xg_adam: the element-wise update restricted to flat
+ * elements [elem_begin, elem_end) (one gradient bucket, so data-parallel
+ * training can update bucket i while bucket i+1 is being all-reduced), and
+ * the quaternion renormalisation (after every bucket is done). */
+xg_status xg_adam_range(float* params, const float* grads, float* exp_avg, float* exp_avg_sq,
+                        int64_t n, int32_t n_features, const double* lr, double beta1, double beta2,
+                        double eps, double bc1, double bc2, const uint32_t* status,
+                        int64_t elem_begin, int64_t elem_end, void* stream);
+xg_status xg_adam_renorm(float* params, int64_t n, int32_t n_features, const uint32_t* status,
+                         void* stream);
 
 /* K4d (1): density-control masks.  flags[N] bit0 high-gradient, bit1 large,
  * bit2 prune, bit3 clone, bit4 split; counts[4] = {prune, clone, split, keep}

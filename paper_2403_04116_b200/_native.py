@@ -86,11 +86,18 @@ SIGNATURES = {
     ),
     "xg_preprocess_bwd": (c_i32, [c_void_p] * 15),
     "xg_check_finite": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
+    "xg_check_finite_range": (c_i32, [c_void_p, c_i64, c_i32, c_i64, c_i64, c_void_p, c_void_p]),
     "xg_adam": (
         c_i32,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_f64, c_f64, c_f64, c_f64, c_f64,
          c_void_p, c_void_p],
     ),
+    "xg_adam_range": (
+        c_i32,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_f64, c_f64, c_f64, c_f64, c_f64,
+         c_void_p, c_i64, c_i64, c_void_p],
+    ),
+    "xg_adam_renorm": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
     "xg_densify_mark": (
         c_i32,
         [c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_void_p],

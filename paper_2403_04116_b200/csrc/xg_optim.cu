@@ -44,33 +44,40 @@ struct AdamArgs {
   float* m;
   float* v;
   long long n;
-  Layout L;
+  long long bound[4];  // field boundaries 3n, 7n, 10n, 11n of the flat layout
+  long long begin, end;
   double lr[kFields];
   double b1, b2, eps, bc1, bc2;
   const uint32_t* status;
 };
 
+// Element-wise over [begin, end) of the flat buffer: coalesced, one read of
+// p, m, v, g and one write of p, m, v per element (28 B, the HBM minimum).
+// A range form lets data-parallel training run Adam on one gradient bucket
+// while the next bucket is still being all-reduced.
 __global__ void k_adam(AdamArgs a) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
   const uint32_t bad = a.status ? (a.status[0] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f : 0u;
-  for (int f = 0; f < kFields; ++f) {
-    if (bad & ((2u << f) - 1u)) return;  // a field <= f diverged: stop (reference raises here)
-    const long long base = a.L.off[f] + i * a.L.width[f];
-    const double lr = a.lr[f];
-    for (int c = 0; c < a.L.width[f]; ++c) {
-      const long long e = base + c;
-      const double g = a.g[e];
-      double m = a.m[e], v = a.v[e];
-      m = a.b1 * m + (1.0 - a.b1) * g;
-      v = a.b2 * v + (1.0 - a.b2) * g * g;
-      a.m[e] = (float)m;
-      a.v[e] = (float)v;
-      a.p[e] = (float)((double)a.p[e] - lr * (m / a.bc1) / (sqrt(v / a.bc2) + a.eps));
-    }
+  for (long long e = a.begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < a.end;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int f = (e >= a.bound[0]) + (e >= a.bound[1]) + (e >= a.bound[2]) + (e >= a.bound[3]);
+    if (bad & ((2u << f) - 1u)) continue;  // a field <= f diverged (the reference raises there)
+    const double g = a.g[e];
+    double m = a.m[e], v = a.v[e];
+    m = a.b1 * m + (1.0 - a.b1) * g;
+    v = a.b2 * v + (1.0 - a.b2) * g * g;
+    a.m[e] = (float)m;
+    a.v[e] = (float)v;
+    a.p[e] = (float)((double)a.p[e] - a.lr[f] * (m / a.bc1) / (sqrt(v / a.bc2) + a.eps));
   }
-  // normalize_rotations (gaussians.py:234-235)
-  float* q = a.p + a.L.off[1] + 4 * i;
+}
+
+// normalize_rotations (gaussians.py:234-235) after the update; skipped if
+// any field diverged (the reference raises before renormalising).
+__global__ void k_renorm(float* q_all, long long n, const uint32_t* status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (status && ((status[0] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f)) return;
+  float* q = q_all + 4 * i;  // 3n-float offset: not 16-byte aligned in general
   const double w = q[0], x = q[1], y = q[2], z = q[3];
   const double nrm = sqrt(((w * w + x * x) + y * y) + z * z);
   q[0] = (float)(w / nrm);
@@ -227,20 +234,28 @@ using namespace xg;
 
 extern "C" {
 
-xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,
-                  int32_t n_features, const double* lr, double beta1, double beta2, double eps,
-                  double bc1, double bc2, const uint32_t* status, void* stream) {
-  if (!params || !grads || !exp_avg || !exp_avg_sq || !lr || n < 1 || n_features < 1) {
+static xg_status adam_launch(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,
+                             int32_t n_features, const double* lr, double beta1, double beta2, double eps,
+                             double bc1, double bc2, const uint32_t* status, int64_t begin, int64_t end,
+                             cudaStream_t s) {
+  if (!params || !grads || !exp_avg || !exp_avg_sq || !lr || n < 1 || n_features < 1 || begin < 0 ||
+      end > n * (11 + n_features) || begin > end) {
     set_error_msg("xg_adam: invalid argument");
     return XG_ERR_INVALID;
   }
+  if (begin == end) return XG_OK;
   AdamArgs a;
   a.p = params;
   a.g = grads;
   a.m = exp_avg;
   a.v = exp_avg_sq;
   a.n = n;
-  a.L = make_layout(n, n_features);
+  a.bound[0] = 3 * n;
+  a.bound[1] = 7 * n;
+  a.bound[2] = 10 * n;
+  a.bound[3] = 11 * n;
+  a.begin = begin;
+  a.end = end;
   for (int f = 0; f < kFields; ++f) a.lr[f] = lr[f];
   a.b1 = beta1;
   a.b2 = beta2;
@@ -248,8 +263,39 @@ xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_
   a.bc1 = bc1;
   a.bc2 = bc2;
   a.status = status;
-  k_adam<<<div_up(n, 128), 128, 0, (cudaStream_t)stream>>>(a);
+  const int64_t cnt = end - begin;
+  int grid = div_up(cnt, 256);
+  if (grid > 148 * 16) grid = 148 * 16;
+  k_adam<<<grid, 256, 0, s>>>(a);
   return check_launch("k_adam");
+}
+
+xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,
+                  int32_t n_features, const double* lr, double beta1, double beta2, double eps,
+                  double bc1, double bc2, const uint32_t* status, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  xg_status st = adam_launch(params, grads, exp_avg, exp_avg_sq, n, n_features, lr, beta1, beta2, eps, bc1,
+                             bc2, status, 0, n * (11 + n_features), s);
+  if (st != XG_OK) return st;
+  return xg_adam_renorm(params, n, n_features, status, stream);
+}
+
+xg_status xg_adam_range(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,
+                        int32_t n_features, const double* lr, double beta1, double beta2, double eps,
+                        double bc1, double bc2, const uint32_t* status, int64_t elem_begin, int64_t elem_end,
+                        void* stream) {
+  return adam_launch(params, grads, exp_avg, exp_avg_sq, n, n_features, lr, beta1, beta2, eps, bc1, bc2,
+                     status, elem_begin, elem_end, (cudaStream_t)stream);
+}
+
+xg_status xg_adam_renorm(float* params, int64_t n, int32_t n_features, const uint32_t* status, void* stream) {
+  if (!params || n < 1) {
+    set_error_msg("xg_adam_renorm: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  (void)n_features;
+  k_renorm<<<div_up(n, 256), 256, 0, (cudaStream_t)stream>>>(params + 3 * n, n, status);
+  return check_launch("k_renorm");
 }
 
 xg_status xg_densify_mark(const float* params, int64_t n, int32_t n_features, const float* norm_sum,

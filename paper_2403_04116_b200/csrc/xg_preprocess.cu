@@ -418,11 +418,12 @@ __global__ void k_preprocess_bwd(CloudPtrs c, Cam k, xg_splats sp, const float* 
     atomicOr(&o.counters[XG_CTR_STATUS], bad << XG_ST_GRAD_NONFINITE_SHIFT);
 }
 
-__global__ void k_check_finite(const float* __restrict__ g, long long n, int nf, uint32_t* counters) {
+__global__ void k_check_finite(const float* __restrict__ g, long long n, int nf, long long begin, long long end,
+                               uint32_t* counters) {
   const long long total = n * (11 + nf);
   const long long bounds[5] = {3 * n, 7 * n, 10 * n, 11 * n, total};
   unsigned bad = 0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+  for (long long e = begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < end;
        e += (long long)gridDim.x * blockDim.x) {
     if (!isfinite(g[e])) {
       int f = 0;
@@ -498,7 +499,20 @@ xg_status xg_check_finite(const float* grads, int64_t n, int32_t n_features, uin
     set_error_msg("xg_check_finite: invalid argument");
     return XG_ERR_INVALID;
   }
-  k_check_finite<<<296, 256, 0, (cudaStream_t)stream>>>(grads, n, n_features, counters);
+  k_check_finite<<<296, 256, 0, (cudaStream_t)stream>>>(grads, n, n_features, 0, n * (11 + n_features),
+                                                        counters);
+  return check_launch("k_check_finite");
+}
+
+xg_status xg_check_finite_range(const float* grads, int64_t n, int32_t n_features, int64_t elem_begin,
+                                int64_t elem_end, uint32_t* counters, void* stream) {
+  if (!grads || !counters || n < 1 || elem_begin < 0 || elem_end > n * (11 + n_features) ||
+      elem_begin > elem_end) {
+    set_error_msg("xg_check_finite_range: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  if (elem_begin == elem_end) return XG_OK;
+  k_check_finite<<<296, 256, 0, (cudaStream_t)stream>>>(grads, n, n_features, elem_begin, elem_end, counters);
   return check_launch("k_check_finite");
 }
 

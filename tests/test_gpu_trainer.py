@@ -287,3 +287,26 @@ class TestTrainLoop:  # test_trainer.py:290-386
         ds = self_render_dataset(xg, truth, sc)
         rep = tr.evaluate(truth, ds, np.array([0, 1]))
         assert rep.psnr > 120.0 and rep.ssim > 0.999999
+
+
+class TestDataParallelSingleRank:
+    """The data-parallel step (bucketed reduce + range Adam + renorm) on one
+    rank must reproduce the single-GPU Trainer exactly (same views, same
+    kernels, no collective)."""
+
+    def test_matches_trainer(self, xg, tr, rng):
+        from paper_2403_04116_b200.parallel import DataParallelTrainer
+
+        sc = small_scanner(32, 32, 6.0, n_views=4)
+        ds = self_render_dataset(xg, cloud_of(xg, random_arrays(8, rng, pos_scale=30.0, scale_range=(8.0, 15.0))), sc)
+        start = random_arrays(6, rng, pos_scale=30.0)
+        cfg = tr.TrainConfig(iterations=30, gamma=0.0, densify_from_iter=5, densify_interval=10,
+                             densify_until_iter=30, densify_grad_threshold=1e-9, log_interval=10**6,
+                             eval_interval=10**6)
+        a = tr.Trainer(ds, cloud_of(xg, start), cfg)
+        b = DataParallelTrainer(ds, cloud_of(xg, start), cfg, bucket_bytes=4 * 37)
+        for _ in range(30):
+            a.step()
+            b.step()
+        assert a.cloud.n_points == b.cloud.n_points > 6
+        assert np.array_equal(np_(a.cloud.flat), np_(b.cloud.flat))

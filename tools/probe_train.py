@@ -22,9 +22,11 @@ tr = Trainer(ds, GaussianCloud(**acui.init_alternative_arrays("cuboid", acui.ben
 for _ in range(5):
     tr.step()
 torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off captures only these iterations
 t0 = time.perf_counter()
 for _ in range(iters):
     tr.step()
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print(f"{iters} iterations: {1e3 * (time.perf_counter() - t0) / iters:.3f} ms/iter, N={tr.cloud.n_points}, "
       f"entries={tr.eng.frame.last_counters[1]}")

@@ -122,6 +122,8 @@ class GradientAllReducer:
 
 def allreduce_stats(stats, group=None) -> None:
     """Sum rank-local DensifyStats before a density-control event."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return
     for t in (stats.norm_sum, stats.obs_count, stats.world_grad_sum):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 

@@ -384,7 +384,7 @@ def run_ours(args) -> None:
         "ms_per_view": ms / (VIEWS * args.steps),
     }
     if not args.no_train:
-        line["train_c2"] = train_block(args, timed, ClockSampler, local)
+        line["train_c2" if world == 1 else "train_c5"] = train_block(args, timed, ClockSampler, local, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample_views or None)
@@ -396,26 +396,36 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def train_block(args, timed, clock_cls, local) -> dict:
-    """C2: ~100k Gaussians, 50 training views at 512x512, full training
-    iterations (render fwd+bwd, L1, Adam, densify/prune every 100) through
-    the public Trainer API; one step = 100 iterations (one densify event)."""
+def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
+    """N=1 -> C2: ~100k Gaussians, 50 training views at 512x512, full
+    training iterations (render fwd+bwd, L1, Adam, densify/prune every 100)
+    through the public Trainer API.  N>1 -> C5: 493k Gaussians, one view per
+    GPU per step, NCCL all-reduce of the flat gradient (bucketed, overlapped
+    with the fused Adam), DataParallelTrainer.  One step = 100 iterations."""
     import torch
 
     from paper_2403_04116_b200 import _native, acui, geometry
     from paper_2403_04116_b200.dataset import self_render
     from paper_2403_04116_b200.gaussians import GaussianCloud
+    from paper_2403_04116_b200.parallel import DataParallelTrainer
     from paper_2403_04116_b200.trainer import TrainConfig, Trainer
 
+    g = G_C2 if world == 1 else G_C3
     sc = geometry.ScannerConfig(L_SO, L_SD, DET, DET, 192.0 / DET, geometry.equal_interval_angles(100))
-    truth = GaussianCloud(**phantom_truth(G_C2), device="cuda")
+    truth = GaussianCloud(**phantom_truth(g), device="cuda")
     ds = self_render(truth, sc)
-    init = acui.init_alternative_arrays("cuboid", acui.benchmark_spec(G_C2), 16, 0)
+    init = acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 0)
     cfg = TrainConfig(iterations=20_000, log_interval=10**9, eval_interval=10**9)
     per = args.train_iters_per_step
     out = {}
     for mode in ("device", "e2e"):
-        tr = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg, targets_on_host=(mode == "e2e"))
+        if world == 1:
+            tr = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg, targets_on_host=(mode == "e2e"))
+        else:
+            dp = DataParallelTrainer(ds, GaussianCloud(**init, device="cuda"), cfg,
+                                     targets_on_host=(mode == "e2e"))
+            tr = dp.t
+            tr.step = dp.step  # the DP step drives the same Trainer state
         warm = max(args.warmup, 5)  # reach densify_from_iter = 500
         for _ in range(warm * per):
             tr.step()
@@ -429,11 +439,15 @@ def train_block(args, timed, clock_cls, local) -> dict:
         torch.cuda.synchronize()
     iters = per * args.steps
     d, e = out["device"], out["e2e"]
+    name = (f"C2: {g}^3-lattice ACUI init ({(2 * (g // 4) + 3) ** 3:,} Gaussians), 50 train views of a "
+            "100-view 512x512 sweep, full iterations incl. densify/prune every 100 (one event per step)"
+            if world == 1 else
+            f"C5: {(2 * (g // 4) + 3) ** 3:,} Gaussians, 512x512, data-parallel x{world}: one view per GPU per "
+            "step, NCCL all-reduce of the 27N gradient bucketed and overlapped with the fused Adam")
     return {"metric": "train iters/s", "value": iters / (d["ms"] / 1e3), "unit": "iters/s",
+            "views_per_s": iters * world / (d["ms"] / 1e3),
             "ms_per_iter": d["ms"] / iters,
-            "config": {"workload": f"C2: {G_C2}^3-lattice ACUI init ({(2 * (G_C2 // 4) + 3) ** 3:,} Gaussians), "
-                                   "50 train views of a 100-view 512x512 sweep, full iterations incl. "
-                                   "densify/prune every 100 (one event per step)",
+            "config": {"workload": name,
                        "iters_per_step": per, "warmup_iters": max(args.warmup, 5) * per,
                        "n_points_timed": [d["n0"], d["n1"]], "densify_events": d["densify_events"],
                        "targets": "rendered by the engine from a synthetic ellipsoid/cuboid phantom cloud"},

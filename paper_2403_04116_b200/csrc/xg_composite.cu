@@ -292,14 +292,19 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // directly (no acc - prefix - contrib cancellation) and T restored by
 // division by (1 - sigma).  Returns G = dL/dsigma * sigma on unclamped
 // pairs (the reference's g_power) and g * w (the intensity gradient).
+// kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
+// safety margin for the MUFU.EX2 error the clamp logic is compiled out.
+constexpr float kNoClampAlpha = 0.98999f;
+
+template <bool kMayClamp>
 __device__ __forceinline__ void unblend(float dy, float bdx, float adx2, const Rec& r, bool act, float g,
                                         float& T, float& S, float& G, float& gw) {
   const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
   const float dens = ex2_approx(p2);
   const float sraw = __fmul_rn(r.b.y, dens);
   const bool valid = act & (p2 <= 0.f) & (p2 >= kCut2);
-  const bool clamped = sraw >= kClamp;
-  const float sg = valid ? fminf(sraw, kClamp) : 0.f;
+  const bool clamped = kMayClamp && (sraw >= kClamp);
+  const float sg = valid ? (kMayClamp ? fminf(sraw, kClamp) : sraw) : 0.f;
   const float rc = rcp_approx(1.f - sg);
   const float Tb = T * rc;
   const float w = sg * Tb;
@@ -311,35 +316,70 @@ __device__ __forceinline__ void unblend(float dy, float bdx, float adx2, const R
   T = valid ? Tb : T;
 }
 
-// Sum 8 per-lane values over the warp; returns the total of value
-// index ((lane>>2)&7) in every lane (transpose-reduce: 9 shuffles).
-__device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
+// Both pixels of the lane for one splat; returns the lane's 7 partial sums.
+template <bool kMayClamp>
+__device__ __forceinline__ bool unblend_splat(const Rec& r, int krel, float fx, float fy0, float fy1,
+                                              int last0, int last1, float g0, float g1, float& T0,
+                                              float& T1, float& S0, float& S1, float* v) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+  const float bdx = __fmul_rn(r.a.w, dx);
+  const float dy0 = __fsub_rn(fy0, r.a.y), dy1 = __fsub_rn(fy1, r.a.y);
+  float G0, G1, gw0, gw1;
+  unblend<kMayClamp>(dy0, bdx, adx2, r, krel <= last0, g0, T0, S0, G0, gw0);
+  unblend<kMayClamp>(dy1, bdx, adx2, r, krel <= last1, g1, T1, S1, G1, gw1);
+  const float Gs = G0 + G1, gws = gw0 + gw1;
+  const float Gdy0 = G0 * dy0, Gdy1 = G1 * dy1;
+  const float Gdys = Gdy0 + Gdy1;
+  v[0] = Gs * dx;
+  v[1] = Gdys;
+  v[2] = Gs * (dx * dx);
+  v[3] = Gdys * dx;
+  v[4] = fmaf(Gdy0, dy0, Gdy1 * dy1);
+  v[5] = gws;
+  v[6] = Gs;
+  v[7] = 0.f;
+  return (Gs != 0.f) | (gws != 0.f);
+}
+
+// Sum 16 per-lane values over the warp (two splats' 8-value records); lane l
+// ends with the total of value index (l >> 1) & 15 (transpose-reduce: 16
+// shuffles for 16 values).
+__device__ __forceinline__ float warp_reduce16(float (&v)[16]) {
   const int lane = threadIdx.x & 31;
   {
     const bool up = lane & 16;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float send = up ? v[i] : v[i + 4];
-      const float keep = up ? v[i + 4] : v[i];
+    for (int i = 0; i < 8; ++i) {
+      const float send = up ? v[i] : v[i + 8];
+      const float keep = up ? v[i + 8] : v[i];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
   }
   {
     const bool up = lane & 8;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float send = up ? v[i] : v[i + 2];
-      const float keep = up ? v[i + 2] : v[i];
+    for (int i = 0; i < 4; ++i) {
+      const float send = up ? v[i] : v[i + 4];
+      const float keep = up ? v[i + 4] : v[i];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
   }
   {
     const bool up = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = up ? v[i] : v[i + 2];
+      const float keep = up ? v[i + 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  {
+    const bool up = lane & 2;
     const float send = up ? v[0] : v[1];
     const float keep = up ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
   }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
   return v[0];
 }
@@ -388,27 +428,38 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
       const int cnt = compact(cur, (int)(b1 - 32 - u.start) + lane, u.x0, u.y0, u.xa, u.xb, u.ya, u.yb, rec,
                               kk, gid);
       nxt = gather(b1 - 64 + lane, u.start, hi, a.entry, a.mean2d, a.coef, a.inten);  // prefetch
-      for (int q = cnt - 1; q >= 0; --q) {
-        const Rec r = rec[q];
-        const int krel = kk[q];
-        const float dx = __fsub_rn(u.fx, r.a.x);
-        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-        const float bdx = __fmul_rn(r.a.w, dx);
-        const float dy0 = __fsub_rn(u.fy0, r.a.y), dy1 = __fsub_rn(u.fy1, r.a.y);
-        float G0, G1, gw0, gw1;
-        unblend(dy0, bdx, adx2, r, krel <= last0, g0, T0, S0, G0, gw0);
-        unblend(dy1, bdx, adx2, r, krel <= last1, g1, T1, S1, G1, gw1);
-        const float Gs = G0 + G1, gws = gw0 + gw1;
-        if (!__any_sync(0xffffffffu, (Gs != 0.f) | (gws != 0.f))) continue;
-        const float Gdy0 = G0 * dy0, Gdy1 = G1 * dy1;
-        const float Gdys = Gdy0 + Gdy1;
-        float v[8] = {Gs * dx, Gdys, Gs * (dx * dx), Gdys * dx, fmaf(Gdy0, dy0, Gdy1 * dy1), gws, Gs, 0.f};
-        const float tot = warp_reduce8(v);
-        // value i sits in lane 4i: gather 0..3 into lane 0 and 4..7 into lane 16
-        const float t1 = __shfl_down_sync(0xffffffffu, tot, 4);
-        const float t2 = __shfl_down_sync(0xffffffffu, tot, 8);
-        const float t3 = __shfl_down_sync(0xffffffffu, tot, 12);
-        if ((lane & 15) == 0) red_add_v4(a.grad_acc + 8 * (long long)gid[q] + (lane >> 2), tot, t1, t2, t3);
+      // splats are processed two at a time, back to front (A = q, then
+      // B = q - 1), and their records reduced together
+      for (int q = cnt - 1; q >= 0; q -= 2) {
+        const bool hasB = q >= 1;
+        const Rec ra = rec[q];
+        const Rec rb = hasB ? rec[q - 1] : ra;
+        const int ka = kk[q], kb = hasB ? kk[q - 1] : ka;
+        float v[16];
+        bool any;
+        if (ra.b.y < kNoClampAlpha && rb.b.y < kNoClampAlpha) {  // warp-uniform
+          any = unblend_splat<false>(ra, ka, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v);
+          if (hasB)
+            any |= unblend_splat<false>(rb, kb, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v + 8);
+        } else {
+          any = unblend_splat<true>(ra, ka, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v);
+          if (hasB)
+            any |= unblend_splat<true>(rb, kb, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v + 8);
+        }
+        if (!hasB)
+#pragma unroll
+          for (int i = 8; i < 16; ++i) v[i] = 0.f;
+        if (!__any_sync(0xffffffffu, any)) continue;
+        const float tot = warp_reduce16(v);
+        // value i sits in lanes 2i, 2i+1: lanes 0/8 collect A's 0-3 / 4-7,
+        // lanes 16/24 collect B's
+        const float t1 = __shfl_down_sync(0xffffffffu, tot, 2);
+        const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
+        const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
+        if ((lane & 7) == 0 && (lane < 16 || hasB)) {
+          const uint32_t id = lane < 16 ? gid[q] : gid[q - 1];
+          red_add_v4(a.grad_acc + 8 * (long long)id + ((lane & 8) ? 4 : 0), tot, t1, t2, t3);
+        }
       }
       __syncwarp();
     }

@@ -34,6 +34,9 @@ namespace {
 constexpr int kWarps = 8;             // independent warps per CTA
 constexpr int kThreads = 32 * kWarps;
 constexpr float kCullMargin = 0.05f;
+// kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
+// safety margin for the MUFU.EX2 error the clamp logic is compiled out.
+constexpr float kNoClampAlpha = 0.98999f;
 
 struct Rec {
   float4 a;  // mx, my (tile-relative), A2, B2
@@ -84,7 +87,8 @@ __device__ __forceinline__ Raw gather(long long k, long long lo, long long hi,
 // survivors (ascending entry order) into the warp's shared slice.  Returns
 // the survivor count.
 __device__ __forceinline__ int compact(const Raw& raw, int krel, double x0, double y0, float xa, float xb,
-                                       float ya, float yb, Rec* s_rec, int* s_k, uint32_t* s_gid) {
+                                       float ya, float yb, Rec* s_rec, int* s_k, uint32_t* s_gid,
+                                       bool* may_clamp = nullptr) {
   Rec r;
   bool keep = false;
   if (raw.valid) {
@@ -93,6 +97,7 @@ __device__ __forceinline__ int compact(const Raw& raw, int krel, double x0, doub
     keep = overlaps(r, xa, xb, ya, yb);
   }
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (may_clamp) *may_clamp = __any_sync(0xffffffffu, keep && !(r.b.y < kNoClampAlpha));
   if (keep) {
     const int pos = __popc(bal & lanemask_lt());
     s_rec[pos] = r;
@@ -164,20 +169,39 @@ struct FwdArgs {
   int ntx, w, h;
 };
 
-// One pixel, one entry: the blend step of _kernels.pyx:57-72.
+// One pixel, one entry: the blend step of _kernels.pyx:57-72.  kTrack
+// records the last blended entry (n_contrib, needed by the backward);
+// kMayClamp keeps the sigma <= 0.99 clamp (only alpha >= 0.99 can reach it).
+template <bool kTrack, bool kMayClamp>
 __device__ __forceinline__ void blend(float dy, float bdx, float adx2, const Rec& r, int krel,
                                       float& T, float& acc, int& last) {
   const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
   const float dens = ex2_approx(p2);
-  float sg = fminf(__fmul_rn(r.b.y, dens), kClamp);
+  float sg = __fmul_rn(r.b.y, dens);
+  if (kMayClamp) sg = fminf(sg, kClamp);
   const bool ok = (p2 <= 0.f) & (p2 >= kCut2) & (T >= kFloor);
   sg = ok ? sg : 0.f;
   const float w = __fmul_rn(sg, T);
   acc = __fmaf_rn(r.b.z, w, acc);
   T = __fmaf_rn(-sg, T, T);
-  last = ok ? krel : last;
+  if (kTrack) last = ok ? krel : last;
 }
 
+template <bool kTrack, bool kMayClamp>
+__device__ __forceinline__ void blend_batch(const Rec* rec, const int* kk, int cnt, const Unit& u, float& T0,
+                                            float& T1, float& acc0, float& acc1, int& last0, int& last1) {
+  for (int q = 0; q < cnt; ++q) {
+    const Rec r = rec[q];
+    const int krel = kTrack ? kk[q] : 0;
+    const float dx = __fsub_rn(u.fx, r.a.x);
+    const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+    const float bdx = __fmul_rn(r.a.w, dx);
+    blend<kTrack, kMayClamp>(__fsub_rn(u.fy0, r.a.y), bdx, adx2, r, krel, T0, acc0, last0);
+    blend<kTrack, kMayClamp>(__fsub_rn(u.fy1, r.a.y), bdx, adx2, r, krel, T1, acc1, last1);
+  }
+}
+
+template <bool kTrack>
 __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
   __shared__ Rec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
@@ -194,18 +218,14 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
     Raw nxt = gather(u.start + lane, u.start, u.end, a.entry, a.mean2d, a.coef, a.inten);
     for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
       const Raw cur = nxt;
+      bool may_clamp;
       const int cnt = compact(cur, (int)(b0 - u.start) + lane, u.x0, u.y0, u.xa, u.xb, u.ya, u.yb, rec, kk,
-                              nullptr);
+                              nullptr, &may_clamp);
       nxt = gather(b0 + 32 + lane, u.start, u.end, a.entry, a.mean2d, a.coef, a.inten);  // prefetch
-      for (int q = 0; q < cnt; ++q) {
-        const Rec r = rec[q];
-        const int krel = kk[q];
-        const float dx = __fsub_rn(u.fx, r.a.x);
-        const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-        const float bdx = __fmul_rn(r.a.w, dx);
-        blend(__fsub_rn(u.fy0, r.a.y), bdx, adx2, r, krel, T0, acc0, last0);
-        blend(__fsub_rn(u.fy1, r.a.y), bdx, adx2, r, krel, T1, acc1, last1);
-      }
+      if (may_clamp)  // warp-uniform, per batch of 32 entries
+        blend_batch<kTrack, true>(rec, kk, cnt, u, T0, T1, acc0, acc1, last0, last1);
+      else
+        blend_batch<kTrack, false>(rec, kk, cnt, u, T0, T1, acc0, acc1, last0, last1);
       __syncwarp();
       alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
     }
@@ -213,15 +233,19 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
     float l1 = 0.f;
     if (u.in0) {
       a.image[o0] = acc0;
-      if (a.t_final) a.t_final[o0] = T0;
-      if (a.n_contrib) a.n_contrib[o0] = last0 + 1;
+      if (kTrack) {
+        a.t_final[o0] = T0;
+        a.n_contrib[o0] = last0 + 1;
+      }
       if (a.target) l1 += fabsf(acc0 - a.target[o0]);
     }
     if (u.in1) {
       const long long o1 = o0 + a.w;
       a.image[o1] = acc1;
-      if (a.t_final) a.t_final[o1] = T1;
-      if (a.n_contrib) a.n_contrib[o1] = last1 + 1;
+      if (kTrack) {
+        a.t_final[o1] = T1;
+        a.n_contrib[o1] = last1 + 1;
+      }
       if (a.target) l1 += fabsf(acc1 - a.target[o1]);
     }
     if (a.target && a.l1_sum) {
@@ -292,10 +316,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // directly (no acc - prefix - contrib cancellation) and T restored by
 // division by (1 - sigma).  Returns G = dL/dsigma * sigma on unclamped
 // pairs (the reference's g_power) and g * w (the intensity gradient).
-// kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
-// safety margin for the MUFU.EX2 error the clamp logic is compiled out.
-constexpr float kNoClampAlpha = 0.98999f;
-
 template <bool kMayClamp>
 __device__ __forceinline__ void unblend(float dy, float bdx, float adx2, const Rec& r, bool act, float g,
                                         float& T, float& S, float& G, float& gw) {
@@ -592,7 +612,12 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
   FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
             target, l1_sum, tiles_x(*cam), cam->width, cam->height};
-  k_composite_fwd<<<persistent_grid(k_composite_fwd, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
+  if (t_final && n_contrib)  // training / backward: per-pixel T and contributor counts
+    k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0,
+                            (cudaStream_t)stream>>>(a);
+  else  // inference: image only
+    k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads,
+                             0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
 }
 

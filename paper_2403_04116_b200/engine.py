@@ -125,20 +125,22 @@ class Frame:
         )
 
     def composite(self, target: torch.Tensor | None = None, l1_sum: torch.Tensor | None = None,
-                  image_out: torch.Tensor | None = None) -> None:
+                  image_out: torch.Tensor | None = None, track: bool = True) -> None:
         """K3.  ``image_out`` (float32 [H, W], contiguous) receives the image
-        instead of the frame's own buffer (e.g. a slot of a sweep stack)."""
+        instead of the frame's own buffer (e.g. a slot of a sweep stack).
+        ``track=False`` (inference) skips the per-pixel final transmittance
+        and contributor counts the backward needs."""
         sp = self.splats_struct()
         img = self.image if image_out is None else image_out
         nat.check(
             nat.lib().xg_composite_fwd(
                 ctypes.byref(self.cam), ctypes.byref(sp), img.data_ptr(),
-                self.t_final.data_ptr(), self.n_contrib.data_ptr(), nat.ptr(target, "target"),
-                nat.ptr(l1_sum, "l1_sum"), nat.stream(),
+                self.t_final.data_ptr() if track else None, self.n_contrib.data_ptr() if track else None,
+                nat.ptr(target, "target"), nat.ptr(l1_sum, "l1_sum"), nat.stream(),
             ),
             "xg_composite_fwd",
         )
-        self.has_forward = True
+        self.has_forward = track
 
     def read_counters(self) -> tuple[int, int, int]:
         c = self.counters.cpu().numpy().astype("int64") & 0xFFFFFFFF

@@ -84,11 +84,11 @@ class SweepRenderer:
                     a = torch.cuda.Event(enable_timing=True)
                     b = torch.cuda.Event(enable_timing=True)
                     a.record(st)
-                    fr.composite(image_out=out[i])
+                    fr.composite(image_out=out[i], track=False)
                     b.record(st)
                     composite_events.append((a, b))
                 else:
-                    fr.composite(image_out=out[i])
+                    fr.composite(image_out=out[i], track=False)
                 status[i : i + 1].copy_(fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
                 if host_out is not None:
                     host_out[i].copy_(out[i], non_blocking=True)

@@ -309,4 +309,5 @@ class TestDataParallelSingleRank:
             a.step()
             b.step()
         assert a.cloud.n_points == b.cloud.n_points > 6
-        assert np.array_equal(np_(a.cloud.flat), np_(b.cloud.flat))
+        # identical up to the summation order of the backward's float atomics
+        assert np.allclose(np_(a.cloud.flat), np_(b.cloud.flat), rtol=1e-4, atol=1e-6)

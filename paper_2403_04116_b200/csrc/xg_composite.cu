@@ -141,12 +141,29 @@ __device__ __forceinline__ Unit make_unit(int tile, int quad, int ntx, int w, in
   return u;
 }
 
-// Next (tile, quarter) unit for this warp from the heaviest-first queue.
-__device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int n_tiles, int& tile, int& quad) {
-  uint32_t k = 0;
-  if ((threadIdx.x & 31) == 0) k = atomicAdd(work, 1u);
-  k = __shfl_sync(0xffffffffu, k, 0);
-  if (k >= 4u * (uint32_t)n_tiles) return false;
+// Next (tile, quarter) unit for this warp.  Units are the heaviest-first
+// tile order x 4 quarters.  The first wave is dealt statically: warp w of
+// CTA c takes unit G*w + c (w even) or G*w + G-1-c (w odd), so every CTA -
+// and with an even CTA count per SM every SM - starts with the same mix of
+// heavy and light units (a shared counter would hand them out in arrival
+// order).  After that, warps pull the remaining (lightest) units from the
+// counter.
+__device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int n_tiles, bool& first,
+                                          int& tile, int& quad) {
+  const uint32_t n_units = 4u * (uint32_t)n_tiles;
+  const uint32_t G = gridDim.x, w = threadIdx.x >> 5;
+  const uint32_t dealt = min(n_units, G * (uint32_t)kWarps);
+  uint32_t k = n_units;
+  if (first) {
+    first = false;
+    k = G * w + ((w & 1u) ? G - 1u - blockIdx.x : blockIdx.x);
+  }
+  if (k >= dealt) {
+    uint32_t d = 0;
+    if ((threadIdx.x & 31) == 0) d = atomicAdd(work, 1u);
+    k = dealt + __shfl_sync(0xffffffffu, d, 0);
+  }
+  if (k >= n_units) return false;
   tile = order[k >> 2];
   quad = (int)(k & 3u);
   return true;
@@ -209,7 +226,8 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
   Rec* rec = s_rec[warp];
   int* kk = s_k[warp];
   int tile, quad;
-  while (next_unit(a.order, a.work, a.n_tiles, tile, quad)) {
+  bool first = true;
+  while (next_unit(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     float T0 = u.in0 ? 1.f : 0.f, T1 = u.in1 ? 1.f : 0.f;
     float acc0 = 0.f, acc1 = 0.f;
@@ -419,7 +437,8 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   int* kk = s_k[warp];
   uint32_t* gid = s_gid[warp];
   int tile, quad;
-  while (next_unit(a.order, a.work, a.n_tiles, tile, quad)) {
+  bool first = true;
+  while (next_unit(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
     float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
@@ -499,9 +518,11 @@ int persistent_grid(K kernel, int n_units, const char* env) {
   if (per_sm < 1) per_sm = 1;
   const char* e = getenv(env);
   if (e && atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
+  // a full wave with the same CTA count on every SM (the dealt first wave
+  // balances per CTA); tiny problems launch only what they can use
   const int grid = sms * per_sm;
   const int need = (n_units + kWarps - 1) / kWarps;
-  return need < grid ? need : grid;
+  return need < sms ? need : grid;
 }
 
 // ---------------------------------------------------------------------------

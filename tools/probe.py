@@ -16,13 +16,17 @@ def main(g=152, d=512, views=20):
     fr.preprocess(cloud, cams[0]); a, e, s = fr.ensure_binned(); fr.composite(); torch.cuda.synchronize()
     print(f"N={cloud.n_points} D={d} active={a} entries={e} status={s}")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    t = np.zeros(3)
+    t = np.zeros(4)
     for cam in cams:
         ev[0].record(); fr.preprocess(cloud, cam); ev[1].record(); fr.bin(); ev[2].record(); fr.composite(); ev[3].record()
         torch.cuda.synchronize()
-        t += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+        t[:3] += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+        ev[0].record(); fr.composite(track=False); ev[1].record()
+        torch.cuda.synchronize()
+        t[3] += ev[0].elapsed_time(ev[1])
     t /= len(cams)
-    print(f"per view ms: preprocess {t[0]:.3f} bin {t[1]:.3f} composite {t[2]:.3f} total {t.sum():.3f} -> {1000/t.sum():.0f} fps")
+    print(f"per view ms: preprocess {t[0]:.3f} bin {t[1]:.3f} composite {t[2]:.3f} (inference {t[3]:.3f}) "
+          f"total {t[:3].sum():.3f} -> {1000/t[:3].sum():.0f} fps")
     # backward timing
     acc = torch.zeros((cloud.n_points, 8), device="cuda")
     gflat = torch.empty_like(cloud.flat); sn = torch.empty(cloud.n_points, device="cuda"); vis = torch.empty(cloud.n_points, dtype=torch.uint8, device="cuda")

@@ -121,6 +121,11 @@ typedef struct xg_splats {
   int32_t*  tile_order;   /* [n_tiles_x*n_tiles_y] tiles by descending entry
                              count (compositing schedule; written by
                              xg_bin_sort)                                   */
+  int32_t*  unit_cost;    /* [4*n_tiles] entries each 8x8 quarter-tile's
+                             reverse replay walks (written by
+                             xg_composite_fwd; optional)                    */
+  int32_t*  unit_order;   /* [4*n_tiles] quarter-tiles by descending
+                             unit_cost (reverse-replay schedule; scratch)   */
 } xg_splats;
 
 /* Optional float64 API outputs of the projection (frontend.py:58-74); any

@@ -62,6 +62,8 @@ class XgSplats(ctypes.Structure):
         ("n", c_i64),
         ("entry_capacity", c_i64),
         ("tile_order", c_void_p),
+        ("unit_cost", c_void_p),
+        ("unit_order", c_void_p),
     ]
 
 

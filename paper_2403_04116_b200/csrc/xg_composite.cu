@@ -148,6 +148,8 @@ __device__ __forceinline__ Unit make_unit(int tile, int quad, int ntx, int w, in
 // heavy and light units (a shared counter would hand them out in arrival
 // order).  After that, warps pull the remaining (lightest) units from the
 // counter.
+// order: tiles (4 units each, kUnits = false) or units (kUnits = true).
+template <bool kUnits>
 __device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int n_tiles, bool& first,
                                           int& tile, int& quad) {
   const uint32_t n_units = 4u * (uint32_t)n_tiles;
@@ -164,8 +166,14 @@ __device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int 
     k = dealt + __shfl_sync(0xffffffffu, d, 0);
   }
   if (k >= n_units) return false;
-  tile = order[k >> 2];
-  quad = (int)(k & 3u);
+  if (kUnits) {
+    const int uidx = order[k];
+    tile = uidx >> 2;
+    quad = uidx & 3;
+  } else {
+    tile = order[k >> 2];
+    quad = (int)(k & 3u);
+  }
   return true;
 }
 
@@ -183,6 +191,7 @@ struct FwdArgs {
   int* n_contrib;
   const float* target;
   double* l1_sum;
+  int* unit_cost;  // optional: entries each unit's reverse replay will walk
   int ntx, w, h;
 };
 
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
   int* kk = s_k[warp];
   int tile, quad;
   bool first = true;
-  while (next_unit(a.order, a.work, a.n_tiles, first, tile, quad)) {
+  while (next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     float T0 = u.in0 ? 1.f : 0.f, T1 = u.in1 ? 1.f : 0.f;
     float acc0 = 0.f, acc1 = 0.f;
@@ -271,7 +280,39 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
       for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
       if (lane == 0) atomicAdd(a.l1_sum, (double)l1);
     }
+    if (kTrack && a.unit_cost) {
+      int wl = max(last0, last1) + 1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+      if (lane == 0) a.unit_cost[4 * tile + quad] = wl;
+    }
   }
+}
+
+// Units (quarter tiles) by descending reverse-replay cost, 64 log buckets.
+__global__ void __launch_bounds__(1024) k_unit_order(const int* __restrict__ cost, int n_units,
+                                                     int* __restrict__ order) {
+  constexpr int NB = 64;
+  __shared__ int hist[NB];
+  __shared__ int off[NB];
+  if (threadIdx.x < NB) hist[threadIdx.x] = 0;
+  __syncthreads();
+  auto key = [&](int u) {
+    const int c = cost[u];
+    const int b = c > 0 ? (int)(4.f * __log2f((float)c + 1.f)) : 0;
+    return NB - 1 - min(b, NB - 1);
+  };
+  for (int u = threadIdx.x; u < n_units; u += blockDim.x) atomicAdd(&hist[key(u)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int b = 0; b < NB; ++b) {
+      off[b] = run;
+      run += hist[b];
+    }
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < n_units; u += blockDim.x) order[atomicAdd(&off[key(u)], 1)] = u;
 }
 
 // Tiles by descending entry count (64 log-spaced buckets; order within a
@@ -313,6 +354,7 @@ struct BwdArgs {
   const int* order;
   uint32_t* work;
   int n_tiles;
+  bool unit_order;  // order lists units (by reverse-replay cost) instead of tiles
   const float* t_final;
   const int* n_contrib;
   const float* dl;       // upstream dL/dI, or null -> fused L1
@@ -438,7 +480,8 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   uint32_t* gid = s_gid[warp];
   int tile, quad;
   bool first = true;
-  while (next_unit(a.order, a.work, a.n_tiles, first, tile, quad)) {
+  while (a.unit_order ? next_unit<true>(a.order, a.work, a.n_tiles, first, tile, quad)
+                      : next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
     float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
@@ -632,7 +675,8 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
   cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
   FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
-            target, l1_sum, tiles_x(*cam), cam->width, cam->height};
+            target, l1_sum, (t_final && n_contrib) ? sp->unit_cost : nullptr, tiles_x(*cam), cam->width,
+            cam->height};
   // (an image-only variant without the contributor tracking measured
   // slower on B200 - 0.71 vs 0.66 ms at C3 - so every launch tracks)
   k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0,
@@ -654,9 +698,17 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
   uint32_t* work = sp->counters + XG_CTR_QUEUE;
   cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
+  // schedule the reverse replay by the per-unit cost the forward recorded
+  const bool by_unit = sp->unit_cost && sp->unit_order;
+  if (by_unit) {
+    k_unit_order<<<1, 1024, 0, (cudaStream_t)stream>>>(sp->unit_cost, 4 * n_tiles, sp->unit_order);
+    xg_status st = check_launch("k_unit_order");
+    if (st != XG_OK) return st;
+  }
   BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
-            (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, t_final, n_contrib, dl_dimage,
-            image, target, l1_scale, grad_acc, tiles_x(*cam), cam->width, cam->height};
+            (const long long*)sp->tile_ranges, by_unit ? sp->unit_order : sp->tile_order, work, n_tiles, by_unit,
+            t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc, tiles_x(*cam), cam->width,
+            cam->height};
   k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
 }

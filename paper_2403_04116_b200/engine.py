@@ -48,6 +48,8 @@ class Frame:
         self.order = torch.empty(n, dtype=torch.int32, device=dev)
         self.tile_ranges = torch.empty((self.n_tiles, 2), dtype=torch.int64, device=dev)
         self.tile_order = torch.empty(self.n_tiles, dtype=torch.int32, device=dev)
+        self.unit_cost = torch.empty(4 * self.n_tiles, dtype=torch.int32, device=dev)
+        self.unit_order = torch.empty(4 * self.n_tiles, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(nat.XG_NCOUNTERS, dtype=torch.int32, device=dev)
         self.image = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
@@ -93,6 +95,8 @@ class Frame:
         s.n = self.n
         s.entry_capacity = self.entry_capacity
         s.tile_order = self.tile_order.data_ptr()
+        s.unit_cost = self.unit_cost.data_ptr()
+        s.unit_order = self.unit_order.data_ptr()
         return s
 
     # --- stages -------------------------------------------------------------

@@ -133,32 +133,175 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused duplicate + stable tile sort ("multisplit" counting sort).  The
+// depth-sorted Gaussians are cut into chunks of kBinChunk (one CTA each);
+// every Gaussian contributes one entry per tile of its rect.  Pass 1 counts
+// entries per (tile, chunk); an exclusive scan over the tile-major table
+// gives each (tile, chunk) its output base - and the tile ranges for free.
+// Pass 2 re-enumerates the chunk's entries in (depth, rect) order and ranks
+// them stably per tile (per-warp counters + __match_any_sync within each
+// 32-entry round), writing entry_splat[] directly in (tile, depth, index)
+// order.  Replaces writing E (key, value) pairs and two radix passes over
+// them with one read of the rects and one write of the values.
+// ---------------------------------------------------------------------------
+constexpr int kBinThreads = 256;
+constexpr int kBinWarps = kBinThreads / 32;
+constexpr int kBinRounds = 4;                                  // 32-Gaussian rounds per warp
+constexpr int kBinChunk = kBinThreads * kBinRounds;            // Gaussians per CTA
+constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
+
+__global__ void __launch_bounds__(kBinThreads)
+    k_bin_count(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
+                const ushort4* __restrict__ rect, long long n, int ntx, int T, uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t cnt[];  // [T]
+  for (int t = threadIdx.x; t < T; t += kBinThreads) cnt[t] = 0;
+  __syncthreads();
+  const long long lo = (long long)blockIdx.x * kBinChunk;
+  const long long hi = lo + kBinChunk < n ? lo + kBinChunk : n;
+  for (long long s = lo + threadIdx.x; s < hi; s += kBinThreads) {
+    const uint32_t g = order[s];
+    if (n_tiles[g] == 0) continue;
+    const ushort4 r = rect[g];
+    for (int ty = r.y; ty <= r.w; ++ty)
+      for (int tx = r.x; tx <= r.z; ++tx) atomicAdd(&cnt[ty * ntx + tx], 1u);
+  }
+  __syncthreads();
+  const int C = gridDim.x;
+  for (int t = threadIdx.x; t < T; t += kBinThreads) hist[(long long)t * C + blockIdx.x] = cnt[t];
+}
+
+__global__ void k_flag_overflow(uint32_t* counters, long long cap) {
+  if (threadIdx.x == 0 && (long long)counters[XG_CTR_ENTRIES] > cap)
+    atomicOr(&counters[XG_CTR_STATUS], XG_ST_ENTRY_OVERFLOW);
+}
+
+__global__ void k_bin_ranges(const uint32_t* __restrict__ offs, int C, int T, const uint32_t* counters,
+                             long long* __restrict__ ranges) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  ranges[2 * t] = offs[(long long)t * C];
+  ranges[2 * t + 1] = t + 1 < T ? (long long)offs[(long long)(t + 1) * C] : (long long)counters[XG_CTR_ENTRIES];
+}
+
+__global__ void __launch_bounds__(kBinThreads)
+    k_bin_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
+               const ushort4* __restrict__ rect, long long n, int ntx, int T,
+               const uint32_t* __restrict__ offs, long long cap, uint32_t* __restrict__ entry_splat) {
+  extern __shared__ uint32_t wcnt[];  // [kBinWarps][T]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = gridDim.x;
+  for (int i = threadIdx.x; i < kBinWarps * T; i += kBinThreads) wcnt[i] = 0;
+  __syncthreads();
+  uint32_t* mine = wcnt + warp * T;
+  const long long wlo = (long long)blockIdx.x * kBinChunk + (long long)warp * 32 * kBinRounds;
+  // phase 1: per-warp entry counts per tile
+  for (int rd = 0; rd < kBinRounds; ++rd) {
+    const long long s = wlo + rd * 32 + lane;
+    if (s < n) {
+      const uint32_t g = order[s];
+      if (n_tiles[g]) {
+        const ushort4 r = rect[g];
+        for (int ty = r.y; ty <= r.w; ++ty)
+          for (int tx = r.x; tx <= r.z; ++tx) atomicAdd(&mine[ty * ntx + tx], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  // phase 2: global base of every (warp, tile) run
+  for (int t = threadIdx.x; t < T; t += kBinThreads) {
+    uint32_t run = offs[(long long)t * C + blockIdx.x];
+    for (int w = 0; w < kBinWarps; ++w) {
+      const uint32_t c = wcnt[w * T + t];
+      wcnt[w * T + t] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // phase 3: enumerate entries in (depth, rect row-major) order, rank per tile
+  const unsigned lt = lanemask_lt();
+  for (int rd = 0; rd < kBinRounds; ++rd) {
+    const long long s = wlo + rd * 32 + lane;
+    uint32_t g = 0, cnt = 0;
+    ushort4 r = make_ushort4(0, 0, 0, 0);
+    if (s < n) {
+      g = order[s];
+      cnt = n_tiles[g];
+      if (cnt) r = rect[g];
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - cnt;
+    const int wdt = cnt ? (int)(r.z - r.x + 1) : 1;
+    for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = lo + step;
+        const uint32_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+        if (cand < 32 && ex <= e) lo = cand;
+      }
+      const uint32_t j = e - __shfl_sync(0xffffffffu, excl, lo);
+      const int ow = __shfl_sync(0xffffffffu, wdt, lo);
+      const int ox = __shfl_sync(0xffffffffu, (int)r.x, lo);
+      const int oy = __shfl_sync(0xffffffffu, (int)r.y, lo);
+      const uint32_t og = __shfl_sync(0xffffffffu, g, lo);
+      const bool valid = e < total;
+      const int t = valid ? (oy + (int)(j / (uint32_t)ow)) * ntx + ox + (int)(j % (uint32_t)ow) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, t);
+      const uint32_t base = valid ? mine[t] : 0u;
+      if (valid) {
+        const long long pos = (long long)base + __popc(peers & lt);
+        if (pos < cap) entry_splat[pos] = og;
+      }
+      __syncwarp();
+      if (valid && (peers >> lane) == 1u) mine[t] = base + __popc(peers);  // highest peer lane
+      __syncwarp();
+    }
+  }
+}
+
 struct BinWs {
   unsigned long long* keyN1;
   uint32_t *valN1, *offN, *keyE0, *keyE1, *valE1;
+  uint32_t *hist, *hoff;  // multisplit path: [T][C] counts and their scan
   void* tail;
   size_t tail_bytes;
 };
 
-size_t tail_bytes(int64_t n, int64_t cap) {
-  size_t a = radix_workspace_bytes(n > cap ? n : cap);
-  size_t b = scan_workspace_bytes(n);
+bool multisplit(int n_tiles) { return n_tiles <= kBinMaxTiles; }
+
+int64_t bin_chunks(int64_t n) { return (n + kBinChunk - 1) / kBinChunk; }
+
+size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
+  size_t a = radix_workspace_bytes(multisplit(n_tiles) ? n : (n > cap ? n : cap));
+  size_t b = scan_workspace_bytes(multisplit(n_tiles) ? (n > n_tiles * bin_chunks(n) ? n : n_tiles * bin_chunks(n)) : n);
   return a > b ? a : b;
 }
 
-bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, BinWs& w) {
+bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, int n_tiles, BinWs& w) {
   char* p = (char*)ws;
   const size_t bn = align_up(sizeof(uint32_t) * (size_t)n);
-  const size_t be = align_up(sizeof(uint32_t) * (size_t)(cap > 0 ? cap : 1));
+  const bool ms = multisplit(n_tiles);
+  const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(cap > 0 ? cap : 1));
+  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles * (size_t)bin_chunks(n)) : 0;
   w.keyN1 = (unsigned long long*)p; p += 2 * bn;
   w.valN1 = (uint32_t*)p; p += bn;
   w.offN = (uint32_t*)p; p += bn;
   w.keyE0 = (uint32_t*)p; p += be;
   w.keyE1 = (uint32_t*)p; p += be;
   w.valE1 = (uint32_t*)p; p += be;
+  w.hist = (uint32_t*)p; p += bh;
+  w.hoff = (uint32_t*)p; p += bh;
   w.tail = p;
   const size_t used = (size_t)(p - (char*)ws);
-  const size_t tb = tail_bytes(n, cap);
+  const size_t tb = tail_bytes(n, cap, n_tiles);
   if (used + tb > bytes) return false;
   w.tail_bytes = bytes - used;
   return true;
@@ -172,10 +315,11 @@ using namespace xg;
 extern "C" {
 
 size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles_total) {
-  (void)n_tiles_total;
   const size_t bn = align_up(sizeof(uint32_t) * (size_t)n);
-  const size_t be = align_up(sizeof(uint32_t) * (size_t)(entry_capacity > 0 ? entry_capacity : 1));
-  return 4 * bn + 3 * be + tail_bytes(n, entry_capacity) + 256;
+  const bool ms = multisplit(n_tiles_total);
+  const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(entry_capacity > 0 ? entry_capacity : 1));
+  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)bin_chunks(n)) : 0;
+  return 4 * bn + 3 * be + 2 * bh + tail_bytes(n, entry_capacity, n_tiles_total) + 256;
 }
 
 xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size_t workspace_bytes,
@@ -187,13 +331,13 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   }
   BinWs w;
   const int64_t n = sp->n, cap = sp->entry_capacity;
-  if (!carve(workspace, workspace_bytes, n, cap, w)) {
+  const int ntx = tiles_x(*cam), nty = tiles_y(*cam);
+  const int n_tiles = ntx * nty;
+  if (!carve(workspace, workspace_bytes, n, cap, n_tiles, w)) {
     set_error_msg("xg_bin_sort: workspace too small");
     return XG_ERR_WORKSPACE;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  const int ntx = tiles_x(*cam), nty = tiles_y(*cam);
-  const int n_tiles = ntx * nty;
   xg_status st;
   // n as a device count for the generic sort: stash it in counters[TOUCH]
   uint32_t* n_dev = sp->counters + XG_CTR_TOUCH;
@@ -207,6 +351,35 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     if ((st = radix_sort_pairs64(keys, vals, n, n_dev, 0, 64, w.tail, w.tail_bytes, s, &res)) != XG_OK)
       return st;
     if (res == 1) cudaMemcpyAsync(sp->order, w.valN1, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
+  }
+  if (multisplit(n_tiles)) {
+    // 2-4. fused duplicate + stable tile sort + ranges
+    const int C = (int)bin_chunks(n);
+    const size_t sm_count = sizeof(uint32_t) * (size_t)n_tiles;
+    const size_t sm_emit = sizeof(uint32_t) * (size_t)kBinWarps * n_tiles;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_bin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(uint32_t) * kBinWarps * kBinMaxTiles));
+      attr_set = true;
+    }
+    k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
+                                                 w.hist);
+    if ((st = check_launch("k_bin_count")) != XG_OK) return st;
+    const long long hn = (long long)n_tiles * C;
+    if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
+                       w.tail_bytes, s)) != XG_OK)
+      return st;
+    k_bin_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(w.hoff, C, n_tiles, sp->counters,
+                                                      (long long*)sp->tile_ranges);
+    if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
+    k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
+                                               w.hoff, cap, sp->entry_splat);
+    if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
+    k_flag_overflow<<<1, 32, 0, s>>>(sp->counters, cap);
+    if ((st = check_launch("k_flag_overflow")) != XG_OK) return st;
+    if (!sp->tile_order) return XG_OK;
+    return launch_tile_order(sp->tile_ranges, n_tiles, sp->tile_order, s);
   }
   // 2. offsets of every Gaussian's entries, in depth order
   if ((st = scan_u32(sp->n_tiles, sp->order, w.offN, n, nullptr, n, sp->counters + XG_CTR_ENTRIES,

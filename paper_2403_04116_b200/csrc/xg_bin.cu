@@ -281,6 +281,8 @@ int64_t bin_chunks(int64_t n) { return (n + kBinChunk - 1) / kBinChunk; }
 
 size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   size_t a = radix_workspace_bytes(multisplit(n_tiles) ? n : (n > cap ? n : cap));
+  const size_t o = onesweep_workspace_bytes(n);
+  if (o > a) a = o;
   size_t b = scan_workspace_bytes(multisplit(n_tiles) ? (n > n_tiles * bin_chunks(n) ? n : n_tiles * bin_chunks(n)) : n);
   return a > b ? a : b;
 }
@@ -347,10 +349,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   {
     unsigned long long* keys[2] = {(unsigned long long*)sp->depth_key, w.keyN1};
     uint32_t* vals[2] = {sp->order, w.valN1};
-    int res = 0;
-    if ((st = radix_sort_pairs64(keys, vals, n, n_dev, 0, 64, w.tail, w.tail_bytes, s, &res)) != XG_OK)
-      return st;
-    if (res == 1) cudaMemcpyAsync(sp->order, w.valN1, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
+    if ((st = onesweep_sort_pairs64(keys, vals, n, n_dev, w.tail, w.tail_bytes, s)) != XG_OK) return st;
   }
   if (multisplit(n_tiles)) {
     // 2-4. fused duplicate + stable tile sort + ranges

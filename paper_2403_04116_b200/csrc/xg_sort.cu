@@ -16,7 +16,7 @@ constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortRounds = 16;                        // 32-item rounds per warp
+constexpr int kSortRounds = 4;                         // 32-item rounds per warp
 constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096
 
 constexpr unsigned long long kFlagAgg = 1ull << 32;
@@ -344,6 +344,249 @@ xg_status radix_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int
                              cudaStream_t s, int* result) {
   return radix_sort_impl<unsigned long long>(keys, vals, cap, n_dev, begin_bit, end_bit, ws, ws_bytes, s,
                                              result);
+}
+
+// ---------------------------------------------------------------------------
+// Onesweep-style LSD radix sort of (uint64 key, uint32 value) pairs: one
+// histogram kernel for all passes, then ONE kernel per 8-bit pass in which
+// each tile ranks its keys locally, publishes per-digit counts and finds its
+// global digit offsets by decoupled look-back over the preceding tiles - no
+// separate histogram/scan launches per pass.  Passes whose digit is the same
+// for every key (e.g. the constant exponent byte of depths) are skipped on
+// the device; the ping-pong buffer each pass reads is chosen on the device.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kOsThreads = 256;
+constexpr int kOsWarps = kOsThreads / 32;
+constexpr int kOsRounds = 8;
+constexpr int kOsTile = kOsThreads * kOsRounds;  // 2048 items
+constexpr int kOsPasses = 8;
+constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsMask = (1u << 30) - 1u;
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kOsThreads)
+    k_os_hist(const unsigned long long* __restrict__ keys, const uint32_t* n_dev, long long cap,
+              uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kOsPasses][256];
+  for (int i = threadIdx.x; i < kOsPasses * 256; i += kOsThreads) (&h[0][0])[i] = 0;
+  __syncthreads();
+  long long n = *n_dev;
+  if (n > cap) n = cap;
+  for (long long i = (long long)blockIdx.x * kOsThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kOsThreads) {
+    const unsigned long long k = keys[i];
+#pragma unroll
+    for (int p = 0; p < kOsPasses; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kOsPasses * 256; i += kOsThreads) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(&ghist[i], v);
+  }
+}
+
+// exclusive offsets per pass, and the buffer each pass reads (sel[p]);
+// sel[kOsPasses] is where the result lands
+__global__ void __launch_bounds__(256) k_os_scan(const uint32_t* __restrict__ ghist, uint32_t* __restrict__ gofs,
+                                                 const uint32_t* n_dev, long long cap, int* __restrict__ sel) {
+  __shared__ uint32_t s[256];
+  __shared__ int trivial[kOsPasses];
+  long long n = *n_dev;
+  if (n > cap) n = cap;
+  const int d = threadIdx.x;
+  for (int p = 0; p < kOsPasses; ++p) {
+    const uint32_t v = ghist[p * 256 + d];
+    const int t = __syncthreads_or((long long)v == n);
+    if (d == 0) trivial[p] = t;
+    s[d] = v;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele
+      const uint32_t x = d >= o ? s[d - o] : 0u;
+      __syncthreads();
+      s[d] += x;
+      __syncthreads();
+    }
+    gofs[p * 256 + d] = s[d] - v;
+    __syncthreads();
+  }
+  if (d == 0) {
+    int cur = 0;
+    for (int p = 0; p < kOsPasses; ++p) {
+      sel[p] = cur;
+      if (!trivial[p]) cur = 1 - cur;
+    }
+    sel[kOsPasses] = cur;
+  }
+}
+
+struct OsArgs {
+  unsigned long long* keys[2];
+  uint32_t* vals[2];
+  const uint32_t* n_dev;
+  long long cap;
+  int pass;
+  const uint32_t* ghist;
+  const uint32_t* gofs;
+  const int* sel;
+  uint32_t* status;    // [tiles][256] for this pass, zeroed
+  uint32_t* tile_ctr;  // zeroed
+};
+
+__global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
+  __shared__ uint32_t wh[kOsWarps][256];
+  __shared__ uint32_t s_pre[256];
+  __shared__ uint32_t s_tile;
+  long long n = *a.n_dev;
+  if (n > a.cap) n = a.cap;
+  const int p = a.pass;
+  // a pass whose digit is constant over all keys is the identity: skip it
+  if (a.sel[p + 1] == a.sel[p]) return;
+  const int src = a.sel[p];
+  const int shift = 8 * p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kOsWarps * 256; i += kOsThreads) (&wh[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const long long base = (long long)tile * kOsTile;
+  if (base >= n) return;
+  const unsigned long long* kin = a.keys[src];
+  const uint32_t* vin = a.vals[src];
+  const unsigned lt = lanemask_lt();
+  unsigned long long key[kOsRounds];
+  uint32_t val[kOsRounds], pos[kOsRounds];
+  const long long seg = base + (long long)warp * (kOsTile / kOsWarps);
+#pragma unroll
+  for (int r = 0; r < kOsRounds; ++r) {
+    const long long idx = seg + r * 32 + lane;
+    const bool valid = idx < n;
+    key[r] = valid ? kin[idx] : 0ull;
+    val[r] = valid ? vin[idx] : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kOsRounds; ++r) {
+    const long long idx = seg + r * 32 + lane;
+    const bool valid = idx < n;
+    const uint32_t d = valid ? (uint32_t)(key[r] >> shift) & 255u : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = wh[warp][valid ? d : 0];
+    pos[r] = before + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (peers >> lane) == 1u) wh[warp][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // 256 threads = 256 digits
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kOsWarps; ++w) {
+      const uint32_t t = wh[w][d];
+      wh[w][d] = run;
+      run += t;
+    }
+    uint32_t* st = a.status + (long long)tile * 256;
+    if (tile == 0) {
+      asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(st + d), "r"(kOsPre | run) : "memory");
+      s_pre[d] = 0;
+    } else {
+      asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(st + d), "r"(kOsAgg | run) : "memory");
+      uint32_t prefix = 0;
+      long long j = (long long)tile - 1;
+      for (;;) {
+        uint32_t v;
+        do {
+          v = ld_volatile_u32(a.status + j * 256 + d);
+        } while ((v & ~kOsMask) == 0);
+        prefix += v & kOsMask;
+        if ((v & ~kOsMask) == kOsPre) break;
+        --j;
+      }
+      asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(st + d), "r"(kOsPre | (prefix + run)) : "memory");
+      s_pre[d] = prefix;
+    }
+  }
+  __syncthreads();
+  unsigned long long* kout = a.keys[1 - src];
+  uint32_t* vout = a.vals[1 - src];
+  const uint32_t* go = a.gofs + p * 256;
+#pragma unroll
+  for (int r = 0; r < kOsRounds; ++r) {
+    const long long idx = seg + r * 32 + lane;
+    if (idx < n) {
+      const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+      const uint32_t dst = go[d] + s_pre[d] + wh[warp][d] + pos[r];
+      kout[dst] = key[r];
+      vout[dst] = val[r];
+    }
+  }
+}
+
+__global__ void k_os_finish(uint32_t* vals0, const uint32_t* vals1, const uint32_t* n_dev, long long cap,
+                            const int* sel) {
+  if (sel[kOsPasses] == 0) return;
+  long long n = *n_dev;
+  if (n > cap) n = cap;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    vals0[i] = vals1[i];
+}
+
+}  // namespace
+
+size_t onesweep_workspace_bytes(int64_t cap) {
+  const int64_t tiles = (cap + kOsTile - 1) / kOsTile;
+  return align_up(sizeof(uint32_t) * kOsPasses * 256 * 2) + align_up(sizeof(int) * (kOsPasses + 1)) +
+         align_up(sizeof(uint32_t) * kOsPasses) + align_up(sizeof(uint32_t) * (size_t)kOsPasses * tiles * 256) + 256;
+}
+
+xg_status onesweep_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                                void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (cap <= 0) return XG_OK;
+  if (ws_bytes < onesweep_workspace_bytes(cap)) {
+    set_error_msg("onesweep_sort_pairs64: workspace too small");
+    return XG_ERR_WORKSPACE;
+  }
+  const int64_t tiles = (cap + kOsTile - 1) / kOsTile;
+  char* p = (char*)ws;
+  uint32_t* ghist = (uint32_t*)p;
+  uint32_t* gofs = ghist + kOsPasses * 256;
+  p += align_up(sizeof(uint32_t) * kOsPasses * 256 * 2);
+  int* sel = (int*)p;
+  p += align_up(sizeof(int) * (kOsPasses + 1));
+  uint32_t* ctr = (uint32_t*)p;
+  p += align_up(sizeof(uint32_t) * kOsPasses);
+  uint32_t* status = (uint32_t*)p;
+  cudaMemsetAsync(ws, 0, onesweep_workspace_bytes(cap), s);
+  const int hgrid = (int)(tiles < 296 ? tiles : 296);
+  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys[0], n_dev, cap, ghist);
+  xg_status st = check_launch("k_os_hist");
+  if (st != XG_OK) return st;
+  k_os_scan<<<1, 256, 0, s>>>(ghist, gofs, n_dev, cap, sel);
+  if ((st = check_launch("k_os_scan")) != XG_OK) return st;
+  for (int pass = 0; pass < kOsPasses; ++pass) {
+    OsArgs a;
+    a.keys[0] = keys[0];
+    a.keys[1] = keys[1];
+    a.vals[0] = vals[0];
+    a.vals[1] = vals[1];
+    a.n_dev = n_dev;
+    a.cap = cap;
+    a.pass = pass;
+    a.ghist = ghist;
+    a.gofs = gofs;
+    a.sel = sel;
+    a.status = status + (size_t)pass * tiles * 256;
+    a.tile_ctr = ctr + pass;
+    k_os_pass<<<(int)tiles, kOsThreads, 0, s>>>(a);
+    if ((st = check_launch("k_os_pass")) != XG_OK) return st;
+  }
+  k_os_finish<<<(int)(tiles < 296 ? tiles : 296), 256, 0, s>>>(vals[0], vals[1], n_dev, cap, sel);
+  return check_launch("k_os_finish");
 }
 
 }  // namespace xg

@@ -24,4 +24,11 @@ xg_status radix_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int
                              const uint32_t* n_dev, int begin_bit, int end_bit, void* ws, size_t ws_bytes,
                              cudaStream_t s, int* result);
 
+// Onesweep variant for 64-bit keys (all 8 byte passes; constant-digit
+// passes are skipped on the device).  Result always ends in vals[0]
+// (keys end wherever the last executed pass wrote them).
+size_t onesweep_workspace_bytes(int64_t cap);
+xg_status onesweep_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                                void* ws, size_t ws_bytes, cudaStream_t s);
+
 }  // namespace xg

@@ -29,10 +29,14 @@
  * algorithm the engine uses for per-Gaussian sigmoids and scales
  * (Cody-Waite + Taylor-13 Horner with fma), so both sides agree bit for bit.
  */
+#define _GNU_SOURCE
 #include <math.h>
+#include <pthread.h>
+#include <stdatomic.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #define TILE 16
 #define LOG2E 1.4426950408889634073599246810019
@@ -298,44 +302,87 @@ static float pixel_p2(const orec* r, float fx, float fy, float* dxo, float* dyo)
   return fmaf(fmaf(r->C, dy, bdx), dy, adx2);
 }
 
+typedef struct {
+  int32_t h, w;
+  const double* mean2d;
+  const float* coef;
+  const float* inten;
+  const uint32_t* entry_splat;
+  const int64_t* tile_ranges;
+  float* image;
+  float* t_final;
+  int32_t* n_contrib;
+  int32_t* n_traversed;
+  uint8_t* ambiguous;
+  double amb_rel;
+  int n_tiles;
+  _Atomic int next;
+} fwd_job;
+
+static void fwd_tile(const fwd_job* j, int t) {
+  const int ntx = (j->w + TILE - 1) / TILE;
+  const int32_t h = j->h, w = j->w;
+  const int x0 = TILE * (t % ntx), y0 = TILE * (t / ntx);
+  const int64_t start = j->tile_ranges[2 * t], end = j->tile_ranges[2 * t + 1];
+  for (int py = y0; py < y0 + TILE && py < h; ++py)
+    for (int px = x0; px < x0 + TILE && px < w; ++px) {
+      const float fx = (float)(px - x0), fy = (float)(py - y0);
+      float T = 1.0f, acc = 0.0f;
+      int last = -1;
+      int64_t k = start;
+      uint8_t amb = 0;
+      for (; k < end; ++k) {
+        if (fabs((double)T / FLOOR_F - 1.0) < j->amb_rel) amb = 1;
+        if (T < FLOOR_F) break; /* _kernels.pyx:57-58 */
+        orec r = make_rec(j->mean2d, j->coef, j->inten, j->entry_splat[k], x0, y0);
+        float dx, dy;
+        float p2 = pixel_p2(&r, fx, fy, &dx, &dy);
+        if (p2 > 0.0f || p2 < CUT2_F) continue; /* :66-67 */
+        float dens = (float)exp2((double)p2);
+        float sg = r.alpha * dens;
+        if (sg >= CLAMP_F) sg = CLAMP_F; /* :68-70 */
+        float wgt = sg * T;
+        acc = fmaf(r.it, wgt, acc); /* :71 */
+        T = fmaf(-sg, T, T);        /* :72 */
+        last = (int)(k - start);
+      }
+      const int64_t o = (int64_t)py * w + px;
+      j->image[o] = acc;
+      if (j->t_final) j->t_final[o] = T;
+      if (j->n_contrib) j->n_contrib[o] = last + 1;
+      if (j->n_traversed) j->n_traversed[o] = (int32_t)(k - start);
+      if (j->ambiguous) j->ambiguous[o] = amb;
+    }
+}
+
+static void* fwd_worker(void* arg) {
+  fwd_job* j = (fwd_job*)arg;
+  for (int t; (t = atomic_fetch_add(&j->next, 1)) < j->n_tiles;) fwd_tile(j, t);
+  return NULL;
+}
+
+/* Forward blend, _kernels.pyx:41-73 per pixel.  Tiles write disjoint pixels,
+ * so they are spread over XGO_THREADS (default: all online cores) threads;
+ * the result does not depend on the thread count. */
 void xgo_composite_fwd(int32_t h, int32_t w, const double* mean2d, const float* coef, const float* inten,
                        const uint32_t* entry_splat, const int64_t* tile_ranges, float* image,
                        float* t_final, int32_t* n_contrib, int32_t* n_traversed, uint8_t* ambiguous,
                        double amb_rel) {
   const int ntx = (w + TILE - 1) / TILE, nty = (h + TILE - 1) / TILE;
-  for (int t = 0; t < ntx * nty; ++t) {
-    const int x0 = TILE * (t % ntx), y0 = TILE * (t / ntx);
-    const int64_t start = tile_ranges[2 * t], end = tile_ranges[2 * t + 1];
-    for (int py = y0; py < y0 + TILE && py < h; ++py)
-      for (int px = x0; px < x0 + TILE && px < w; ++px) {
-        const float fx = (float)(px - x0), fy = (float)(py - y0);
-        float T = 1.0f, acc = 0.0f;
-        int last = -1;
-        int64_t k = start;
-        uint8_t amb = 0;
-        for (; k < end; ++k) {
-          if (fabs((double)T / FLOOR_F - 1.0) < amb_rel) amb = 1;
-          if (T < FLOOR_F) break; /* _kernels.pyx:57-58 */
-          orec r = make_rec(mean2d, coef, inten, entry_splat[k], x0, y0);
-          float dx, dy;
-          float p2 = pixel_p2(&r, fx, fy, &dx, &dy);
-          if (p2 > 0.0f || p2 < CUT2_F) continue; /* :66-67 */
-          float dens = (float)exp2((double)p2);
-          float sg = r.alpha * dens;
-          if (sg >= CLAMP_F) sg = CLAMP_F; /* :68-70 */
-          float wgt = sg * T;
-          acc = fmaf(r.it, wgt, acc); /* :71 */
-          T = fmaf(-sg, T, T);        /* :72 */
-          last = (int)(k - start);
-        }
-        const int64_t o = (int64_t)py * w + px;
-        image[o] = acc;
-        if (t_final) t_final[o] = T;
-        if (n_contrib) n_contrib[o] = last + 1;
-        if (n_traversed) n_traversed[o] = (int32_t)(k - start);
-        if (ambiguous) ambiguous[o] = amb;
-      }
+  fwd_job j = {h, w, mean2d, coef, inten, entry_splat, tile_ranges, image, t_final, n_contrib, n_traversed,
+               ambiguous, amb_rel, ntx * nty, 0};
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  const char* env = getenv("XGO_THREADS");
+  if (env && atoi(env) > 0) nt = atoi(env);
+  if (nt > 64) nt = 64;
+  if (nt > j.n_tiles / 4) nt = j.n_tiles / 4;
+  if (nt <= 1) {
+    fwd_worker(&j);
+    return;
   }
+  pthread_t th[64];
+  for (long i = 0; i < nt; ++i) pthread_create(&th[i], NULL, fwd_worker, &j);
+  for (long i = 0; i < nt; ++i) pthread_join(th[i], NULL);
 }
 
 /* Gradient pass (_kernels.pyx:121-177) in float64 on the float32 forward's

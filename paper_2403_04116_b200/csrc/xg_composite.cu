@@ -47,14 +47,18 @@ struct Rec {
 // (tile-relative) compared against the cut-off.  The maximiser lies on the
 // edge facing the mean (or is the mean), so checking the two clamped edge
 // maxima is exact.
-__device__ __forceinline__ bool overlaps(const Rec& r, float xa, float xb, float ya, float yb) {
-  const float mx = r.a.x, my = r.a.y, A = r.a.z, B = r.a.w, C = r.b.x;
-  if (!(A < 0.f) || !(C < 0.f)) return true;
+__device__ __forceinline__ bool overlaps(float mx, float my, float A, float B, float C, float xa, float xb, float ya,
+                                         float yb) {
+  if (!(A < -1e-30f) || !(C < -1e-30f)) return true;  // (keeps the reciprocals below finite)
+  // (the edge maximiser's location only needs to be close: a misplaced
+  // point lowers the computed max by O(error^2), far inside kCullMargin, so
+  // the approximate MUFU.RCP division is safe - the IEEE division's slow
+  // path used to cost a fifth of the kernel's instructions)
   const float dx1 = fminf(fmaxf(mx, xa), xb) - mx;
-  const float dy1 = fminf(fmaxf(-B * dx1 / (2.f * C), ya - my), yb - my);
+  const float dy1 = fminf(fmaxf(__fdividef(-B * dx1, 2.f * C), ya - my), yb - my);
   const float p1 = A * dx1 * dx1 + B * dx1 * dy1 + C * dy1 * dy1;
   const float dy2 = fminf(fmaxf(my, ya), yb) - my;
-  const float dx2 = fminf(fmaxf(-B * dy2 / (2.f * A), xa - mx), xb - mx);
+  const float dx2 = fminf(fmaxf(__fdividef(-B * dy2, 2.f * A), xa - mx), xb - mx);
   const float p2 = A * dx2 * dx2 + B * dx2 * dy2 + C * dy2 * dy2;
   return fmaxf(p1, p2) >= kCut2 - kCullMargin;
 }
@@ -94,7 +98,7 @@ __device__ __forceinline__ int compact(const Raw& raw, int krel, double x0, doub
   if (raw.valid) {
     r.a = make_float4((float)(raw.m.x - x0), (float)(raw.m.y - y0), raw.c.x, raw.c.y);
     r.b = make_float4(raw.c.z, raw.c.w, raw.it, 0.f);
-    keep = overlaps(r, xa, xb, ya, yb);
+    keep = overlaps(r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, xa, xb, ya, yb);
   }
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   if (may_clamp) *may_clamp = __any_sync(0xffffffffu, keep && !(r.b.y < kNoClampAlpha));
@@ -195,67 +199,152 @@ struct FwdArgs {
   int ntx, w, h;
 };
 
-// One pixel, one entry: the blend step of _kernels.pyx:57-72.  kTrack
-// records the last blended entry (n_contrib, needed by the backward);
-// kMayClamp keeps the sigma <= 0.99 clamp (only alpha >= 0.99 can reach it).
-template <bool kTrack, bool kMayClamp>
-__device__ __forceinline__ void blend(float dy, float bdx, float adx2, const Rec& r, int krel,
-                                      float& T, float& acc, int& last) {
-  const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
-  const float dens = ex2_approx(p2);
-  float sg = __fmul_rn(r.b.y, dens);
-  if (kMayClamp) sg = fminf(sg, kClamp);
-  const bool ok = (p2 <= 0.f) & (p2 >= kCut2) & (T >= kFloor);
-  sg = ok ? sg : 0.f;
-  const float w = __fmul_rn(sg, T);
-  acc = __fmaf_rn(r.b.z, w, acc);
-  T = __fmaf_rn(-sg, T, T);
-  if (kTrack) last = ok ? krel : last;
+// Forward records in shared memory, signs folded so that every per-pixel
+// step of the lane's two pixels is ONE packed FP32x2 instruction (sm_100
+// FADD2 / FFMA2 / FMUL2, two IEEE round-to-nearest results per issue slot):
+//   dy = fy + (-my)           == fy - my
+//   s  = (-alpha) * 2^p2      == -sigma
+//   w  = s * T                == -(sigma T)
+//   acc = fma(-i, w, acc)     == fma(i, sigma T, acc)
+//   T   = fma(s, T, T)        == fma(-sigma, T, T)
+// - bit for bit the reference-order float32 operations the oracle performs.
+struct FRec {
+  float4 a;  // mx (tile-relative), -my, A2, B2
+  float4 b;  // C2, -alpha, -intensity, 0
+};
+
+// The p2 <= 0 test can be dropped for a splat whose quadratic form
+// M = -[[A2, B2/2], [B2/2, C2]] is positive definite with
+// lambda_min / lambda_max > 2.0000001 u (u = 2^-24): the computed
+// p2 = fma(fma(C2, dy, B2 dx), dy, (A2 dx) dx) differs from the exact form
+// by at most 2.0000001 u lambda_max |v|^2 (five roundings), so it cannot
+// round above zero.  lambda_min / lambda_max >= det / tr^2;
+// the float test det >= 1e-6 tr^2 leaves a 7x margin over the rounding of
+// det and tr themselves.
+__device__ __forceinline__ bool well_conditioned(float A, float B, float C) {
+  const float det = A * C - 0.25f * B * B;
+  const float tr = A + C;
+  return (A < 0.f) && (C < 0.f) && (det < INFINITY) && (det >= 1e-6f * tr * tr);
 }
 
-template <bool kTrack, bool kMayClamp>
-__device__ __forceinline__ void blend_batch(const Rec* rec, const int* kk, int cnt, const Unit& u, float& T0,
-                                            float& T1, float& acc0, float& acc1, int& last0, int& last1) {
-  for (int q = 0; q < cnt; ++q) {
-    const Rec r = rec[q];
-    const int krel = kTrack ? kk[q] : 0;
-    const float dx = __fsub_rn(u.fx, r.a.x);
-    const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-    const float bdx = __fmul_rn(r.a.w, dx);
-    blend<kTrack, kMayClamp>(__fsub_rn(u.fy0, r.a.y), bdx, adx2, r, krel, T0, acc0, last0);
-    blend<kTrack, kMayClamp>(__fsub_rn(u.fy1, r.a.y), bdx, adx2, r, krel, T1, acc1, last1);
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+
+// One splat, the lane's two pixels: the blend step of _kernels.pyx:57-72.
+// kGeneral keeps the sigma <= 0.99 clamp (only alpha >= 0.99 can reach it)
+// and the p2 <= 0 test (only ill-conditioned splats can need it); both are
+// warp-uniform per batch.  Records the last blended entry (n_contrib).
+template <bool kGeneral>
+__device__ __forceinline__ void blend2(const FRec& r, int krel, float fx, float2 fy, float2& T, float2& acc,
+                                       int& last0, int& last1) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+  const float bdx = __fmul_rn(r.a.w, dx);
+  const float2 dy = __fadd2_rn(fy, bc(r.a.y));
+  const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
+  float2 sg = __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
+  if (kGeneral) {
+    sg.x = fmaxf(sg.x, -kClamp);
+    sg.y = fmaxf(sg.y, -kClamp);
   }
+  bool ok0 = (p.x >= kCut2) & (T.x >= kFloor);
+  bool ok1 = (p.y >= kCut2) & (T.y >= kFloor);
+  if (kGeneral) {
+    ok0 &= p.x <= 0.f;
+    ok1 &= p.y <= 0.f;
+  }
+  sg.x = ok0 ? sg.x : 0.f;
+  sg.y = ok1 ? sg.y : 0.f;
+  const float2 w = __fmul2_rn(sg, T);
+  acc = __ffma2_rn(bc(r.b.z), w, acc);
+  T = __ffma2_rn(sg, T, T);
+  last0 = ok0 ? krel : last0;
+  last1 = ok1 ? krel : last1;
+}
+
+// Record half of the gather (the entry index is loaded one batch earlier).
+__device__ __forceinline__ Raw fetch(uint32_t g, bool valid, const double2* __restrict__ mean2d,
+                                     const float4* __restrict__ coef, const float* __restrict__ inten) {
+  Raw r;
+  r.valid = valid;
+  r.g = g;
+  if (valid) {
+    r.m = __ldg(mean2d + g);
+    r.c = __ldg(coef + g);
+    r.it = __ldg(inten + g);
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint32_t entry_at(const uint32_t* __restrict__ entry, long long k, long long hi) {
+  return k < hi ? __ldg(entry + k) : 0u;
+}
+
+// Re-base, cull against the warp's sub-block, ballot-compact the survivors
+// into the warp's shared slice.  general = some survivor needs the clamp or
+// the p2 <= 0 test.
+__device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit& u, FRec* s_rec, int* s_k,
+                                           bool& general) {
+  FRec r;
+  bool keep = false, gen = false;
+  if (raw.valid) {
+    const float mx = (float)(raw.m.x - (double)u.x0), my = (float)(raw.m.y - (double)u.y0);
+    const float A = raw.c.x, B = raw.c.y, C = raw.c.z, alpha = raw.c.w;
+    keep = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya, u.yb);
+    gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
+    r.a = make_float4(mx, -my, A, B);
+    r.b = make_float4(C, -alpha, -raw.it, 0.f);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  general = __any_sync(0xffffffffu, keep && gen);
+  if (keep) {
+    const int pos = __popc(bal & lanemask_lt());
+    s_rec[pos] = r;
+    s_k[pos] = krel;
+  }
+  __syncwarp();
+  return __popc(bal);
+}
+
+template <bool kGeneral>
+__device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, float2 fy,
+                                            float2& T, float2& acc, int& last0, int& last1) {
+#pragma unroll 4
+  for (int q = 0; q < cnt; ++q) blend2<kGeneral>(rec[q], kk[q], fx, fy, T, acc, last0, last1);
 }
 
 template <bool kTrack>
 __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
-  __shared__ Rec s_rec[kWarps][32];
+  __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Rec* rec = s_rec[warp];
+  FRec* rec = s_rec[warp];
   int* kk = s_k[warp];
   int tile, quad;
   bool first = true;
   while (next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
-    float T0 = u.in0 ? 1.f : 0.f, T1 = u.in1 ? 1.f : 0.f;
-    float acc0 = 0.f, acc1 = 0.f;
+    const float2 fy = make_float2(u.fy0, u.fy1);
+    float2 T = make_float2(u.in0 ? 1.f : 0.f, u.in1 ? 1.f : 0.f);
+    float2 acc = make_float2(0.f, 0.f);
     int last0 = -1, last1 = -1;
     bool alive = __any_sync(0xffffffffu, u.in0 || u.in1);
-    Raw nxt = gather(u.start + lane, u.start, u.end, a.entry, a.mean2d, a.coef, a.inten);
+    // two-stage prefetch: entry indices one batch ahead of the records
+    Raw nxt = fetch(entry_at(a.entry, u.start + lane, u.end), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
+    uint32_t g_nxt = entry_at(a.entry, u.start + 32 + lane, u.end);
     for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
       const Raw cur = nxt;
-      bool may_clamp;
-      const int cnt = compact(cur, (int)(b0 - u.start) + lane, u.x0, u.y0, u.xa, u.xb, u.ya, u.yb, rec, kk,
-                              nullptr, &may_clamp);
-      nxt = gather(b0 + 32 + lane, u.start, u.end, a.entry, a.mean2d, a.coef, a.inten);  // prefetch
-      if (may_clamp)  // warp-uniform, per batch of 32 entries
-        blend_batch<kTrack, true>(rec, kk, cnt, u, T0, T1, acc0, acc1, last0, last1);
+      bool general;
+      const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
+      nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
+      g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
+      if (general)  // warp-uniform, per batch of 32 entries
+        blend_batch<true>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
       else
-        blend_batch<kTrack, false>(rec, kk, cnt, u, T0, T1, acc0, acc1, last0, last1);
+        blend_batch<false>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
       __syncwarp();
-      alive = __any_sync(0xffffffffu, (T0 >= kFloor) || (T1 >= kFloor));
+      alive = __any_sync(0xffffffffu, (T.x >= kFloor) || (T.y >= kFloor));
     }
+    const float acc0 = acc.x, acc1 = acc.y, T0 = T.x, T1 = T.y;
     const long long o0 = (long long)u.py0 * a.w + u.px;
     float l1 = 0.f;
     if (u.in0) {

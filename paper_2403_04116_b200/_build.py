@@ -72,5 +72,34 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def variant_path(name: str) -> Path:
+    return PKG / "csrc" / "_variants" / f"libxgauss_{name}.so"
+
+
+def build_variant(name: str, defines: list[str]) -> Path:
+    """A tuning build of the library with extra -D flags (development aid:
+    loaded instead of libxgauss.so when XG_LIB_VARIANT=name)."""
+    out_dir = PKG / "csrc" / "_variants" / name
+    out_dir.mkdir(parents=True, exist_ok=True)
+    cc = nvcc()
+    dflags = [f"-D{d}" for d in defines]
+
+    def compile_one(src: str) -> Path:
+        out = out_dir / (Path(src).stem + ".o")
+        cmd = [cc, *ARCH, *COMMON, *dflags, *PER_FILE.get(src, []), "-c", str(CSRC / src), "-o", str(out)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+        return out
+
+    with ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    lib = variant_path(name)
+    r = subprocess.run([cc, *ARCH, "-shared", "-o", str(lib), *map(str, objs)], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
+    return lib
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

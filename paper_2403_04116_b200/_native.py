@@ -149,7 +149,13 @@ def load_library() -> ctypes.CDLL:
             f"{LIB_PATH} missing: build it with `python -m paper_2403_04116_b200._build` "
             "(the engine has no CPU fallback)"
         )
-    lib = ctypes.CDLL(str(LIB_PATH))
+    path = LIB_PATH
+    variant = os.environ.get("XG_LIB_VARIANT")  # development: a tuning build (tools/variants.py)
+    if variant:
+        path = _build.variant_path(variant)
+        if not path.exists():
+            raise NativeError(f"variant library {path} not built")
+    lib = ctypes.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -31,17 +31,26 @@
 namespace xg {
 namespace {
 
-constexpr int kWarps = 8;             // independent warps per CTA
+#ifndef XG_COMPOSITE_WARPS
+#define XG_COMPOSITE_WARPS 4
+#endif
+constexpr int kWarps = XG_COMPOSITE_WARPS;  // independent warps per CTA
+#ifndef XG_FWD_UNROLL
+#define XG_FWD_UNROLL 4
+#endif
+constexpr int kFwdUnroll = XG_FWD_UNROLL;
 constexpr int kThreads = 32 * kWarps;
 constexpr float kCullMargin = 0.05f;
 // kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
 // safety margin for the MUFU.EX2 error the clamp logic is compiled out.
 constexpr float kNoClampAlpha = 0.98999f;
 
-struct Rec {
-  float4 a;  // mx, my (tile-relative), A2, B2
-  float4 b;  // C2, alpha, intensity, 0
-};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Max of the concave p2 over the rectangle of pixel centres [xa,xb]x[ya,yb]
 // (tile-relative) compared against the cut-off.  The maximiser lies on the
@@ -55,10 +64,10 @@ __device__ __forceinline__ bool overlaps(float mx, float my, float A, float B, f
   // the approximate MUFU.RCP division is safe - the IEEE division's slow
   // path used to cost a fifth of the kernel's instructions)
   const float dx1 = fminf(fmaxf(mx, xa), xb) - mx;
-  const float dy1 = fminf(fmaxf(__fdividef(-B * dx1, 2.f * C), ya - my), yb - my);
+  const float dy1 = fminf(fmaxf(-B * dx1 * rcp_approx(2.f * C), ya - my), yb - my);
   const float p1 = A * dx1 * dx1 + B * dx1 * dy1 + C * dy1 * dy1;
   const float dy2 = fminf(fmaxf(my, ya), yb) - my;
-  const float dx2 = fminf(fmaxf(__fdividef(-B * dy2, 2.f * A), xa - mx), xb - mx);
+  const float dx2 = fminf(fmaxf(-B * dy2 * rcp_approx(2.f * A), xa - mx), xb - mx);
   const float p2 = A * dx2 * dx2 + B * dx2 * dy2 + C * dy2 * dy2;
   return fmaxf(p1, p2) >= kCut2 - kCullMargin;
 }
@@ -71,46 +80,6 @@ struct Raw {
   uint32_t g;
   bool valid;
 };
-
-__device__ __forceinline__ Raw gather(long long k, long long lo, long long hi,
-                                      const uint32_t* __restrict__ entry,
-                                      const double2* __restrict__ mean2d,
-                                      const float4* __restrict__ coef, const float* __restrict__ inten) {
-  Raw r;
-  r.valid = k >= lo && k < hi;
-  if (r.valid) {
-    r.g = __ldg(entry + k);
-    r.m = __ldg(mean2d + r.g);
-    r.c = __ldg(coef + r.g);
-    r.it = __ldg(inten + r.g);
-  }
-  return r;
-}
-
-// Re-base, cull against the warp's sub-block and ballot-compact the
-// survivors (ascending entry order) into the warp's shared slice.  Returns
-// the survivor count.
-__device__ __forceinline__ int compact(const Raw& raw, int krel, double x0, double y0, float xa, float xb,
-                                       float ya, float yb, Rec* s_rec, int* s_k, uint32_t* s_gid,
-                                       bool* may_clamp = nullptr) {
-  Rec r;
-  bool keep = false;
-  if (raw.valid) {
-    r.a = make_float4((float)(raw.m.x - x0), (float)(raw.m.y - y0), raw.c.x, raw.c.y);
-    r.b = make_float4(raw.c.z, raw.c.w, raw.it, 0.f);
-    keep = overlaps(r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, xa, xb, ya, yb);
-  }
-  const unsigned bal = __ballot_sync(0xffffffffu, keep);
-  if (may_clamp) *may_clamp = __any_sync(0xffffffffu, keep && !(r.b.y < kNoClampAlpha));
-  if (keep) {
-    const int pos = __popc(bal & lanemask_lt());
-    s_rec[pos] = r;
-    s_k[pos] = krel;
-    if (s_gid) s_gid[pos] = raw.g;
-  }
-  __syncwarp();
-  return __popc(bal);
-}
 
 struct Unit {
   int x0, y0;            // tile origin
@@ -233,7 +202,7 @@ __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
 // kGeneral keeps the sigma <= 0.99 clamp (only alpha >= 0.99 can reach it)
 // and the p2 <= 0 test (only ill-conditioned splats can need it); both are
 // warp-uniform per batch.  Records the last blended entry (n_contrib).
-template <bool kGeneral>
+template <bool kGeneral, bool kTrack>
 __device__ __forceinline__ void blend2(const FRec& r, int krel, float fx, float2 fy, float2& T, float2& acc,
                                        int& last0, int& last1) {
   const float dx = __fsub_rn(fx, r.a.x);
@@ -257,8 +226,10 @@ __device__ __forceinline__ void blend2(const FRec& r, int krel, float fx, float2
   const float2 w = __fmul2_rn(sg, T);
   acc = __ffma2_rn(bc(r.b.z), w, acc);
   T = __ffma2_rn(sg, T, T);
-  last0 = ok0 ? krel : last0;
-  last1 = ok1 ? krel : last1;
+  if (kTrack) {
+    last0 = ok0 ? krel : last0;
+    last1 = ok1 ? krel : last1;
+  }
 }
 
 // Record half of the gather (the entry index is loaded one batch earlier).
@@ -305,15 +276,19 @@ __device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit&
   return __popc(bal);
 }
 
-template <bool kGeneral>
+template <bool kGeneral, bool kTrack>
 __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, float2 fy,
                                             float2& T, float2& acc, int& last0, int& last1) {
-#pragma unroll 4
-  for (int q = 0; q < cnt; ++q) blend2<kGeneral>(rec[q], kk[q], fx, fy, T, acc, last0, last1);
+#pragma unroll kFwdUnroll
+  for (int q = 0; q < cnt; ++q) blend2<kGeneral, kTrack>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last0, last1);
 }
 
+#ifndef XG_FWD_MIN_CTAS
+#define XG_FWD_MIN_CTAS 1
+#endif
+
 template <bool kTrack>
-__global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd(FwdArgs a) {
   __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -338,9 +313,9 @@ __global__ void __launch_bounds__(kThreads) k_composite_fwd(FwdArgs a) {
       nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
       g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
       if (general)  // warp-uniform, per batch of 32 entries
-        blend_batch<true>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
+        blend_batch<true, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
       else
-        blend_batch<false>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
+        blend_batch<false, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
       __syncwarp();
       alive = __any_sync(0xffffffffu, (T.x >= kFloor) || (T.y >= kFloor));
     }
@@ -454,61 +429,73 @@ struct BwdArgs {
   int ntx, w, h;
 };
 
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
+// Backward records (shared memory), signs folded as in the forward:
+// every per-pixel step of the lane's two pixels is one packed FP32x2 op.
+struct BRec {
+  float4 a;  // mx (tile-relative), -my, A2, B2
+  float4 b;  // C2, -alpha, intensity, 0
+};
 
-// Reverse step for one pixel and one entry: the gradient pass of
+// Reverse step of one splat for the lane's two pixels: the gradient pass of
 // _kernels.pyx:142-177 run back to front, with the suffix sum accumulated
 // directly (no acc - prefix - contrib cancellation) and T restored by
-// division by (1 - sigma).  Returns G = dL/dsigma * sigma on unclamped
-// pairs (the reference's g_power) and g * w (the intensity gradient).
-template <bool kMayClamp>
-__device__ __forceinline__ void unblend(float dy, float bdx, float adx2, const Rec& r, bool act, float g,
-                                        float& T, float& S, float& G, float& gw) {
-  const float p2 = __fmaf_rn(__fmaf_rn(r.b.x, dy, bdx), dy, adx2);
-  const float dens = ex2_approx(p2);
-  const float sraw = __fmul_rn(r.b.y, dens);
-  const bool valid = act & (p2 <= 0.f) & (p2 >= kCut2);
-  const bool clamped = kMayClamp && (sraw >= kClamp);
-  const float sg = valid ? (kMayClamp ? fminf(sraw, kClamp) : sraw) : 0.f;
-  const float rc = rcp_approx(1.f - sg);
-  const float Tb = T * rc;
-  const float w = sg * Tb;
-  const float it = r.b.z;
-  gw = g * w;
-  const float dsig = g * fmaf(-S, rc, it * Tb);
-  G = (valid && !clamped) ? dsig * sg : 0.f;
-  S = fmaf(it, w, S);
-  T = valid ? Tb : T;
+// division by (1 - sigma).  Packed state: T, nS = -S (suffix sum), g.
+// Produces, per pixel, nG = -(dL/dsigma * sigma) on unclamped pairs (the
+// reference's g_power) and ngw = -(g * w) (the intensity gradient).
+template <bool kGeneral>
+__device__ __forceinline__ void unblend2(const BRec& r, float2 dy, float bdx, float adx2, bool act0, bool act1,
+                                         float2 g, float2& T, float2& nS, float2& nG, float2& ngw) {
+  const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
+  float2 ns = __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));  // -sigma (raw)
+  bool v0 = act0 & (p.x >= kCut2), v1 = act1 & (p.y >= kCut2);
+  bool c0 = false, c1 = false;
+  if (kGeneral) {
+    v0 &= p.x <= 0.f;
+    v1 &= p.y <= 0.f;
+    c0 = ns.x <= -kClamp;
+    c1 = ns.y <= -kClamp;
+    ns.x = fmaxf(ns.x, -kClamp);
+    ns.y = fmaxf(ns.y, -kClamp);
+  }
+  ns.x = v0 ? ns.x : 0.f;
+  ns.y = v1 ? ns.y : 0.f;
+  const float2 om = __fadd2_rn(bc(1.f), ns);  // 1 - sigma
+  const float2 rc = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+  const float2 Tb = __fmul2_rn(T, rc);        // T before this splat
+  const float2 nw = __fmul2_rn(ns, Tb);       // -(sigma T)
+  ngw = __fmul2_rn(g, nw);
+  const float2 in = __ffma2_rn(nS, rc, __fmul2_rn(bc(r.b.z), Tb));  // i T - S / (1 - sigma)
+  const float2 dsig = __fmul2_rn(g, in);
+  nG = __fmul2_rn(dsig, ns);
+  if (!v0 || c0) nG.x = 0.f;
+  if (!v1 || c1) nG.y = 0.f;
+  nS = __ffma2_rn(bc(r.b.z), nw, nS);
+  T.x = v0 ? Tb.x : T.x;
+  T.y = v1 ? Tb.y : T.y;
 }
 
-// Both pixels of the lane for one splat; returns the lane's 7 partial sums.
-template <bool kMayClamp>
-__device__ __forceinline__ bool unblend_splat(const Rec& r, int krel, float fx, float fy0, float fy1,
-                                              int last0, int last1, float g0, float g1, float& T0,
-                                              float& T1, float& S0, float& S1, float* v) {
+// Both pixels of the lane for one splat; the lane's 7 partial sums (negated:
+// the caller negates the warp totals, which is exact).
+template <bool kGeneral>
+__device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx, float2 fy, int last0, int last1,
+                                              float2 g, float2& T, float2& nS, float* v) {
   const float dx = __fsub_rn(fx, r.a.x);
   const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
   const float bdx = __fmul_rn(r.a.w, dx);
-  const float dy0 = __fsub_rn(fy0, r.a.y), dy1 = __fsub_rn(fy1, r.a.y);
-  float G0, G1, gw0, gw1;
-  unblend<kMayClamp>(dy0, bdx, adx2, r, krel <= last0, g0, T0, S0, G0, gw0);
-  unblend<kMayClamp>(dy1, bdx, adx2, r, krel <= last1, g1, T1, S1, G1, gw1);
-  const float Gs = G0 + G1, gws = gw0 + gw1;
-  const float Gdy0 = G0 * dy0, Gdy1 = G1 * dy1;
-  const float Gdys = Gdy0 + Gdy1;
+  const float2 dy = __fadd2_rn(fy, bc(r.a.y));
+  float2 nG, ngw;
+  unblend2<kGeneral>(r, dy, bdx, adx2, krel <= last0, krel <= last1, g, T, nS, nG, ngw);
+  const float2 Gdy = __fmul2_rn(nG, dy);
+  const float Gs = nG.x + nG.y, Gdys = Gdy.x + Gdy.y;
   v[0] = Gs * dx;
   v[1] = Gdys;
-  v[2] = Gs * (dx * dx);
+  v[2] = v[0] * dx;
   v[3] = Gdys * dx;
-  v[4] = fmaf(Gdy0, dy0, Gdy1 * dy1);
-  v[5] = gws;
+  v[4] = fmaf(Gdy.x, dy.x, Gdy.y * dy.y);
+  v[5] = ngw.x + ngw.y;
   v[6] = Gs;
   v[7] = 0.f;
-  return (Gs != 0.f) | (gws != 0.f);
+  return (Gs != 0.f) | (v[5] != 0.f);
 }
 
 // Sum 16 per-lane values over the warp (two splats' 8-value records); lane l
@@ -553,18 +540,73 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16]) {
   return v[0];
 }
 
+__device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit& u, BRec* s_rec, int* s_k,
+                                           uint32_t* s_gid, bool& general) {
+  BRec r;
+  bool keep = false, gen = false;
+  if (raw.valid) {
+    const float mx = (float)(raw.m.x - (double)u.x0), my = (float)(raw.m.y - (double)u.y0);
+    const float A = raw.c.x, B = raw.c.y, C = raw.c.z, alpha = raw.c.w;
+    keep = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya, u.yb);
+    gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
+    r.a = make_float4(mx, -my, A, B);
+    r.b = make_float4(C, -alpha, raw.it, 0.f);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  general = __any_sync(0xffffffffu, keep && gen);
+  if (keep) {
+    const int pos = __popc(bal & lanemask_lt());
+    s_rec[pos] = r;
+    s_k[pos] = krel;
+    s_gid[pos] = raw.g;
+  }
+  __syncwarp();
+  return __popc(bal);
+}
+
 // Per-splat accumulators (grad_acc[N][8]), per (pixel, entry) pair with
 // G = dL/dsigma * sigma (unclamped pairs) and w = sigma T:
 //   {sum G dx, sum G dy, sum G dx^2, sum G dx dy, sum G dy^2, sum g w, sum G, 0}
 // xg_preprocess_bwd turns them into the reference's g_mean / g_conic /
 // g_int / g_alpha using the splat's own (A2, B2, C2, alpha).  Each warp
 // reduces its 64 pixels per splat and issues two vector reductions.
+template <bool kGeneral>
+__device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, const uint32_t* gid, int cnt,
+                                              const Unit& u, float2 fy, int last0, int last1, float2 g,
+                                              float2& T, float2& nS, float* grad_acc) {
+  const int lane = threadIdx.x & 31;
+  // splats two at a time, back to front (A = q, then B = q - 1), their
+  // records reduced together
+  for (int q = cnt - 1; q >= 0; q -= 2) {
+    const bool hasB = q >= 1;
+    float v[16];
+    bool any = unblend_splat<kGeneral>(rec[q], kk[q], u.fx, fy, last0, last1, g, T, nS, v);
+    if (hasB) {
+      any |= unblend_splat<kGeneral>(rec[q - 1], kk[q - 1], u.fx, fy, last0, last1, g, T, nS, v + 8);
+    } else {
+#pragma unroll
+      for (int i = 8; i < 16; ++i) v[i] = 0.f;
+    }
+    if (!__any_sync(0xffffffffu, any)) continue;
+    const float tot = -warp_reduce16(v);
+    // value i sits in lanes 2i, 2i+1: lanes 0/8 collect A's 0-3 / 4-7,
+    // lanes 16/24 collect B's
+    const float t1 = __shfl_down_sync(0xffffffffu, tot, 2);
+    const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
+    const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
+    if ((lane & 7) == 0 && (lane < 16 || hasB)) {
+      const uint32_t id = lane < 16 ? gid[q] : gid[q - 1];
+      red_add_v4(grad_acc + 8 * (long long)id + ((lane & 8) ? 4 : 0), tot, t1, t2, t3);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
-  __shared__ Rec s_rec[kWarps][32];
+  __shared__ BRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   __shared__ uint32_t s_gid[kWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Rec* rec = s_rec[warp];
+  BRec* rec = s_rec[warp];
   int* kk = s_k[warp];
   uint32_t* gid = s_gid[warp];
   int tile, quad;
@@ -573,65 +615,42 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
                       : next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
-    float T0 = 0.f, T1 = 0.f, g0 = 0.f, g1 = 0.f;
+    float2 T = make_float2(0.f, 0.f), g = make_float2(0.f, 0.f);
     int last0 = -1, last1 = -1;
     if (u.in0) {
-      T0 = a.t_final[o0];
+      T.x = a.t_final[o0];
       last0 = a.n_contrib[o0] - 1;
-      g0 = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
+      g.x = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
     }
     if (u.in1) {
-      T1 = a.t_final[o1];
+      T.y = a.t_final[o1];
       last1 = a.n_contrib[o1] - 1;
-      g1 = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
+      g.y = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
     }
-    if (g0 == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
-    if (g1 == 0.f) last1 = -1;
+    if (g.x == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
+    if (g.y == 0.f) last1 = -1;
     int wl = max(last0, last1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
     const long long hi = u.start + wl + 1;  // one past the last entry this warp needs
-    float S0 = 0.f, S1 = 0.f;
-    // batches of 32 walked back to front: [b1 - 32, b1)
-    Raw nxt = gather(hi - 32 + lane, u.start, hi, a.entry, a.mean2d, a.coef, a.inten);
+    const float2 fy = make_float2(u.fy0, u.fy1);
+    float2 nS = make_float2(0.f, 0.f);
+    // batches of 32 walked back to front: [b1 - 32, b1); two-stage prefetch
+    // (entry indices one batch ahead of the records)
+    Raw nxt = fetch(hi - 32 + lane >= u.start ? entry_at(a.entry, hi - 32 + lane, hi) : 0u,
+                    hi - 32 + lane >= u.start && hi - 32 + lane < hi, a.mean2d, a.coef, a.inten);
+    uint32_t g_nxt = hi - 64 + lane >= u.start ? entry_at(a.entry, hi - 64 + lane, hi) : 0u;
     for (long long b1 = hi; b1 > u.start; b1 -= 32) {
       const Raw cur = nxt;
-      const int cnt = compact(cur, (int)(b1 - 32 - u.start) + lane, u.x0, u.y0, u.xa, u.xb, u.ya, u.yb, rec,
-                              kk, gid);
-      nxt = gather(b1 - 64 + lane, u.start, hi, a.entry, a.mean2d, a.coef, a.inten);  // prefetch
-      // splats are processed two at a time, back to front (A = q, then
-      // B = q - 1), and their records reduced together
-      for (int q = cnt - 1; q >= 0; q -= 2) {
-        const bool hasB = q >= 1;
-        const Rec ra = rec[q];
-        const Rec rb = hasB ? rec[q - 1] : ra;
-        const int ka = kk[q], kb = hasB ? kk[q - 1] : ka;
-        float v[16];
-        bool any;
-        if (ra.b.y < kNoClampAlpha && rb.b.y < kNoClampAlpha) {  // warp-uniform
-          any = unblend_splat<false>(ra, ka, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v);
-          if (hasB)
-            any |= unblend_splat<false>(rb, kb, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v + 8);
-        } else {
-          any = unblend_splat<true>(ra, ka, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v);
-          if (hasB)
-            any |= unblend_splat<true>(rb, kb, u.fx, u.fy0, u.fy1, last0, last1, g0, g1, T0, T1, S0, S1, v + 8);
-        }
-        if (!hasB)
-#pragma unroll
-          for (int i = 8; i < 16; ++i) v[i] = 0.f;
-        if (!__any_sync(0xffffffffu, any)) continue;
-        const float tot = warp_reduce16(v);
-        // value i sits in lanes 2i, 2i+1: lanes 0/8 collect A's 0-3 / 4-7,
-        // lanes 16/24 collect B's
-        const float t1 = __shfl_down_sync(0xffffffffu, tot, 2);
-        const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
-        const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
-        if ((lane & 7) == 0 && (lane < 16 || hasB)) {
-          const uint32_t id = lane < 16 ? gid[q] : gid[q - 1];
-          red_add_v4(a.grad_acc + 8 * (long long)id + ((lane & 8) ? 4 : 0), tot, t1, t2, t3);
-        }
-      }
+      bool general;
+      const int cnt = compact_bwd(cur, (int)(b1 - 32 - u.start) + lane, u, rec, kk, gid, general);
+      const long long kn = b1 - 64 + lane;
+      nxt = fetch(g_nxt, kn >= u.start, a.mean2d, a.coef, a.inten);
+      g_nxt = kn - 32 >= u.start ? entry_at(a.entry, kn - 32, hi) : 0u;
+      if (general)
+        unblend_batch<true>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
+      else
+        unblend_batch<false>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
       __syncwarp();
     }
   }
@@ -766,8 +785,13 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
             target, l1_sum, (t_final && n_contrib) ? sp->unit_cost : nullptr, tiles_x(*cam), cam->width,
             cam->height};
-  // (an image-only variant without the contributor tracking measured
-  // slower on B200 - 0.71 vs 0.66 ms at C3 - so every launch tracks)
+#ifndef XG_FWD_ALWAYS_TRACK
+  if (!t_final || !n_contrib) {  // image only: no contributor tracking
+    k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads,
+                             0, (cudaStream_t)stream>>>(a);
+    return check_launch("k_composite_fwd");
+  }
+#endif
   k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0,
                           (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");

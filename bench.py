@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-sample-views", type=int, default=0, help="0 = one per worker")
     ap.add_argument("--no-train", action="store_true", help="skip the C2 training-iteration block")
     ap.add_argument("--train-iters-per-step", type=int, default=100)
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (1M Gaussians, 1024^2) stress block")
     return ap.parse_args()
 
 
@@ -383,6 +384,8 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "ms_per_view": ms / (VIEWS * args.steps),
     }
+    if not args.no_c4:
+        line["stress_c4"] = c4_block(args, timed, world, rank)
     if not args.no_train:
         line["train_c2" if world == 1 else "train_c5"] = train_block(args, timed, ClockSampler, local, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -394,6 +397,57 @@ def run_ours(args) -> None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+G_C4, DET_C4, VIEWS_C4 = 196, 1024, 8
+
+
+def c4_block(args, timed, world: int, rank: int) -> dict:
+    """C4 of BASELINE.json: 1,030,301 ACUI Gaussians at a 1024x1024 detector
+    (binning/sort and compositing stress).  One step = 8 views (45 degree
+    steps, offset per rank); per-stage times from CUDA events on single
+    views, throughput from the multi-stream sweep with images left in HBM."""
+    import torch
+
+    from paper_2403_04116_b200 import acui, geometry
+    from paper_2403_04116_b200.engine import Frame
+    from paper_2403_04116_b200.gaussians import GaussianCloud
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    cloud = GaussianCloud(**acui.init_alternative_arrays("cuboid", acui.benchmark_spec(G_C4), 16, 0), device="cuda")
+    sc = geometry.ScannerConfig(L_SO, L_SD, DET_C4, DET_C4, 192.0 / DET_C4)
+    angles = (np.arange(VIEWS_C4) + rank / max(world, 1)) * (np.pi / VIEWS_C4)
+    rend = SweepRenderer(cloud, sc, n_streams=args.streams)
+    out = torch.empty((VIEWS_C4, DET_C4, DET_C4), dtype=torch.float32, device="cuda")
+    fr = Frame(cloud.n_points, DET_C4, DET_C4, "cuda")
+    stages = np.zeros(3)
+    entries = []
+    for phi in angles:
+        cam = rend.camera(phi)
+        fr.preprocess(cloud, cam)
+        entries.append(fr.ensure_binned()[1])
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        fr.preprocess(cloud, cam)
+        ev[1].record()
+        fr.bin()
+        ev[2].record()
+        fr.composite(track=False)
+        ev[3].record()
+        torch.cuda.synchronize()
+        stages += [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+    stages /= VIEWS_C4
+    for _ in range(args.warmup):
+        rend.render(angles, out=out)
+    ms = timed(lambda: rend.render(angles, out=out, check=False), args.steps)
+    rend.render(angles, out=out)  # status check
+    return {"metric": "fps (1024x1024 cone-beam projections/s), 1M Gaussians",
+            "value": VIEWS_C4 * args.steps * world / (ms / 1e3), "unit": "fps",
+            "ms_per_view": ms / (VIEWS_C4 * args.steps),
+            "stages_ms_isolated": {"preprocess": stages[0], "bin_sort": stages[1], "composite": stages[2]},
+            "entries_per_view": float(np.mean(entries)),
+            "config": {"workload": f"C4: {cloud.n_points:,} ACUI Gaussians (G={G_C4}), {DET_C4}x{DET_C4} detector, "
+                                   f"{VIEWS_C4} views per GPU per step", "streams": args.streams}}
 
 
 def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:

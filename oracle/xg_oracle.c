@@ -387,16 +387,16 @@ void xgo_composite_fwd(int32_t h, int32_t w, const double* mean2d, const float* 
 
 /* Gradient pass (_kernels.pyx:121-177) in float64 on the float32 forward's
  * decisions.  Outputs are indexed by cloud row (n rows), accumulated. */
-void xgo_composite_bwd(int32_t h, int32_t w, const double* mean2d, const float* coef, const float* inten,
-                       const uint32_t* entry_splat, const int64_t* tile_ranges, const double* dl,
-                       double* g_mean, double* g_conic, double* g_int, double* g_alpha) {
+static void bwd_core(int32_t h, int32_t w, const double* mean2d, const float* coef, const float* inten,
+                     const uint32_t* entry_splat, const int64_t* tile_ranges, const double* dl, int t_first,
+                     int t_stride, double* g_mean, double* g_conic, double* g_int, double* g_alpha) {
   const int ntx = (w + TILE - 1) / TILE, nty = (h + TILE - 1) / TILE;
   const double ln2 = 0.69314718055994530942;
   int64_t cap = 64;
   int64_t* ks = (int64_t*)malloc(sizeof(int64_t) * cap);
   double* sig = (double*)malloc(sizeof(double) * cap);
   uint8_t* clamped = (uint8_t*)malloc(cap);
-  for (int t = 0; t < ntx * nty; ++t) {
+  for (int t = t_first; t < ntx * nty; t += t_stride) {
     const int x0 = TILE * (t % ntx), y0 = TILE * (t / ntx);
     const int64_t start = tile_ranges[2 * t], end = tile_ranges[2 * t + 1];
     for (int py = y0; py < y0 + TILE && py < h; ++py)
@@ -472,4 +472,67 @@ void xgo_composite_bwd(int32_t h, int32_t w, const double* mean2d, const float* 
   free(ks);
   free(sig);
   free(clamped);
+}
+
+void xgo_composite_bwd(int32_t h, int32_t w, const double* mean2d, const float* coef, const float* inten,
+                       const uint32_t* entry_splat, const int64_t* tile_ranges, const double* dl,
+                       double* g_mean, double* g_conic, double* g_int, double* g_alpha) {
+  bwd_core(h, w, mean2d, coef, inten, entry_splat, tile_ranges, dl, 0, 1, g_mean, g_conic, g_int, g_alpha);
+}
+
+typedef struct {
+  int32_t h, w;
+  const double* mean2d;
+  const float* coef;
+  const float* inten;
+  const uint32_t* entry_splat;
+  const int64_t* tile_ranges;
+  const double* dl;
+  int tid, nt;
+  double* buf; /* [n][7]: g_mean 2, g_conic 3, g_int, g_alpha */
+  int64_t n;
+} bwd_job;
+
+static void* bwd_worker(void* arg) {
+  bwd_job* j = (bwd_job*)arg;
+  double* b = j->buf;
+  bwd_core(j->h, j->w, j->mean2d, j->coef, j->inten, j->entry_splat, j->tile_ranges, j->dl, j->tid, j->nt, b,
+           b + 2 * j->n, b + 5 * j->n, b + 6 * j->n);
+  return NULL;
+}
+
+/* The same gradient pass over XGO_THREADS threads (default: online cores):
+ * static tile assignment, per-thread float64 accumulators summed in thread
+ * order afterwards - deterministic for a given thread count, and equal to the
+ * serial pass up to float64 summation order. */
+void xgo_composite_bwd_mt(int32_t h, int32_t w, int64_t n, const double* mean2d, const float* coef,
+                          const float* inten, const uint32_t* entry_splat, const int64_t* tile_ranges,
+                          const double* dl, double* g_mean, double* g_conic, double* g_int, double* g_alpha) {
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  const char* env = getenv("XGO_THREADS");
+  if (env && atoi(env) > 0) nt = atoi(env);
+  if (nt > 64) nt = 64;
+  const int n_tiles = ((w + TILE - 1) / TILE) * ((h + TILE - 1) / TILE);
+  if (nt > n_tiles) nt = n_tiles;
+  if (nt <= 1 || n <= 0) {
+    xgo_composite_bwd(h, w, mean2d, coef, inten, entry_splat, tile_ranges, dl, g_mean, g_conic, g_int, g_alpha);
+    return;
+  }
+  bwd_job jobs[64];
+  pthread_t th[64];
+  for (long i = 0; i < nt; ++i) {
+    bwd_job jb = {h, w, mean2d, coef, inten, entry_splat, tile_ranges, dl, (int)i, (int)nt,
+                  (double*)calloc((size_t)n * 7, sizeof(double)), n};
+    jobs[i] = jb;
+    pthread_create(&th[i], NULL, bwd_worker, &jobs[i]);
+  }
+  for (long i = 0; i < nt; ++i) pthread_join(th[i], NULL);
+  for (long i = 0; i < nt; ++i) {
+    const double* b = jobs[i].buf;
+    for (int64_t r = 0; r < 2 * n; ++r) g_mean[r] += b[r];
+    for (int64_t r = 0; r < 3 * n; ++r) g_conic[r] += b[2 * n + r];
+    for (int64_t r = 0; r < n; ++r) g_int[r] += b[5 * n + r];
+    for (int64_t r = 0; r < n; ++r) g_alpha[r] += b[6 * n + r];
+    free(jobs[i].buf);
+  }
 }

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kBinThreads)
 }
 
 struct BinWs {
-  unsigned long long* keyN1;
+  unsigned long long *keyN1, *keyN2;
   uint32_t *valN1, *offN, *keyE0, *keyE1, *valE1;
   uint32_t *hist, *hoff;  // multisplit path: [T][C] counts and their scan
   void* tail;
@@ -294,6 +294,7 @@ bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, int n_tiles, BinWs& w
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(cap > 0 ? cap : 1));
   const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles * (size_t)bin_chunks(n)) : 0;
   w.keyN1 = (unsigned long long*)p; p += 2 * bn;
+  w.keyN2 = (unsigned long long*)p; p += 2 * bn;
   w.valN1 = (uint32_t*)p; p += bn;
   w.offN = (uint32_t*)p; p += bn;
   w.keyE0 = (uint32_t*)p; p += be;
@@ -321,7 +322,7 @@ size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles
   const bool ms = multisplit(n_tiles_total);
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(entry_capacity > 0 ? entry_capacity : 1));
   const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)bin_chunks(n)) : 0;
-  return 4 * bn + 3 * be + 2 * bh + tail_bytes(n, entry_capacity, n_tiles_total) + 256;
+  return 6 * bn + 3 * be + 2 * bh + tail_bytes(n, entry_capacity, n_tiles_total) + 256;
 }
 
 xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size_t workspace_bytes,
@@ -346,11 +347,11 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   // 1. depth sort
   k_iota<<<div_up(n, 256), 256, 0, s>>>(sp->order, n, n_dev);
   if ((st = check_launch("k_iota")) != XG_OK) return st;
-  {
-    unsigned long long* keys[2] = {(unsigned long long*)sp->depth_key, w.keyN1};
-    uint32_t* vals[2] = {sp->order, w.valN1};
-    if ((st = onesweep_sort_pairs64(keys, vals, n, n_dev, w.tail, w.tail_bytes, s)) != XG_OK) return st;
-  }
+  // (depth_key is the sort's read-only input: a re-bin after an entry
+  // overflow sorts the same keys again)
+  if ((st = onesweep_sort_pairs64((const unsigned long long*)sp->depth_key, sp->order, w.keyN1, w.keyN2, w.valN1,
+                                  sp->order, sp->order, n, n_dev, w.tail, w.tail_bytes, s)) != XG_OK)
+    return st;
   if (multisplit(n_tiles)) {
     // 2-4. fused duplicate + stable tile sort + ranges
     const int C = (int)bin_chunks(n);

@@ -414,19 +414,20 @@ __global__ void __launch_bounds__(256) k_os_scan(const uint32_t* __restrict__ gh
     gofs[p * 256 + d] = s[d] - v;
     __syncthreads();
   }
+  // buffers: 0 / 1 ping-pong scratch, 2 the caller's input (never written)
   if (d == 0) {
-    int cur = 0;
+    int cur = 2;
     for (int p = 0; p < kOsPasses; ++p) {
       sel[p] = cur;
-      if (!trivial[p]) cur = 1 - cur;
+      if (!trivial[p]) cur = cur == 0 ? 1 : 0;
     }
     sel[kOsPasses] = cur;
   }
 }
 
 struct OsArgs {
-  unsigned long long* keys[2];
-  uint32_t* vals[2];
+  unsigned long long* keys[3];  // scratch A, scratch B, input (read-only)
+  uint32_t* vals[3];
   const uint32_t* n_dev;
   long long cap;
   int pass;
@@ -512,8 +513,8 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
     }
   }
   __syncthreads();
-  unsigned long long* kout = a.keys[1 - src];
-  uint32_t* vout = a.vals[1 - src];
+  unsigned long long* kout = a.keys[a.sel[p + 1]];
+  uint32_t* vout = a.vals[a.sel[p + 1]];
   const uint32_t* go = a.gofs + p * 256;
 #pragma unroll
   for (int r = 0; r < kOsRounds; ++r) {
@@ -527,13 +528,16 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
   }
 }
 
-__global__ void k_os_finish(uint32_t* vals0, const uint32_t* vals1, const uint32_t* n_dev, long long cap,
-                            const int* sel) {
-  if (sel[kOsPasses] == 0) return;
+// the result lands in vals[sel[K]]: copy it to vals_out unless it is there
+__global__ void k_os_finish(uint32_t* vals_out, const uint32_t* vals_a, const uint32_t* vals_b,
+                            const uint32_t* n_dev, long long cap, const int* sel) {
+  const int r = sel[kOsPasses];
+  const uint32_t* src = r == 0 ? vals_a : r == 1 ? vals_b : nullptr;
+  if (!src || src == vals_out) return;
   long long n = *n_dev;
   if (n > cap) n = cap;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    vals0[i] = vals1[i];
+    vals_out[i] = src[i];
 }
 
 }  // namespace
@@ -544,7 +548,9 @@ size_t onesweep_workspace_bytes(int64_t cap) {
          align_up(sizeof(uint32_t) * kOsPasses) + align_up(sizeof(uint32_t) * (size_t)kOsPasses * tiles * 256) + 256;
 }
 
-xg_status onesweep_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_t* vals_in,
+                                unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a,
+                                uint32_t* vals_b, uint32_t* vals_out, int64_t cap, const uint32_t* n_dev,
                                 void* ws, size_t ws_bytes, cudaStream_t s) {
   if (cap <= 0) return XG_OK;
   if (ws_bytes < onesweep_workspace_bytes(cap)) {
@@ -563,17 +569,19 @@ xg_status onesweep_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], 
   uint32_t* status = (uint32_t*)p;
   cudaMemsetAsync(ws, 0, onesweep_workspace_bytes(cap), s);
   const int hgrid = (int)(tiles < 296 ? tiles : 296);
-  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys[0], n_dev, cap, ghist);
+  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys_in, n_dev, cap, ghist);
   xg_status st = check_launch("k_os_hist");
   if (st != XG_OK) return st;
   k_os_scan<<<1, 256, 0, s>>>(ghist, gofs, n_dev, cap, sel);
   if ((st = check_launch("k_os_scan")) != XG_OK) return st;
   for (int pass = 0; pass < kOsPasses; ++pass) {
     OsArgs a;
-    a.keys[0] = keys[0];
-    a.keys[1] = keys[1];
-    a.vals[0] = vals[0];
-    a.vals[1] = vals[1];
+    a.keys[0] = keys_a;
+    a.keys[1] = keys_b;
+    a.keys[2] = const_cast<unsigned long long*>(keys_in);
+    a.vals[0] = vals_a;
+    a.vals[1] = vals_b;
+    a.vals[2] = const_cast<uint32_t*>(vals_in);
     a.n_dev = n_dev;
     a.cap = cap;
     a.pass = pass;
@@ -585,7 +593,7 @@ xg_status onesweep_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], 
     k_os_pass<<<(int)tiles, kOsThreads, 0, s>>>(a);
     if ((st = check_launch("k_os_pass")) != XG_OK) return st;
   }
-  k_os_finish<<<(int)(tiles < 296 ? tiles : 296), 256, 0, s>>>(vals[0], vals[1], n_dev, cap, sel);
+  k_os_finish<<<(int)(tiles < 296 ? tiles : 296), 256, 0, s>>>(vals_out, vals_a, vals_b, n_dev, cap, sel);
   return check_launch("k_os_finish");
 }
 

@@ -28,7 +28,12 @@ xg_status radix_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int
 // passes are skipped on the device).  Result always ends in vals[0]
 // (keys end wherever the last executed pass wrote them).
 size_t onesweep_workspace_bytes(int64_t cap);
-xg_status onesweep_sort_pairs64(unsigned long long* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+// Stable LSD sort of (64-bit key, u32 value) pairs; keys_in / vals_in are
+// never written (passes ping-pong between the a / b scratch buffers; vals_b
+// may alias vals_in), the sorted values land in vals_out.
+xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_t* vals_in,
+                                unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a,
+                                uint32_t* vals_b, uint32_t* vals_out, int64_t cap, const uint32_t* n_dev,
                                 void* ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace xg

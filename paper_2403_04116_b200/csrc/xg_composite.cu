@@ -467,11 +467,17 @@ __device__ __forceinline__ void unblend2(const BRec& r, float2 dy, float bdx, fl
   const float2 in = __ffma2_rn(nS, rc, __fmul2_rn(bc(r.b.z), Tb));  // i T - S / (1 - sigma)
   const float2 dsig = __fmul2_rn(g, in);
   nG = __fmul2_rn(dsig, ns);
-  if (!v0 || c0) nG.x = 0.f;
-  if (!v1 || c1) nG.y = 0.f;
   nS = __ffma2_rn(bc(r.b.z), nw, nS);
-  T.x = v0 ? Tb.x : T.x;
-  T.y = v1 ? Tb.y : T.y;
+  if (kGeneral) {
+    if (!v0 || c0) nG.x = 0.f;
+    if (!v1 || c1) nG.y = 0.f;
+    T.x = v0 ? Tb.x : T.x;
+    T.y = v1 ? Tb.y : T.y;
+  } else {
+    // an invalid pair has sigma = 0: 1 - sigma = 1, rcp.approx(1) = 1
+    // exactly, so Tb = T, w = 0 and G = dsig * 0 = 0 without selects
+    T = Tb;
+  }
 }
 
 // Both pixels of the lane for one splat; the lane's 7 partial sums (negated:

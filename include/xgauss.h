@@ -28,6 +28,8 @@
  *   xg_densify_mark     trainer.py:206-225 densify masks and counts
  *   xg_densify_apply    trainer.py:227-261 compaction, clone shift, split
  *   xg_intensities      gaussians.py:230-232 GaussianCloud.intensities
+ *   xg_ssim             metrics.py:57-124 ssim / ssim_and_gradient, fused into
+ *                       the trainer.py:109-123 loss gradient for gamma > 0
  */
 #ifndef XGAUSS_H
 #define XGAUSS_H
@@ -266,6 +268,20 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
                             const int64_t* tile_ranges, int64_t n_splats, const double* dl_dimage,
                             double* g_mean, double* g_conic, double* g_int, double* g_alpha,
                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* SSIM of pred vs ref (metrics.py:57-124): mean over every fully-interior
+ * 11x11 Gaussian window (sigma 1.5, K1 0.01, K2 0.03), float64 arithmetic;
+ * pred / ref float32 (is_f64 = 0) or float64 [h][w], h, w >= 11.
+ * ssim_out (device double, optional) receives the mean; grad_out (optional,
+ * float64 [h][w]) d(mean SSIM)/d pred (metrics.py:98-124); dl_out
+ * (optional, float32 [h][w]) the trainer's fused upstream gradient
+ *   dl = dl_ssim_scale * dSSIM/dpred + dl_l1_scale * sign(pred - ref)
+ * (trainer.py:117-123 with dl_ssim_scale = -gamma, dl_l1_scale =
+ * (1 - gamma) / (h w)).  workspace >= xg_ssim_workspace_bytes(h, w). */
+size_t xg_ssim_workspace_bytes(int32_t h, int32_t w);
+xg_status xg_ssim(const void* pred, const void* ref, int32_t is_f64, int32_t h, int32_t w, double data_range,
+                  double* ssim_out, double* grad_out, float* dl_out, double dl_ssim_scale, double dl_l1_scale,
+                  void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ OBJ = PKG / "csrc" / "_obj"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
 PER_FILE = {"xg_preprocess.cu": ["-fmad=false"]}
-SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu"]
+SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu"]
 
 
 def nvcc() -> str:

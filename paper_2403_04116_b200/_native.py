@@ -112,6 +112,9 @@ SIGNATURES = {
     ),
     "xg_intensities": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "xg_tiles_workspace_bytes": (c_size, [c_i64, c_i32, c_i32]),
+    "xg_ssim_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "xg_ssim": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_f64, c_void_p, c_void_p, c_void_p, c_f64,
+                        c_f64, c_void_p, c_size, c_void_p]),
     "xg_forward_tiles": (
         c_i32,
         [c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p,

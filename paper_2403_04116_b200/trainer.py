@@ -43,7 +43,7 @@ from .engine import Frame
 from .errors import InvalidParameterError, TrainingDivergenceError, XSplatError
 from .gaussians import PARAM_FIELDS, GaussianCloud, flat_size, flat_views, logit
 from .geometry import camera_pod, extrinsic_from_angle, intrinsic_from_config
-from .metrics import MetricReport, psnr, ssim, ssim_and_gradient
+from .metrics import MetricReport, SsimEngine, psnr, ssim, ssim_and_gradient
 from .rasterizer.backward import make_gradients
 from .rasterizer.frontend import RenderGradients, render
 
@@ -112,8 +112,8 @@ def position_learning_rate(cfg: TrainConfig, t: int) -> float:
 
 def _dev(x, device=None) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
-        return x.to(dtype=torch.float64, device=device or x.device)
-    return torch.as_tensor(np.asarray(x, dtype=np.float64), device=device)
+        return x.to(dtype=torch.float64, device=device or (x.device if x.is_cuda else "cuda"))
+    return torch.as_tensor(np.asarray(x, dtype=np.float64), device=device or "cuda")
 
 
 def loss(rendered, target, gamma: float):
@@ -315,6 +315,8 @@ class _IterationEngine:
         self.h, self.w = h, w
         self.resize(cloud)
         self.l1 = torch.zeros(1, dtype=torch.float64, device=cloud.device)
+        self.dl = torch.empty((h, w), dtype=torch.float32, device=cloud.device)  # fused loss gradient
+        self.ssim = None  # SsimEngine, created on the first gamma > 0 step
 
     def resize(self, cloud: GaussianCloud, capacity: int | None = None) -> None:
         n = cloud.n_points
@@ -403,9 +405,14 @@ class Trainer:
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
                         l1_scale=1.0 / (h * w), stats=self.stats)
         else:
-            value, dl = loss(fr.image, tgt, cfg.gamma)
+            # xg_ssim writes dl = -gamma dSSIM/dI + (1 - gamma) sign(I - T) / HW
+            # (trainer.py:117-123) straight into the backward's input
+            if eng.ssim is None:
+                eng.ssim = SsimEngine(h, w, self.dev)
+            s_dev = eng.ssim.run(fr.image, tgt, 1.0, dl=eng.dl, dl_ssim_scale=-cfg.gamma,
+                                 dl_l1_scale=(1.0 - cfg.gamma) / (h * w))
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis,
-                        dl_dimage=dl.float().contiguous(), stats=self.stats)
+                        dl_dimage=eng.dl, stats=self.stats)
         # carry this step's non-finite flags into the sticky word Adam reads
         fr.counters[nat.XG_CTR_STICKY : nat.XG_CTR_STICKY + 1].bitwise_or_(
             fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1] & self.grad_mask)
@@ -435,6 +442,8 @@ class Trainer:
         if log_now:
             if value is None:
                 value = float(eng.l1.item()) / (h * w)
+                if cfg.gamma != 0.0:
+                    value = (1.0 - cfg.gamma) * value + cfg.gamma * (1.0 - float(s_dev.item()))
             row = {"iteration": it, "loss": value, "train_psnr": psnr(fr.image, tgt), "test_psnr": None,
                    "test_ssim": None, "n_points": self.cloud.n_points}
             if it % cfg.eval_interval == 0 or it == cfg.iterations:

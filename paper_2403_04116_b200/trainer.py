@@ -43,7 +43,7 @@ from .engine import Frame
 from .errors import InvalidParameterError, TrainingDivergenceError, XSplatError
 from .gaussians import PARAM_FIELDS, GaussianCloud, flat_size, flat_views, logit
 from .geometry import camera_pod, extrinsic_from_angle, intrinsic_from_config
-from .metrics import MetricReport, SsimEngine, psnr, ssim, ssim_and_gradient
+from .metrics import MetricReport, SsimEngine, psnr, ssim, ssim_and_gradient, ssim_psnr_stack
 from .rasterizer.backward import make_gradients
 from .rasterizer.frontend import RenderGradients, render
 
@@ -289,11 +289,10 @@ def evaluate(cloud: GaussianCloud, dataset: ProjectionSet, indices, use_clean: b
     if indices.size == 0:
         return MetricReport(psnr=float("nan"), ssim=float("nan"), per_view=[])
     imgs = SweepRenderer(cloud, dataset.scanner, n_streams=2).render(dataset.angles[indices])
-    per = []
-    for k, i in enumerate(indices):
-        ref = torch.as_tensor(stack[i], device=cloud.device)
-        per.append({"view": int(i), "angle": float(dataset.angles[i]), "psnr": psnr(imgs[k], ref),
-                    "ssim": ssim(imgs[k], ref)})
+    refs = torch.as_tensor(np.asarray(stack)[indices], device=cloud.device)
+    s, p = ssim_psnr_stack(imgs, refs)  # one launch per view, one sync
+    per = [{"view": int(i), "angle": float(dataset.angles[i]), "psnr": float(p[k]), "ssim": float(s[k])}
+           for k, i in enumerate(indices)]
     return MetricReport(psnr=float(np.mean([v["psnr"] for v in per])),
                         ssim=float(np.mean([v["ssim"] for v in per])), per_view=per)
 

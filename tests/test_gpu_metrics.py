@@ -147,3 +147,17 @@ class TestReferencePorts:
         a = rng.uniform(0.2, 0.8, size=(16, 16))
         _, grad = m.ssim_and_gradient(a, a)
         assert np.allclose(grad.cpu().numpy(), 0.0, atol=1e-12)
+
+
+def test_stack_matches_per_view(m, rng):
+    """evaluate()'s batched path: one launch per view, one sync - same
+    numbers as per-view ssim() / psnr()."""
+    import torch
+
+    a = torch.as_tensor(rng.uniform(size=(5, 40, 52)), dtype=torch.float32, device="cuda")
+    b = torch.clamp(a + 0.05 * torch.randn_like(a), 0, 1)
+    b[2] = a[2]
+    s, p = m.ssim_psnr_stack(a, b)
+    for v in range(5):
+        assert s[v] == m.ssim(a[v], b[v])
+        assert p[v] == m.psnr(a[v], b[v]) or (np.isinf(p[v]) and np.isinf(m.psnr(a[v], b[v])))

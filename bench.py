@@ -66,23 +66,23 @@ def sweep_angles(rank: int, world: int) -> np.ndarray:
 G_C2 = 88
 
 
-def phantom_truth(g: int):
-    """Synthetic 'phantom' for the training benchmark: the ACUI lattice with
-    intensities / opacities of two nested ellipsoids plus an off-centre
-    cuboid insert (the reference's default phantom primitives,
-    phantom.py:163-178, restated as per-Gaussian attributes)."""
-    from paper_2403_04116_b200 import acui
+def phantom_dataset(g: int, scanner):
+    """Training targets exactly as the reference's pipeline makes them
+    (cli.py:60-72): the default phantom primitives voxelised on
+    the G^3 grid of the 100 mm ACUI cuboid, cone-beam projected at every
+    angle (GPU projector, phantom.py:190-250), normalised by the global max
+    and given 3 % Gaussian noise (seed 0).  Returns (dataset, seconds)."""
+    import torch
 
-    a = acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 1)
-    p = a["positions"]
-    r_out = ((p[:, 0] / 45) ** 2 + (p[:, 1] / 38) ** 2 + (p[:, 2] / 42) ** 2) <= 1
-    r_in = ((p[:, 0] / 25) ** 2 + ((p[:, 1] - 5) / 20) ** 2 + (p[:, 2] / 22) ** 2) <= 1
-    box = (np.abs(p[:, 0] + 15) < 8) & (np.abs(p[:, 1] - 15) < 6) & (np.abs(p[:, 2]) < 10)
-    dens = np.clip(0.02 + 0.45 * r_out + 0.35 * r_in + 0.5 * box, 0.02, 0.95)
-    a["features"] = np.repeat(np.log(dens / (1 - dens))[:, None] / 16.0, 16, axis=1)
-    alpha = np.where(r_out | box, 0.25, 0.01)
-    a["raw_opacities"] = np.log(alpha / (1 - alpha))
-    return a
+    from paper_2403_04116_b200.dataset import add_noise, make_projection_set
+    from paper_2403_04116_b200.phantom import default_phantom_primitives, make_phantom
+
+    extent = np.full(3, 100.0)
+    t0 = time.perf_counter()
+    ph = make_phantom(default_phantom_primitives(extent), (g, g, g), extent / g)
+    ds = add_noise(make_projection_set(ph, scanner), 0.03, 0)
+    torch.cuda.synchronize()
+    return ds, time.perf_counter() - t0
 
 
 def c3_arrays():
@@ -459,19 +459,25 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
     import torch
 
     from paper_2403_04116_b200 import _native, acui, geometry
-    from paper_2403_04116_b200.dataset import self_render
     from paper_2403_04116_b200.gaussians import GaussianCloud
     from paper_2403_04116_b200.parallel import DataParallelTrainer
     from paper_2403_04116_b200.trainer import TrainConfig, Trainer
 
     g = G_C2 if world == 1 else G_C3
     sc = geometry.ScannerConfig(L_SO, L_SD, DET, DET, 192.0 / DET, geometry.equal_interval_angles(100))
-    truth = GaussianCloud(**phantom_truth(g), device="cuda")
-    ds = self_render(truth, sc)
+    ds, prep_s = phantom_dataset(g, sc)
     init = acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 0)
     cfg = TrainConfig(iterations=20_000, log_interval=10**9, eval_interval=10**9)
     per = args.train_iters_per_step
     out = {}
+    # prime the process once (caching-allocator segments for the density-
+    # control resizes, lazily loaded kernels): without it whichever mode runs
+    # first measured ~15 % slow
+    prime = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg)
+    for _ in range(7 * per):
+        prime.step()
+    del prime
+    torch.cuda.synchronize()
     for mode in ("device", "e2e"):
         if world == 1:
             tr = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg, targets_on_host=(mode == "e2e"))
@@ -504,7 +510,9 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
             "config": {"workload": name,
                        "iters_per_step": per, "warmup_iters": max(args.warmup, 5) * per,
                        "n_points_timed": [d["n0"], d["n1"]], "densify_events": d["densify_events"],
-                       "targets": "rendered by the engine from a synthetic ellipsoid/cuboid phantom cloud"},
+                       "targets": f"default voxel phantom ({g}^3, 100 mm) cone-beam projected on the GPU "
+                                  f"(xg_project_volume), normalised, 3 % noise - {prep_s:.2f} s for "
+                                  f"{len(sc.angles)} views"},
             "e2e": {"value": iters / (e["ms"] / 1e3), "unit": "iters/s", "h2d_bytes_per_step": 4 * DET * DET * per,
                     "d2h_bytes_per_step": 8 * per,
                     "note": "targets in pinned host memory, copied H2D every iteration; L1 loss copied D2H"},

@@ -28,6 +28,8 @@
  *   xg_densify_mark     trainer.py:206-225 densify masks and counts
  *   xg_densify_apply    trainer.py:227-261 compaction, clone shift, split
  *   xg_intensities      gaussians.py:230-232 GaussianCloud.intensities
+ *   xg_project_volume   phantom.py:181-250 project_phantom (cone-beam ray march
+ *                       of a voxel phantom: the training-target generator)
  *   xg_ssim             metrics.py:57-124 ssim / ssim_and_gradient, fused into
  *                       the trainer.py:109-123 loss gradient for gamma > 0
  */
@@ -267,6 +269,33 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
                             const int32_t* entry_splat, int64_t n_entries,
                             const int64_t* tile_ranges, int64_t n_splats, const double* dl_dimage,
                             double* g_mean, double* g_conic, double* g_int, double* g_alpha,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* A voxel phantom (phantom.py:117-140): float64 densities [m0][m1][m2]
+ * (C order; axes = world x, y, z), centred on the world origin. */
+typedef struct xg_volume {
+  const double* densities;
+  int32_t m[3];
+  int32_t _pad;
+  double voxel_size[3];  /* mm per voxel, per axis */
+} xg_volume;
+
+/* One cone-beam view for the projector (phantom.py:193-213): source
+ * position, world->camera rotation R (row-major; ray directions are
+ * d_cam @ R, d_cam = ((x - W/2) / f, (y - H/2) / f, 1)), focal length in
+ * pixels, detector size.  Host-computed (math.sin / math.cos). */
+typedef struct xg_cone_view {
+  double source[3];
+  double rot[9];
+  double focal;
+  int32_t width, height;
+} xg_cone_view;
+
+/* Raw line integrals of one view (project_phantom, phantom.py:181-236):
+ * out float64 [H][W].  step_factor in (0, 0.5].  workspace >=
+ * xg_project_workspace_bytes(H, W). */
+size_t xg_project_workspace_bytes(int32_t h, int32_t w);
+xg_status xg_project_volume(const xg_volume* vol, const xg_cone_view* view, double step_factor, double* out,
                             void* workspace, size_t workspace_bytes, void* stream);
 
 /* SSIM of pred vs ref (metrics.py:57-124): mean over every fully-interior

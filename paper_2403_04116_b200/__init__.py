@@ -4,10 +4,13 @@ A drop-in for the reference engine's hot path (``xsplat``): the same Python
 API - ``GaussianCloud``, ``render`` / ``render_view`` / ``project_splats`` /
 ``render_backward``, ``adam_step`` / ``densify_and_prune`` / ``train`` - on
 hand-written sm_100a CUDA kernels behind the C ABI of ``include/xgauss.h``
-(libxgauss.so).  There is no CPU fallback.
+(libxgauss.so) - plus the path's callers on either side: the SSIM loss
+(``metrics``), the cone-beam phantom projector that makes training targets
+(``phantom``, ``dataset``).  There is no CPU fallback.
 """
 
 from .acui import CuboidSpec, init_alternative, init_cloud, sample_cuboid
+from .dataset import ProjectionSet, add_noise, load_dataset, make_projection_set, save_dataset
 from .errors import (
     ConfigError,
     DatasetError,
@@ -40,6 +43,17 @@ from .geometry import (
     projection_jacobian,
     viewing_rotation,
     world_to_camera,
+)
+from .metrics import MetricReport, psnr, ssim, ssim_and_gradient
+from .phantom import (
+    Cuboid,
+    Ellipsoid,
+    VoxelPhantom,
+    default_phantom_primitives,
+    make_phantom,
+    primitive_from_dict,
+    project_all,
+    project_phantom,
 )
 from .rasterizer import (
     Projection,

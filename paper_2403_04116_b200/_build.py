@@ -2,9 +2,11 @@
 
 The shared library is the product's only native artefact; it is built in
 the package directory so it travels with the repository snapshot to the GPU
-box.  ``xg_preprocess.cu`` is compiled with ``-fmad=false``: the per-Gaussian
-float64 projection must round every product/sum as written so radii, tile
-rects and depth keys reproduce the oracle bit for bit.
+box.  ``xg_preprocess.cu`` and ``xg_project.cu`` are compiled with
+``-fmad=false``: the per-Gaussian float64 projection (and the phantom
+projector's ray samples) must round every product/sum as written so radii,
+tile rects, depth keys and sample positions reproduce the oracle /
+reference bit for bit.
 """
 
 from __future__ import annotations
@@ -23,8 +25,8 @@ OBJ = PKG / "csrc" / "_obj"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
-PER_FILE = {"xg_preprocess.cu": ["-fmad=false"]}
-SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu"]
+PER_FILE = {"xg_preprocess.cu": ["-fmad=false"], "xg_project.cu": ["-fmad=false"]}
+SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu", "xg_project.cu"]
 
 
 def nvcc() -> str:

@@ -47,6 +47,14 @@ class XgCloud(ctypes.Structure):
     _fields_ = [("params", c_void_p), ("basis", c_void_p), ("n", c_i64), ("n_features", c_i32), ("_pad", c_i32)]
 
 
+class XgVolume(ctypes.Structure):
+    _fields_ = [("densities", c_void_p), ("m", c_i32 * 3), ("_pad", c_i32), ("voxel_size", c_f64 * 3)]
+
+
+class XgConeView(ctypes.Structure):
+    _fields_ = [("source", c_f64 * 3), ("rot", c_f64 * 9), ("focal", c_f64), ("width", c_i32), ("height", c_i32)]
+
+
 class XgSplats(ctypes.Structure):
     _fields_ = [
         ("mean2d", c_void_p),
@@ -113,6 +121,8 @@ SIGNATURES = {
     "xg_intensities": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "xg_tiles_workspace_bytes": (c_size, [c_i64, c_i32, c_i32]),
     "xg_ssim_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "xg_project_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "xg_project_volume": (c_i32, [c_void_p, c_void_p, c_f64, c_void_p, c_void_p, c_size, c_void_p]),
     "xg_ssim": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_f64, c_void_p, c_void_p, c_void_p, c_f64,
                         c_f64, c_void_p, c_size, c_void_p]),
     "xg_forward_tiles": (

@@ -8,14 +8,13 @@ import torch
 sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_2403_04116_b200 import acui, geometry  # noqa: E402
-from paper_2403_04116_b200.dataset import self_render  # noqa: E402
 from paper_2403_04116_b200.gaussians import GaussianCloud  # noqa: E402
 from paper_2403_04116_b200.trainer import TrainConfig, Trainer  # noqa: E402
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 g = int(sys.argv[2]) if len(sys.argv) > 2 else 88
 sc = geometry.ScannerConfig(1000.0, 1500.0, 512, 512, 192.0 / 512, geometry.equal_interval_angles(100))
-ds = self_render(GaussianCloud(**bench.phantom_truth(g), device="cuda"), sc)
+ds, _ = bench.phantom_dataset(g, sc)
 tr = Trainer(ds, GaussianCloud(**acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 0),
                                device="cuda"), TrainConfig(iterations=20000, log_interval=10**9,
                                                            eval_interval=10**9))

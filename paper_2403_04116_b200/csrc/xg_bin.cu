@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
 
 // ---------------------------------------------------------------------------
 // Fused duplicate + stable tile sort ("multisplit" counting sort).  The
-// depth-sorted Gaussians are cut into chunks of kBinChunk (one CTA each);
+// depth-sorted Gaussians are cut into chunks of 256 x rounds (one CTA each);
 // every Gaussian contributes one entry per tile of its rect.  Pass 1 counts
 // entries per (tile, chunk); an exclusive scan over the tile-major table
 // gives each (tile, chunk) its output base - and the tile ranges for free.
@@ -147,18 +147,27 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
 // ---------------------------------------------------------------------------
 constexpr int kBinThreads = 256;
 constexpr int kBinWarps = kBinThreads / 32;
-constexpr int kBinRounds = 4;                                  // 32-Gaussian rounds per warp
-constexpr int kBinChunk = kBinThreads * kBinRounds;            // Gaussians per CTA
+constexpr int kBinMaxRounds = 4;                               // 32-Gaussian rounds per warp (max)
+
+// Rounds per warp (chunk = 256 x rounds Gaussians per CTA): as many as keep
+// >= ~3 CTAs per SM, so small clouds (training at 100k) still fill the GPU.
+inline int bin_rounds(int64_t n) {
+  const int64_t r = n / ((int64_t)kBinThreads * 444);
+  return r < 1 ? 1 : (r > kBinMaxRounds ? kBinMaxRounds : (int)r);
+}
+inline int64_t bin_chunk(int64_t n) { return (int64_t)kBinThreads * bin_rounds(n); }
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
 
 __global__ void __launch_bounds__(kBinThreads)
     k_bin_count(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
-                const ushort4* __restrict__ rect, long long n, int ntx, int T, uint32_t* __restrict__ hist) {
+                const ushort4* __restrict__ rect, long long n, int ntx, int T, int rounds,
+                uint32_t* __restrict__ hist) {
   extern __shared__ uint32_t cnt[];  // [T]
   for (int t = threadIdx.x; t < T; t += kBinThreads) cnt[t] = 0;
   __syncthreads();
-  const long long lo = (long long)blockIdx.x * kBinChunk;
-  const long long hi = lo + kBinChunk < n ? lo + kBinChunk : n;
+  const long long chunk = (long long)kBinThreads * rounds;
+  const long long lo = (long long)blockIdx.x * chunk;
+  const long long hi = lo + chunk < n ? lo + chunk : n;
   for (long long s = lo + threadIdx.x; s < hi; s += kBinThreads) {
     const uint32_t g = order[s];
     if (n_tiles[g] == 0) continue;
@@ -186,7 +195,7 @@ __global__ void k_bin_ranges(const uint32_t* __restrict__ offs, int C, int T, co
 
 __global__ void __launch_bounds__(kBinThreads)
     k_bin_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
-               const ushort4* __restrict__ rect, long long n, int ntx, int T,
+               const ushort4* __restrict__ rect, long long n, int ntx, int T, int rounds,
                const uint32_t* __restrict__ offs, long long cap, uint32_t* __restrict__ entry_splat) {
   extern __shared__ uint32_t wcnt[];  // [kBinWarps][T]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,9 +203,9 @@ __global__ void __launch_bounds__(kBinThreads)
   for (int i = threadIdx.x; i < kBinWarps * T; i += kBinThreads) wcnt[i] = 0;
   __syncthreads();
   uint32_t* mine = wcnt + warp * T;
-  const long long wlo = (long long)blockIdx.x * kBinChunk + (long long)warp * 32 * kBinRounds;
+  const long long wlo = (long long)blockIdx.x * kBinThreads * rounds + (long long)warp * 32 * rounds;
   // phase 1: per-warp entry counts per tile
-  for (int rd = 0; rd < kBinRounds; ++rd) {
+  for (int rd = 0; rd < rounds; ++rd) {
     const long long s = wlo + rd * 32 + lane;
     if (s < n) {
       const uint32_t g = order[s];
@@ -220,7 +229,7 @@ __global__ void __launch_bounds__(kBinThreads)
   __syncthreads();
   // phase 3: enumerate entries in (depth, rect row-major) order, rank per tile
   const unsigned lt = lanemask_lt();
-  for (int rd = 0; rd < kBinRounds; ++rd) {
+  for (int rd = 0; rd < rounds; ++rd) {
     const long long s = wlo + rd * 32 + lane;
     uint32_t g = 0, cnt = 0;
     ushort4 r = make_ushort4(0, 0, 0, 0);
@@ -277,7 +286,7 @@ struct BinWs {
 
 bool multisplit(int n_tiles) { return n_tiles <= kBinMaxTiles; }
 
-int64_t bin_chunks(int64_t n) { return (n + kBinChunk - 1) / kBinChunk; }
+int64_t bin_chunks(int64_t n) { return (n + bin_chunk(n) - 1) / bin_chunk(n); }
 
 size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   size_t a = radix_workspace_bytes(multisplit(n_tiles) ? n : (n > cap ? n : cap));
@@ -364,7 +373,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
       attr_set = true;
     }
     k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                                 w.hist);
+                                                 bin_rounds(n), w.hist);
     if ((st = check_launch("k_bin_count")) != XG_OK) return st;
     const long long hn = (long long)n_tiles * C;
     if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
@@ -374,7 +383,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                                                       (long long*)sp->tile_ranges);
     if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
     k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                               w.hoff, cap, sp->entry_splat);
+                                               bin_rounds(n), w.hoff, cap, sp->entry_splat);
     if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
     k_flag_overflow<<<1, 32, 0, s>>>(sp->counters, cap);
     if ((st = check_launch("k_flag_overflow")) != XG_OK) return st;

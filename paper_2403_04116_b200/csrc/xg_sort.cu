@@ -359,7 +359,10 @@ namespace {
 
 constexpr int kOsThreads = 256;
 constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsRounds = 8;
+#ifndef XG_OS_ROUNDS
+#define XG_OS_ROUNDS 8
+#endif
+constexpr int kOsRounds = XG_OS_ROUNDS;
 constexpr int kOsTile = kOsThreads * kOsRounds;  // 2048 items
 constexpr int kOsPasses = 8;
 constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsMask = (1u << 30) - 1u;

@@ -283,8 +283,10 @@ __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int 
   for (int q = 0; q < cnt; ++q) blend2<kGeneral, kTrack>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last0, last1);
 }
 
+// 5 CTAs (20 warps) per SM: ptxas fits the image-only variant in 96
+// registers; measured 5 % faster than the unbounded 97-register build
 #ifndef XG_FWD_MIN_CTAS
-#define XG_FWD_MIN_CTAS 1
+#define XG_FWD_MIN_CTAS 5
 #endif
 
 template <bool kTrack>
@@ -607,7 +609,13 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
   }
 }
 
+// (no min-blocks bound: ptxas then settles at 92 registers = 5 CTAs per SM,
+// measured fastest; forcing 6+ CTAs spills or slows the replay)
+#ifdef XG_BWD_MIN_CTAS
+__global__ void __launch_bounds__(kThreads, XG_BWD_MIN_CTAS) k_composite_bwd(BwdArgs a) {
+#else
 __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
+#endif
   __shared__ BRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   __shared__ uint32_t s_gid[kWarps][32];

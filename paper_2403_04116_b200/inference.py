@@ -15,6 +15,8 @@ ranks with no collective (see ``parallel.py``).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -28,13 +30,19 @@ class SweepRenderer:
     """Reusable multi-stream renderer for one cloud and one detector."""
 
     def __init__(self, cloud: GaussianCloud, scanner: ScannerConfig, n_streams: int = 3,
-                 capacity_factor: float = 1.3):
+                 capacity_factor: float = 1.3, priority_composite: bool | None = None):
         nat.require_cuda(cloud.flat, "cloud")
         self.cloud = cloud
         self.scanner = scanner
         self.h, self.w = scanner.detector_height, scanner.detector_width
         self.intr = intrinsic_from_config(scanner)
         self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, n_streams))]
+        if priority_composite is None:
+            priority_composite = os.environ.get("XG_PRIORITY_COMPOSITE", "0") == "1"
+        # optional: compositing on high-priority streams, so the binning of the
+        # next views only fills the SMs the persistent composite leaves idle
+        self.comp_streams = ([torch.cuda.Stream(device=cloud.device, priority=-1) for _ in self.streams]
+                             if priority_composite else None)
         self.capacity_factor = capacity_factor
         self.frames: list[Frame] = []
         self.capacity = 0
@@ -74,12 +82,21 @@ class SweepRenderer:
         for s in self.streams:
             s.wait_stream(main)
         launches = 0
+        if self.comp_streams is not None:
+            for s in self.comp_streams:
+                s.wait_stream(main)
         for i, phi in enumerate(angles):
             k = i % len(self.streams)
             st, fr = self.streams[k], self.frames[k]
             with torch.cuda.stream(st):
+                if self.comp_streams is not None:
+                    st.wait_stream(self.comp_streams[k])  # the frame's previous composite is done
                 fr.preprocess(self.cloud, self.camera(phi))
                 fr.bin()
+            if self.comp_streams is not None:
+                self.comp_streams[k].wait_stream(st)
+                st = self.comp_streams[k]
+            with torch.cuda.stream(st):
                 if composite_events is not None:
                     a = torch.cuda.Event(enable_timing=True)
                     b = torch.cuda.Event(enable_timing=True)
@@ -93,7 +110,7 @@ class SweepRenderer:
                 if host_out is not None:
                     host_out[i].copy_(out[i], non_blocking=True)
             launches += 1
-        for s in self.streams:
+        for s in self.streams + (self.comp_streams or []):
             main.wait_stream(s)
         self.kernel_launches = launches
         if check:

@@ -271,9 +271,18 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    # XG_BENCH_SHARE_GPU=1 (test aid): ranks share the visible GPUs round-robin
+    # and talk over gloo - exercises the multi-rank code path on one GPU;
+    # its numbers are not a measurement.
+    share = os.environ.get("XG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2403_04116_b200 import _native, geometry
     from paper_2403_04116_b200.gaussians import GaussianCloud
     from paper_2403_04116_b200.inference import SweepRenderer

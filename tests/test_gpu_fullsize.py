@@ -174,3 +174,23 @@ def test_ragged_detectors(xg, w, h, phi):
         assert float(proj.pixels.abs().max()) == 0.0
         return
     _check_forward(f"{w}x{h}", proj, sp, pre, binned, fwd)
+
+
+def test_intensities_view_independent_across_full_scan(xg, rng):
+    """test_acceptance.py:108-129: the per-view intensities of a 100-angle
+    scan are bit-identical to each other and to the cloud's own
+    intensities (X-Gaussian's isotropic RIRF, no view dependence)."""
+    from conftest import random_arrays
+
+    sc = xg.ScannerConfig(1000.0, 1500.0, 64, 64, 3.0, xg.equal_interval_angles(100))
+    cloud = xg.GaussianCloud(**random_arrays(32, rng, pos_scale=30.0, scale_range=(4.0, 10.0)), device="cuda")
+    expected = cloud.intensities().cpu().numpy()
+    host = xg.rirf(cloud.to_numpy()["features"], cloud.to_numpy()["basis_weights"])
+    assert np.allclose(expected, host, rtol=1e-6)
+    checked = 0
+    for phi in sc.angles:
+        _, sp = xg.render_view(cloud, sc, float(phi))
+        act = sp.active_indices.cpu().numpy()
+        assert np.array_equal(sp.intensities.cpu().numpy(), expected[act]), phi
+        checked += act.size
+    assert checked > 0

@@ -147,15 +147,23 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
 // ---------------------------------------------------------------------------
 constexpr int kBinThreads = 256;
 constexpr int kBinWarps = kBinThreads / 32;
-constexpr int kBinMaxRounds = 4;                               // 32-Gaussian rounds per warp (max)
+#ifndef XG_BIN_MAX_ROUNDS
+#define XG_BIN_MAX_ROUNDS 16
+#endif
+constexpr int kBinMaxRounds = XG_BIN_MAX_ROUNDS;              // 32-Gaussian rounds per warp (max)
 
-// Rounds per warp (chunk = 256 x rounds Gaussians per CTA): as many as keep
-// >= ~3 CTAs per SM, so small clouds (training at 100k) still fill the GPU.
-inline int bin_rounds(int64_t n) {
-  const int64_t r = n / ((int64_t)kBinThreads * 444);
-  return r < 1 ? 1 : (r > kBinMaxRounds ? kBinMaxRounds : (int)r);
+// Rounds per warp (chunk = 256 x rounds Gaussians per CTA).  Every CTA pays
+// O(T) fixed work (zeroing and scanning its 8 x T per-warp counters, reading
+// T offsets), so the chunk grows with the tile count: ~3 CTAs per SM for
+// T <= 1024 (small training clouds still fill the GPU), ~2 waves of one
+// CTA per SM (128 KB of counters) at T = 4096.
+inline int bin_rounds(int64_t n, int n_tiles) {
+  const int64_t ctas = n_tiles > 1024 ? 296 : 444;
+  const int64_t r = (n + (int64_t)kBinThreads * ctas - 1) / ((int64_t)kBinThreads * ctas);
+  const int cap = n_tiles > 1024 ? kBinMaxRounds : 4;
+  return r < 1 ? 1 : (r > cap ? cap : (int)r);
 }
-inline int64_t bin_chunk(int64_t n) { return (int64_t)kBinThreads * bin_rounds(n); }
+inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
 
 __global__ void __launch_bounds__(kBinThreads)
@@ -286,13 +294,13 @@ struct BinWs {
 
 bool multisplit(int n_tiles) { return n_tiles <= kBinMaxTiles; }
 
-int64_t bin_chunks(int64_t n) { return (n + bin_chunk(n) - 1) / bin_chunk(n); }
+int64_t bin_chunks(int64_t n, int n_tiles) { return (n + bin_chunk(n, n_tiles) - 1) / bin_chunk(n, n_tiles); }
 
 size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   size_t a = radix_workspace_bytes(multisplit(n_tiles) ? n : (n > cap ? n : cap));
   const size_t o = onesweep_workspace_bytes(n);
   if (o > a) a = o;
-  size_t b = scan_workspace_bytes(multisplit(n_tiles) ? (n > n_tiles * bin_chunks(n) ? n : n_tiles * bin_chunks(n)) : n);
+  size_t b = scan_workspace_bytes(multisplit(n_tiles) ? (n > n_tiles * bin_chunks(n, n_tiles) ? n : n_tiles * bin_chunks(n, n_tiles)) : n);
   return a > b ? a : b;
 }
 
@@ -301,7 +309,7 @@ bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, int n_tiles, BinWs& w
   const size_t bn = align_up(sizeof(uint32_t) * (size_t)n);
   const bool ms = multisplit(n_tiles);
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(cap > 0 ? cap : 1));
-  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles * (size_t)bin_chunks(n)) : 0;
+  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles * (size_t)bin_chunks(n, n_tiles)) : 0;
   w.keyN1 = (unsigned long long*)p; p += 2 * bn;
   w.keyN2 = (unsigned long long*)p; p += 2 * bn;
   w.valN1 = (uint32_t*)p; p += bn;
@@ -330,7 +338,7 @@ size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles
   const size_t bn = align_up(sizeof(uint32_t) * (size_t)n);
   const bool ms = multisplit(n_tiles_total);
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(entry_capacity > 0 ? entry_capacity : 1));
-  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)bin_chunks(n)) : 0;
+  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)bin_chunks(n, n_tiles_total)) : 0;
   return 6 * bn + 3 * be + 2 * bh + tail_bytes(n, entry_capacity, n_tiles_total) + 256;
 }
 
@@ -363,7 +371,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     return st;
   if (multisplit(n_tiles)) {
     // 2-4. fused duplicate + stable tile sort + ranges
-    const int C = (int)bin_chunks(n);
+    const int C = (int)bin_chunks(n, n_tiles);
     const size_t sm_count = sizeof(uint32_t) * (size_t)n_tiles;
     const size_t sm_emit = sizeof(uint32_t) * (size_t)kBinWarps * n_tiles;
     static bool attr_set = false;
@@ -373,7 +381,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
       attr_set = true;
     }
     k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                                 bin_rounds(n), w.hist);
+                                                 bin_rounds(n, n_tiles), w.hist);
     if ((st = check_launch("k_bin_count")) != XG_OK) return st;
     const long long hn = (long long)n_tiles * C;
     if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
@@ -383,7 +391,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                                                       (long long*)sp->tile_ranges);
     if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
     k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                               bin_rounds(n), w.hoff, cap, sp->entry_splat);
+                                               bin_rounds(n, n_tiles), w.hoff, cap, sp->entry_splat);
     if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
     k_flag_overflow<<<1, 32, 0, s>>>(sp->counters, cap);
     if ((st = check_launch("k_flag_overflow")) != XG_OK) return st;

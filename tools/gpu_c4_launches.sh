@@ -1,0 +1,2 @@
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_c4.csv python tools/prof_c3.py 1 196 1024 > /dev/null 2>&1; echo "rc=$?"

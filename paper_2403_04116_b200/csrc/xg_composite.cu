@@ -198,6 +198,18 @@ __device__ __forceinline__ bool well_conditioned(float A, float B, float C) {
 
 __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
 
+// (p2 >= cut && T >= floor) ? sg : 0 as FSETP, FSETP.AND, FSEL
+__device__ __forceinline__ float select_ok(float sg, float p2, float T) {
+  float r;
+  asm("{\n\t.reg .pred q, o;\n\t"
+      "setp.ge.f32 q, %3, %5;\n\t"
+      "setp.ge.and.f32 o, %2, %4, q;\n\t"
+      "selp.f32 %0, %1, 0f00000000, o;\n\t}"
+      : "=f"(r)
+      : "f"(sg), "f"(p2), "f"(T), "f"(kCut2), "f"(kFloor));
+  return r;
+}
+
 // One splat, the lane's two pixels: the blend step of _kernels.pyx:57-72.
 // kGeneral keeps the sigma <= 0.99 clamp (only alpha >= 0.99 can reach it)
 // and the p2 <= 0 test (only ill-conditioned splats can need it); both are
@@ -221,8 +233,15 @@ __device__ __forceinline__ void blend2(const FRec& r, int krel, float fx, float2
     ok0 &= p.x <= 0.f;
     ok1 &= p.y <= 0.f;
   }
-  sg.x = ok0 ? sg.x : 0.f;
-  sg.y = ok1 ? sg.y : 0.f;
+  if (kGeneral || kTrack) {
+    sg.x = ok0 ? sg.x : 0.f;
+    sg.y = ok1 ? sg.y : 0.f;
+  } else {
+    // one chained compare + one select per pixel (left to itself the
+    // compiler splits the conjunction into two compare/select pairs)
+    sg.x = select_ok(sg.x, p.x, T.x);
+    sg.y = select_ok(sg.y, p.y, T.y);
+  }
   const float2 w = __fmul2_rn(sg, T);
   acc = __ffma2_rn(bc(r.b.z), w, acc);
   T = __ffma2_rn(sg, T, T);

@@ -194,3 +194,64 @@ def test_intensities_view_independent_across_full_scan(xg, rng):
         assert np.array_equal(sp.intensities.cpu().numpy(), expected[act]), phi
         checked += act.size
     assert checked > 0
+
+
+def _random_fields(rng, n, opacity, scale_lo, scale_hi, aniso):
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ls = np.log(rng.uniform(scale_lo, scale_hi, size=(n, 3)))
+    ls[:, 0] += np.log(aniso)  # one axis stretched: ill-conditioned 2D conics
+    return {k: np.asarray(v, np.float32) for k, v in {
+        "positions": rng.uniform(-40, 40, size=(n, 3)), "rotations": q, "log_scales": ls,
+        "raw_opacities": np.log(opacity) - np.log1p(-opacity),
+        "features": rng.normal(scale=0.5, size=(n, 4))}.items()}
+
+
+@pytest.mark.parametrize("case", ["clamp", "ill_conditioned", "mixed"])
+def test_general_blend_paths(xg, case):
+    """Scenes that force the kernels' general variants - sigma clamped at 0.99
+    (alpha >= 0.99), ill-conditioned conics (the p2 <= 0 test kept) - against
+    the oracle: forward bit-exact integers / 2e-5 image, backward normwise
+    1e-4.  (ACUI scenes never leave the fast path.)"""
+    import torch
+
+    rng = np.random.default_rng({"clamp": 11, "ill_conditioned": 12, "mixed": 13}[case])
+    n = 300
+    if case == "clamp":
+        f = _random_fields(rng, n, rng.uniform(0.985, 0.9995, size=n), 2.0, 8.0, 1.0)
+    elif case == "ill_conditioned":
+        # (the +0.3 px^2 low-pass bounds cond(cov2d) by lambda_max / 0.3: only
+        # splats spanning ~1000 px reach det < 1e-6 tr^2 - one axis ~ metres)
+        f = _random_fields(rng, n, rng.uniform(0.05, 0.6, size=n), 0.3, 1.5, 2000.0)
+    else:
+        f = _random_fields(rng, n, np.where(rng.uniform(size=n) < 0.3, 0.995, 0.3), 0.5, 6.0, 1.0)
+        f["log_scales"][: n // 4, 1] += np.float32(np.log(2000.0))
+    basis = np.ones(4, np.float32)
+    cloud = xg.GaussianCloud(**f, basis_weights=basis, device="cuda")
+    d = 96
+    sc = xg.ScannerConfig(L_SO, L_SD, d, d, 2.0)
+    phi = 0.4
+    proj, sp = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (d, d))
+    torch.cuda.synchronize()
+    cam = orc.camera_from_view(L_SO, L_SD, d, d, 2.0, phi)
+    pre = orc.preprocess(f, basis, cam)
+    binned = orc.bin_entries(pre, cam)
+    fwd = orc.composite_fwd(pre, binned, d, d)
+    # the scene really exercises the general variant (same criteria as the kernels)
+    act = np.flatnonzero(pre["active"])
+    c = pre["coef"][act].astype(np.float32)
+    A, B, C, alpha = c[:, 0], c[:, 1], c[:, 2], c[:, 3]
+    det, tr = A * C - np.float32(0.25) * B * B, A + C
+    general = ~(alpha < np.float32(0.98999)) | ~((A < 0) & (C < 0) & (det >= np.float32(1e-6) * tr * tr))
+    assert general.mean() > 0.1, (case, general.mean())
+    _check_forward(case, proj, sp, pre, binned, fwd)
+    dl = rng.normal(size=(d, d)) / (d * d)
+    kg = {k: torch.zeros(s, dtype=torch.float64, device="cuda")
+          for k, s in (("g_mean", (n, 2)), ("g_conic", (n, 3)), ("g_int", n), ("g_alpha", n))}
+    xg.render_backward(cloud, sp, torch.as_tensor(dl), kernel_grads=kg)
+    torch.cuda.synchronize()
+    want = orc.composite_bwd(pre, binned, d, d, dl)
+    floor = 1e-3 * max(np.abs(v[act]).max() for v in want.values())
+    for k, ref in want.items():
+        ok, rel = normwise_ok(kg[k].cpu().numpy()[act], ref[act], floor)
+        assert ok, (case, k, rel)

@@ -165,6 +165,8 @@ struct FwdArgs {
   const float* target;
   double* l1_sum;
   int* unit_cost;  // optional: entries each unit's reverse replay will walk
+  const uint32_t* n_entries;  // counters[XG_CTR_ENTRIES] (or null)
+  long long cap;              // entry capacity: an overflowed view is skipped (re-binned by the caller)
   int ntx, w, h;
 };
 
@@ -317,6 +319,9 @@ __global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd(Fwd
   int* kk = s_k[warp];
   int tile, quad;
   bool first = true;
+  // an entry-buffer overflow leaves tile ranges past the buffer: touch nothing
+  // (the caller sees XG_ST_ENTRY_OVERFLOW and re-bins the view)
+  if (a.n_entries && (long long)*a.n_entries > a.cap) return;
   while (next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
     const float2 fy = make_float2(u.fy0, u.fy1);
@@ -447,6 +452,8 @@ struct BwdArgs {
   const float* target;
   float l1_scale;
   float* grad_acc;       // [N][8]
+  const uint32_t* n_entries;  // counters[XG_CTR_ENTRIES] (or null)
+  long long cap;
   int ntx, w, h;
 };
 
@@ -644,6 +651,7 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   uint32_t* gid = s_gid[warp];
   int tile, quad;
   bool first = true;
+  if (a.n_entries && (long long)*a.n_entries > a.cap) return;  // overflowed view: see k_composite_fwd
   while (a.unit_order ? next_unit<true>(a.order, a.work, a.n_tiles, first, tile, quad)
                       : next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
     const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
@@ -816,8 +824,9 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
   cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
   FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
-            target, l1_sum, (t_final && n_contrib) ? sp->unit_cost : nullptr, tiles_x(*cam), cam->width,
-            cam->height};
+            target, l1_sum, (t_final && n_contrib) ? sp->unit_cost : nullptr,
+            sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
+            tiles_x(*cam), cam->width, cam->height};
 #ifndef XG_FWD_ALWAYS_TRACK
   if (!t_final || !n_contrib) {  // image only: no contributor tracking
     k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads,
@@ -853,8 +862,9 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   }
   BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
             (const long long*)sp->tile_ranges, by_unit ? sp->unit_order : sp->tile_order, work, n_tiles, by_unit,
-            t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc, tiles_x(*cam), cam->width,
-            cam->height};
+            t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc,
+            sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
+            tiles_x(*cam), cam->width, cam->height};
   k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
 }

@@ -28,4 +28,4 @@ for _ in range(iters):
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print(f"{iters} iterations: {1e3 * (time.perf_counter() - t0) / iters:.3f} ms/iter, N={tr.cloud.n_points}, "
-      f"entries={tr.eng.frame.last_counters[1]}")
+      f"entries={getattr(tr.eng.frame, 'last_counters', [0, -1])[1]}")

@@ -145,7 +145,10 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
 // order.  Replaces writing E (key, value) pairs and two radix passes over
 // them with one read of the rects and one write of the values.
 // ---------------------------------------------------------------------------
-constexpr int kBinThreads = 256;
+#ifndef XG_BIN_THREADS
+#define XG_BIN_THREADS 256
+#endif
+constexpr int kBinThreads = XG_BIN_THREADS;
 constexpr int kBinWarps = kBinThreads / 32;
 #ifndef XG_BIN_MAX_ROUNDS
 #define XG_BIN_MAX_ROUNDS 16

@@ -176,6 +176,18 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
 xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
                            int32_t* n_contrib, const float* target, double* l1_sum, void* stream);
 
+/* K3 over a batch of binned views that share the detector size (image only,
+ * e.g. a novel-view sweep): ONE persistent launch with one heaviest-first
+ * queue over every (view, tile, quarter) unit, so per-view tails overlap.
+ * images[i] is a device pointer to view i's [H][W] output (the array itself
+ * is host memory); 1 <= n_views <= XG_MAX_BATCH.  An overflowed view
+ * (counters[ENTRIES] > entry_capacity) is skipped.  workspace >=
+ * xg_composite_batch_workspace_bytes(cams, n_views). */
+#define XG_MAX_BATCH 16
+size_t xg_composite_batch_workspace_bytes(const xg_camera* cam, int32_t n_views);
+xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, float* const* images,
+                                 int32_t n_views, void* workspace, size_t workspace_bytes, void* stream);
+
 /* K4a: reverse replay.  Per-pixel upstream gradient is dl_dimage[H][W], or,
  * when dl_dimage == NULL, the fused L1 gradient l1_scale*sign(image-target).
  * Accumulates (atomically) into grad_acc[N][8]:

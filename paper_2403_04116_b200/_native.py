@@ -33,6 +33,7 @@ XG_ST_ENTRY_OVERFLOW = 0x8
 XG_ST_GRAD_SHIFT = 8
 XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
 XG_NCOUNTERS = 8
+XG_MAX_BATCH = 16
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
 
 c_void_p = ctypes.c_void_p
@@ -121,6 +122,8 @@ SIGNATURES = {
     "xg_intensities": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "xg_tiles_workspace_bytes": (c_size, [c_i64, c_i32, c_i32]),
     "xg_ssim_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "xg_composite_batch_workspace_bytes": (c_size, [c_void_p, c_i32]),
+    "xg_composite_fwd_batch": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_void_p, c_size, c_void_p]),
     "xg_project_workspace_bytes": (c_size, [c_i32, c_i32]),
     "xg_project_volume": (c_i32, [c_void_p, c_void_p, c_f64, c_void_p, c_void_p, c_size, c_void_p]),
     "xg_ssim": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_i32, c_f64, c_void_p, c_void_p, c_void_p, c_f64,

@@ -310,72 +310,172 @@ __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int 
 #define XG_FWD_MIN_CTAS 5
 #endif
 
+// One (tile, quarter) unit of the forward: the warp walks the tile's entry
+// list and writes the unit's 64 pixels.
+template <bool kTrack>
+__device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int quad, FRec* rec, int* kk) {
+  const int lane = threadIdx.x & 31;
+  const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
+  const float2 fy = make_float2(u.fy0, u.fy1);
+  float2 T = make_float2(u.in0 ? 1.f : 0.f, u.in1 ? 1.f : 0.f);
+  float2 acc = make_float2(0.f, 0.f);
+  int last0 = -1, last1 = -1;
+  bool alive = __any_sync(0xffffffffu, u.in0 || u.in1);
+  // two-stage prefetch: entry indices one batch ahead of the records
+  Raw nxt = fetch(entry_at(a.entry, u.start + lane, u.end), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
+  uint32_t g_nxt = entry_at(a.entry, u.start + 32 + lane, u.end);
+  for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
+    const Raw cur = nxt;
+    bool general;
+    const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
+    nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
+    g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
+    if (general)  // warp-uniform, per batch of 32 entries
+      blend_batch<true, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
+    else
+      blend_batch<false, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
+    __syncwarp();
+    alive = __any_sync(0xffffffffu, (T.x >= kFloor) || (T.y >= kFloor));
+  }
+  const float acc0 = acc.x, acc1 = acc.y, T0 = T.x, T1 = T.y;
+  const long long o0 = (long long)u.py0 * a.w + u.px;
+  float l1 = 0.f;
+  if (u.in0) {
+    a.image[o0] = acc0;
+    if (kTrack && a.t_final) {
+      a.t_final[o0] = T0;
+      a.n_contrib[o0] = last0 + 1;
+    }
+    if (a.target) l1 += fabsf(acc0 - a.target[o0]);
+  }
+  if (u.in1) {
+    const long long o1 = o0 + a.w;
+    a.image[o1] = acc1;
+    if (kTrack && a.t_final) {
+      a.t_final[o1] = T1;
+      a.n_contrib[o1] = last1 + 1;
+    }
+    if (a.target) l1 += fabsf(acc1 - a.target[o1]);
+  }
+  if (a.target && a.l1_sum) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    if (lane == 0) atomicAdd(a.l1_sum, (double)l1);
+  }
+  if (kTrack && a.unit_cost) {
+    int wl = max(last0, last1) + 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+    if (lane == 0) a.unit_cost[4 * tile + quad] = wl;
+  }
+}
+
 template <bool kTrack>
 __global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd(FwdArgs a) {
   __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  FRec* rec = s_rec[warp];
-  int* kk = s_k[warp];
+  const int warp = threadIdx.x >> 5;
   int tile, quad;
   bool first = true;
   // an entry-buffer overflow leaves tile ranges past the buffer: touch nothing
   // (the caller sees XG_ST_ENTRY_OVERFLOW and re-bins the view)
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
-  while (next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
-    const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
-    const float2 fy = make_float2(u.fy0, u.fy1);
-    float2 T = make_float2(u.in0 ? 1.f : 0.f, u.in1 ? 1.f : 0.f);
-    float2 acc = make_float2(0.f, 0.f);
-    int last0 = -1, last1 = -1;
-    bool alive = __any_sync(0xffffffffu, u.in0 || u.in1);
-    // two-stage prefetch: entry indices one batch ahead of the records
-    Raw nxt = fetch(entry_at(a.entry, u.start + lane, u.end), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
-    uint32_t g_nxt = entry_at(a.entry, u.start + 32 + lane, u.end);
-    for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
-      const Raw cur = nxt;
-      bool general;
-      const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
-      nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
-      g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
-      if (general)  // warp-uniform, per batch of 32 entries
-        blend_batch<true, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
-      else
-        blend_batch<false, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
-      __syncwarp();
-      alive = __any_sync(0xffffffffu, (T.x >= kFloor) || (T.y >= kFloor));
+  while (next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad))
+    composite_unit<kTrack>(a, tile, quad, s_rec[warp], s_k[warp]);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-view forward (image only): one persistent launch composites up to
+// kMaxBatch views of the same detector from ONE heaviest-first queue over all
+// their (view, tile, quarter) units, so no view's tail leaves SMs idle and a
+// launch measures the kernel alone.  Per-view buffers travel in the kernel
+// parameters (no device-side table).
+// ---------------------------------------------------------------------------
+constexpr int kMaxBatch = 16;
+
+struct BatchView {
+  const double2* mean2d;
+  const float4* coef;
+  const float* inten;
+  const uint32_t* entry;
+  const long long* ranges;
+  const uint32_t* n_entries;
+  long long cap;
+  float* image;
+};
+
+struct BatchArgs {
+  BatchView v[kMaxBatch];
+  const int* order;  // (view << 20) | tile, heaviest first over all views
+  uint32_t* work;
+  int n_views, n_tiles, ntx, w, h;
+};
+
+__device__ __forceinline__ bool next_batch_unit(const BatchArgs& b, bool& first, int& view, int& tile, int& quad) {
+  const uint32_t n_units = 4u * (uint32_t)(b.n_tiles * b.n_views);
+  const uint32_t G = gridDim.x, w = threadIdx.x >> 5;
+  const uint32_t dealt = min(n_units, G * (uint32_t)kWarps);
+  uint32_t k = n_units;
+  if (first) {
+    first = false;
+    k = G * w + ((w & 1u) ? G - 1u - blockIdx.x : blockIdx.x);
+  }
+  if (k >= dealt) {
+    uint32_t d = 0;
+    if ((threadIdx.x & 31) == 0) d = atomicAdd(b.work, 1u);
+    k = dealt + __shfl_sync(0xffffffffu, d, 0);
+  }
+  if (k >= n_units) return false;
+  const int vt = b.order[k >> 2];
+  view = vt >> 20;
+  tile = vt & ((1 << 20) - 1);
+  quad = (int)(k & 3u);
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_batch(BatchArgs b) {
+  __shared__ FRec s_rec[kWarps][32];
+  __shared__ int s_k[kWarps][32];
+  const int warp = threadIdx.x >> 5;
+  int view, tile, quad;
+  bool first = true;
+  while (next_batch_unit(b, first, view, tile, quad)) {
+    const BatchView& v = b.v[view];
+    if (v.n_entries && (long long)*v.n_entries > v.cap) continue;  // overflowed view: re-rendered by the caller
+    FwdArgs a{v.mean2d, v.coef, v.inten, v.entry, v.ranges, nullptr, nullptr, b.n_tiles, v.image, nullptr,
+              nullptr, nullptr, nullptr, nullptr, nullptr, 0, b.ntx, b.w, b.h};
+    composite_unit<false>(a, tile, quad, s_rec[warp], s_k[warp]);
+  }
+}
+
+// (view, tile) pairs of a batch by descending entry count (64 log buckets).
+__global__ void __launch_bounds__(1024) k_batch_tile_order(BatchArgs b, int* __restrict__ order) {
+  constexpr int NB = 64;
+  __shared__ int hist[NB];
+  __shared__ int off[NB];
+  if (threadIdx.x < NB) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = b.n_tiles * b.n_views;
+  auto key = [&](int i) {
+    const int vw = i / b.n_tiles, t = i - vw * b.n_tiles;
+    const long long* r = b.v[vw].ranges;
+    const long long len = r[2 * t + 1] - r[2 * t];
+    const int bk = len > 0 ? (int)(4.f * __log2f((float)len + 1.f)) : 0;
+    return NB - 1 - min(bk, NB - 1);
+  };
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[key(i)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int k = 0; k < NB; ++k) {
+      off[k] = run;
+      run += hist[k];
     }
-    const float acc0 = acc.x, acc1 = acc.y, T0 = T.x, T1 = T.y;
-    const long long o0 = (long long)u.py0 * a.w + u.px;
-    float l1 = 0.f;
-    if (u.in0) {
-      a.image[o0] = acc0;
-      if (kTrack && a.t_final) {
-        a.t_final[o0] = T0;
-        a.n_contrib[o0] = last0 + 1;
-      }
-      if (a.target) l1 += fabsf(acc0 - a.target[o0]);
-    }
-    if (u.in1) {
-      const long long o1 = o0 + a.w;
-      a.image[o1] = acc1;
-      if (kTrack && a.t_final) {
-        a.t_final[o1] = T1;
-        a.n_contrib[o1] = last1 + 1;
-      }
-      if (a.target) l1 += fabsf(acc1 - a.target[o1]);
-    }
-    if (a.target && a.l1_sum) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-      if (lane == 0) atomicAdd(a.l1_sum, (double)l1);
-    }
-    if (kTrack && a.unit_cost) {
-      int wl = max(last0, last1) + 1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
-      if (lane == 0) a.unit_cost[4 * tile + quad] = wl;
-    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int vw = i / b.n_tiles, t = i - vw * b.n_tiles;
+    order[atomicAdd(&off[key(i)], 1)] = (vw << 20) | t;
   }
 }
 
@@ -837,6 +937,54 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
   k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0,
                           (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
+}
+
+size_t xg_composite_batch_workspace_bytes(const xg_camera* cam, int32_t n_views) {
+  if (!cam || n_views < 1) return 256;
+  return al(sizeof(int32_t) * (size_t)n_views * (size_t)(tiles_x(*cam) * tiles_y(*cam))) + 256 + 256;
+}
+
+xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, float* const* images,
+                                 int32_t n_views, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!cams || !sps || !images || !workspace || n_views < 1 || n_views > kMaxBatch) {
+    set_error_msg("xg_composite_fwd_batch: invalid argument (1 <= n_views <= XG_MAX_BATCH)");
+    return XG_ERR_INVALID;
+  }
+  if (workspace_bytes < xg_composite_batch_workspace_bytes(cams, n_views)) {
+    set_error_msg("xg_composite_fwd_batch: workspace too small");
+    return XG_ERR_WORKSPACE;
+  }
+  BatchArgs b{};
+  const xg_camera& c0 = cams[0];
+  for (int i = 0; i < n_views; ++i) {
+    const xg_splats* sp = sps + i;
+    if (cams[i].width != c0.width || cams[i].height != c0.height || !images[i] || !sp->entry_splat ||
+        !sp->tile_ranges || !sp->mean2d || !sp->coef || !sp->inten) {
+      set_error_msg("xg_composite_fwd_batch: views must share the detector size and be binned");
+      return XG_ERR_INVALID;
+    }
+    b.v[i] = BatchView{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+                       (const long long*)sp->tile_ranges,
+                       sp->entry_capacity > 0 && sp->counters ? sp->counters + XG_CTR_ENTRIES : nullptr,
+                       (long long)sp->entry_capacity, images[i]};
+  }
+  b.n_views = n_views;
+  b.n_tiles = tiles_x(c0) * tiles_y(c0);
+  b.ntx = tiles_x(c0);
+  b.w = c0.width;
+  b.h = c0.height;
+  int* order = (int*)workspace;
+  uint32_t* work = (uint32_t*)((char*)workspace + al(sizeof(int32_t) * (size_t)n_views * (size_t)b.n_tiles));
+  b.order = order;
+  b.work = work;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(work, 0, sizeof(uint32_t), s);
+  k_batch_tile_order<<<1, 1024, 0, s>>>(b, order);
+  xg_status st = check_launch("k_batch_tile_order");
+  if (st != XG_OK) return st;
+  k_composite_fwd_batch<<<persistent_grid(k_composite_fwd_batch, 4 * b.n_tiles * n_views, "XG_FWD_CTAS_PER_SM"),
+                          kThreads, 0, s>>>(b);
+  return check_launch("k_composite_fwd_batch");
 }
 
 xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,

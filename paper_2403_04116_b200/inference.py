@@ -15,7 +15,7 @@ ranks with no collective (see ``parallel.py``).
 
 from __future__ import annotations
 
-import os
+import ctypes
 
 import numpy as np
 import torch
@@ -23,30 +23,40 @@ import torch
 from . import _native as nat
 from .engine import Frame
 from .gaussians import GaussianCloud
-from .geometry import ScannerConfig, camera_pod, extrinsic_from_angle, intrinsic_from_config
+from .geometry import ScannerConfig, XgCamera, camera_pod, extrinsic_from_angle, intrinsic_from_config
 
 
 class SweepRenderer:
-    """Reusable multi-stream renderer for one cloud and one detector."""
+    """Reusable multi-stream renderer for one cloud and one detector.
+
+    ``batch == 1``: view i runs preprocess -> bin -> composite on stream
+    i % n_streams (one ``Frame`` per stream), so the binning of later views
+    overlaps the compositing of earlier ones.
+
+    ``batch == K > 1``: K views are binned concurrently on K streams into one
+    of two frame sets, then composited by ONE ``xg_composite_fwd_batch``
+    launch over all their units (one heaviest-first queue, no per-view tail)
+    on a composite stream, while the next K views are binned into the other
+    set."""
 
     def __init__(self, cloud: GaussianCloud, scanner: ScannerConfig, n_streams: int = 3,
-                 capacity_factor: float = 1.3, priority_composite: bool | None = None):
+                 capacity_factor: float = 1.3, batch: int = 1):
         nat.require_cuda(cloud.flat, "cloud")
         self.cloud = cloud
         self.scanner = scanner
         self.h, self.w = scanner.detector_height, scanner.detector_width
         self.intr = intrinsic_from_config(scanner)
-        self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, n_streams))]
-        if priority_composite is None:
-            priority_composite = os.environ.get("XG_PRIORITY_COMPOSITE", "0") == "1"
-        # optional: compositing on high-priority streams, so the binning of the
-        # next views only fills the SMs the persistent composite leaves idle
-        self.comp_streams = ([torch.cuda.Stream(device=cloud.device, priority=-1) for _ in self.streams]
-                             if priority_composite else None)
+        self.batch = int(batch)
+        if not 1 <= self.batch <= nat.XG_MAX_BATCH:
+            raise ValueError(f"batch must be in [1, {nat.XG_MAX_BATCH}]")
+        n = self.batch if self.batch > 1 else max(1, n_streams)
+        self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(n)]
+        self.comp_stream = torch.cuda.Stream(device=cloud.device) if self.batch > 1 else None
         self.capacity_factor = capacity_factor
         self.frames: list[Frame] = []
         self.capacity = 0
         self.kernel_launches = 0
+        self._batch_ws = None
 
     def _probe_capacity(self, phi: float) -> int:
         fr = Frame(self.cloud.n_points, self.h, self.w, self.cloud.device)
@@ -62,60 +72,103 @@ class SweepRenderer:
         angles = np.atleast_1d(np.asarray(angles, dtype=np.float64))
         if not self.frames or self.capacity == 0:
             self.capacity = self._probe_capacity(float(angles[0]))
+            n = 2 * self.batch if self.batch > 1 else len(self.streams)
             self.frames = [Frame(self.cloud.n_points, self.h, self.w, self.cloud.device,
-                                 entry_capacity=self.capacity) for _ in self.streams]
+                                 entry_capacity=self.capacity) for _ in range(n)]
+        if self.batch > 1 and self._batch_ws is None:
+            cam = self.camera(float(angles[0]))
+            nb = nat.lib().xg_composite_batch_workspace_bytes(ctypes.byref(cam), self.batch)
+            self._batch_ws = torch.empty(int(nb), dtype=torch.uint8, device=self.cloud.device)
 
     def render(self, angles, out: torch.Tensor | None = None, host_out: torch.Tensor | None = None,
                check: bool = True, composite_events: list | None = None) -> torch.Tensor:
         """Render every angle into ``out`` ([V, H, W] float32 on the device).
         If ``host_out`` (pinned [V, H, W]) is given, each image is also copied
-        to it asynchronously on the view's stream.  ``composite_events``
-        collects (start, end) CUDA events around every compositing launch,
-        recorded on the stream it runs on."""
+        to it asynchronously.  ``composite_events`` collects (start, end, views)
+        CUDA events around every compositing launch, recorded on the stream
+        it runs on."""
         angles = np.atleast_1d(np.asarray(angles, dtype=np.float64))
         v = angles.shape[0]
         self.prepare(angles)
         if out is None:
             out = torch.empty((v, self.h, self.w), dtype=torch.float32, device=self.cloud.device)
         status = torch.zeros(v, dtype=torch.int32, device=self.cloud.device)
+        if self.batch > 1:
+            self._render_batched(angles, out, host_out, status, composite_events)
+        else:
+            self._render_streams(angles, out, host_out, status, composite_events)
+        if check:
+            self.finish(angles, out, host_out, status)
+        return out
+
+    def _render_streams(self, angles, out, host_out, status, composite_events) -> None:
         main = torch.cuda.current_stream()
         for s in self.streams:
             s.wait_stream(main)
-        launches = 0
-        if self.comp_streams is not None:
-            for s in self.comp_streams:
-                s.wait_stream(main)
         for i, phi in enumerate(angles):
             k = i % len(self.streams)
             st, fr = self.streams[k], self.frames[k]
             with torch.cuda.stream(st):
-                if self.comp_streams is not None:
-                    st.wait_stream(self.comp_streams[k])  # the frame's previous composite is done
                 fr.preprocess(self.cloud, self.camera(phi))
                 fr.bin()
-            if self.comp_streams is not None:
-                self.comp_streams[k].wait_stream(st)
-                st = self.comp_streams[k]
-            with torch.cuda.stream(st):
                 if composite_events is not None:
                     a = torch.cuda.Event(enable_timing=True)
                     b = torch.cuda.Event(enable_timing=True)
                     a.record(st)
                     fr.composite(image_out=out[i], track=False)
                     b.record(st)
-                    composite_events.append((a, b))
+                    composite_events.append((a, b, 1))
                 else:
                     fr.composite(image_out=out[i], track=False)
                 status[i : i + 1].copy_(fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
                 if host_out is not None:
                     host_out[i].copy_(out[i], non_blocking=True)
-            launches += 1
-        for s in self.streams + (self.comp_streams or []):
+        for s in self.streams:
             main.wait_stream(s)
-        self.kernel_launches = launches
-        if check:
-            self.finish(angles, out, host_out, status)
-        return out
+        self.kernel_launches = len(angles)
+
+    def _render_batched(self, angles, out, host_out, status, composite_events) -> None:
+        main = torch.cuda.current_stream()
+        cs, K = self.comp_stream, self.batch
+        for s in self.streams + [cs]:
+            s.wait_stream(main)
+        done = [None, None]  # composite-finished event per frame set
+        lib = nat.lib()
+        for j, lo in enumerate(range(0, len(angles), K)):
+            hi = min(lo + K, len(angles))
+            fs = self.frames[(j % 2) * K:(j % 2) * K + K]
+            for i in range(lo, hi):
+                st, fr = self.streams[i - lo], fs[i - lo]
+                with torch.cuda.stream(st):
+                    if done[j % 2] is not None:
+                        st.wait_event(done[j % 2])  # the set's previous composite read these buffers
+                    fr.preprocess(self.cloud, self.camera(angles[i]))
+                    fr.bin()
+                cs.wait_stream(st)
+            nv = hi - lo
+            cams = (XgCamera * nv)(*[fs[i].cam for i in range(nv)])
+            sps = (nat.XgSplats * nv)(*[fs[i].splats_struct() for i in range(nv)])
+            imgs = (ctypes.c_void_p * nv)(*[out[lo + i].data_ptr() for i in range(nv)])
+            with torch.cuda.stream(cs):
+                a = b = None
+                if composite_events is not None:
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(cs)
+                nat.check(lib.xg_composite_fwd_batch(cams, sps, imgs, nv, self._batch_ws.data_ptr(),
+                                                     self._batch_ws.numel(), nat.stream()), "xg_composite_fwd_batch")
+                if b is not None:
+                    b.record(cs)
+                    composite_events.append((a, b, nv))
+                for i in range(nv):
+                    status[lo + i : lo + i + 1].copy_(fs[i].counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
+                if host_out is not None:
+                    host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                done[j % 2] = ev
+        for s in self.streams + [cs]:
+            main.wait_stream(s)
+        self.kernel_launches = (len(angles) + K - 1) // K
 
     def finish(self, angles, out, host_out, status: torch.Tensor) -> None:
         st = status.cpu().numpy().astype(np.int64) & 0xFFFFFFFF

@@ -113,9 +113,11 @@ def test_backward_full_size_c1(xg):
     assert torch.isfinite(grads.flat).all()
 
 
-def test_sweep_matches_single_renders(xg):
-    """The multi-stream sweep (the bench path) renders every view exactly as
-    render() does: same kernels, buffers per stream."""
+@pytest.mark.parametrize("batch", [1, 3, 4])
+def test_sweep_matches_single_renders(xg, batch):
+    """The sweep renderer (the bench path) renders every view exactly as
+    render() does - per-view streams (batch 1) and the multi-view
+    compositing launch (xg_composite_fwd_batch, incl. a partial last batch)."""
     import torch
 
     from paper_2403_04116_b200.inference import SweepRenderer
@@ -123,8 +125,13 @@ def test_sweep_matches_single_renders(xg):
     g, d = CONFIGS["C3"]
     cloud = xg.GaussianCloud(**_arrays(g), device="cuda")
     sc = xg.ScannerConfig(L_SO, L_SD, d, d, 192.0 / d)
-    angles = np.array([0.0, 0.3, np.pi / 4, 1.2, 2.9])
-    out = SweepRenderer(cloud, sc, n_streams=3).render(angles)
+    angles = np.array([0.0, 0.3, np.pi / 4, 1.2, 2.9, 0.05, 1.7, 2.2, 0.9, 3.0, 1.45])
+    rend = SweepRenderer(cloud, sc, n_streams=3, batch=batch)
+    out = rend.render(angles)
+    host = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+    out2 = rend.render(angles, host_out=host)  # frames reused, host copies
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2) and torch.equal(host, out.cpu())
     for i, phi in enumerate(angles):
         proj, _ = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (d, d))
         assert torch.equal(out[i], proj.pixels.to(out.dtype)), i

@@ -262,10 +262,12 @@ def fp32_peak() -> tuple[float, str]:
     return 74.45, "nominal 148 SM x 128 FMA x 2 x 1.965 GHz (no measured FP32 peak)"
 
 
-def dram_traffic_per_launch() -> float | None:
+def dram_traffic_per_view(batched: bool) -> float | None:
+    """DRAM bytes per composited view from the committed ncu capture."""
     p = ROOT / "profiles" / "ncu_composite_fwd.json"
     if p.exists():
-        return float(json.loads(p.read_text())["dram_bytes_per_launch"])
+        d = json.loads(p.read_text())
+        return float(d["dram_bytes_per_view_batched" if batched else "dram_bytes_per_view_single"])
     return None
 
 
@@ -403,7 +405,8 @@ def run_ours(args) -> None:
         "roofline": {"bound": "fp32", "kernel": "k_composite_fwd_batch" if args.batch > 1 else "k_composite_fwd",
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": (dram_traffic_per_launch() * launch_views) if dram_traffic_per_launch() else None,
+                     "traffic": (dram_traffic_per_view(args.batch > 1) * launch_views
+                                 if dram_traffic_per_view(args.batch > 1) else None),
                      "flop_per_unit": FLOP_PER_PAIR, "units_per_launch": pairs_per_view * launch_views,
                      "views_per_launch": launch_views,
                      "kernel_ms_in_timed_region": comp_ctx * launch_views, "kernel_ms_isolated": comp_iso_ms,

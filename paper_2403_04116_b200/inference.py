@@ -188,8 +188,11 @@ class SweepRenderer:
             self.frames = []  # grow all frames on the next sweep
 
 
-def render_sweep(cloud: GaussianCloud, scanner: ScannerConfig, angles=None, n_streams: int = 3) -> torch.Tensor:
-    """Render ``angles`` (default: the scanner's) into a [V, H, W] device stack."""
+def render_sweep(cloud: GaussianCloud, scanner: ScannerConfig, angles=None, n_streams: int = 3,
+                 batch: int = 8) -> torch.Tensor:
+    """Render ``angles`` (default: the scanner's) into a [V, H, W] device
+    stack (batches of ``batch`` views per compositing launch)."""
     if angles is None:
         angles = scanner.angles
-    return SweepRenderer(cloud, scanner, n_streams).render(angles)
+    n = np.atleast_1d(angles).size
+    return SweepRenderer(cloud, scanner, n_streams, batch=max(1, min(batch, n))).render(angles)

@@ -102,6 +102,11 @@ typedef struct xg_cloud {
   int64_t n;
   int32_t n_features;
   int32_t _pad;
+  const float* intensities;  /* optional [N] sigmoid(F . lambda) from xg_intensities: the
+                                projection copies (or, when xg_splats.inten points at this
+                                very buffer, just uses) it instead of recomputing the
+                                view-independent intensity per view - the non-finite
+                                feature check is then xg_intensities' */
 } xg_cloud;
 
 /* Per-view screen-space buffers.  Per-Gaussian arrays are indexed by cloud

@@ -45,7 +45,8 @@ c_size = ctypes.c_size_t
 
 
 class XgCloud(ctypes.Structure):
-    _fields_ = [("params", c_void_p), ("basis", c_void_p), ("n", c_i64), ("n_features", c_i32), ("_pad", c_i32)]
+    _fields_ = [("params", c_void_p), ("basis", c_void_p), ("n", c_i64), ("n_features", c_i32), ("_pad", c_i32),
+                ("intensities", c_void_p)]
 
 
 class XgVolume(ctypes.Structure):
@@ -214,12 +215,13 @@ def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def cloud_struct(cloud) -> XgCloud:
+def cloud_struct(cloud, intensities: torch.Tensor | None = None) -> XgCloud:
     s = XgCloud()
     s.params = ptr(cloud.flat, "cloud")
     s.basis = ptr(cloud.basis_weights, "basis_weights")
     s.n = cloud.n_points
     s.n_features = cloud.n_features
+    s.intensities = ptr(intensities, "intensities")
     return s
 
 

@@ -40,6 +40,7 @@ struct CloudPtrs {
   const float* raw;
   const float* feat;
   const float* basis;
+  const float* inten_pre;  // optional precomputed sigmoid(F . lambda) (xg_cloud.intensities)
   long long n;
   int nf;
 };
@@ -53,6 +54,7 @@ __host__ static CloudPtrs make_cloud(const xg_cloud& c) {
   p.raw = p.logs + 3 * n;
   p.feat = p.raw + n;
   p.basis = c.basis;
+  p.inten_pre = c.intensities;
   p.n = n;
   p.nf = c.n_features;
   return p;
@@ -172,10 +174,14 @@ __global__ void k_preprocess(CloudPtrs c, Cam k, xg_splats sp, xg_splat_extras e
   if (i < c.n) {
     Proj p;
     project_one(c, k, i, p);
-    bool finite;
-    const double inten = intensity_of(c, i, &finite);
-    sp.inten[i] = (float)inten;
-    if (!finite) status |= XG_ST_NONFINITE_FEAT;
+    if (c.inten_pre) {  // view-independent: computed once per cloud (xg_intensities)
+      if (sp.inten != c.inten_pre) sp.inten[i] = c.inten_pre[i];
+    } else {
+      bool finite;
+      const double inten = intensity_of(c, i, &finite);
+      sp.inten[i] = (float)inten;
+      if (!finite) status |= XG_ST_NONFINITE_FEAT;
+    }
     uint32_t ntiles = 0;
     unsigned long long key = ~0ull;
     if (p.visible && p.zero_q) status |= XG_ST_ZERO_QUAT;

@@ -42,6 +42,7 @@ class Frame:
         self.mean2d = torch.empty((n, 2), dtype=torch.float64, device=dev)
         self.coef = torch.empty((n, 4), dtype=torch.float32, device=dev)
         self.inten = torch.empty(n, dtype=torch.float32, device=dev)
+        self._own_inten = self.inten
         self.rect = torch.empty((n, 4), dtype=torch.int16, device=dev)
         self.tiles_touched = torch.empty(n, dtype=torch.int32, device=dev)
         self.depth_key = torch.empty(n, dtype=torch.int64, device=dev)
@@ -100,11 +101,18 @@ class Frame:
         return s
 
     # --- stages -------------------------------------------------------------
-    def preprocess(self, cloud, cam: XgCamera) -> None:
+    def preprocess(self, cloud, cam: XgCamera, intensities: torch.Tensor | None = None) -> None:
+        """K1.  ``intensities`` (the cloud's precomputed [N] float32
+        sigmoid(F . lambda), e.g. for a sweep) is used as this frame's
+        intensity buffer instead of recomputing it per view."""
         if cloud.n_points != self.n:
             raise ValueError("frame was allocated for a different cloud size")
         self.cam = cam
-        cs = nat.cloud_struct(cloud)
+        if intensities is not None:
+            self.inten = intensities  # shared, read-only for the compositing kernels
+        elif getattr(self, "_own_inten", None) is not None and self.inten is not self._own_inten:
+            self.inten = self._own_inten
+        cs = nat.cloud_struct(cloud, intensities)
         sp = self.splats_struct()
         ex = None
         if self.extras is not None:

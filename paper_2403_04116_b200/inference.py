@@ -93,6 +93,9 @@ class SweepRenderer:
         if out is None:
             out = torch.empty((v, self.h, self.w), dtype=torch.float32, device=self.cloud.device)
         status = torch.zeros(v, dtype=torch.int32, device=self.cloud.device)
+        # the intensities are view-independent (isotropic RIRF): once per sweep
+        # (raises for non-finite features, as the per-view check would)
+        self._inten = nat.intensities(self.cloud)
         if self.batch > 1:
             self._render_batched(angles, out, host_out, status, composite_events)
         else:
@@ -109,7 +112,7 @@ class SweepRenderer:
             k = i % len(self.streams)
             st, fr = self.streams[k], self.frames[k]
             with torch.cuda.stream(st):
-                fr.preprocess(self.cloud, self.camera(phi))
+                fr.preprocess(self.cloud, self.camera(phi), self._inten)
                 fr.bin()
                 if composite_events is not None:
                     a = torch.cuda.Event(enable_timing=True)
@@ -142,7 +145,7 @@ class SweepRenderer:
                 with torch.cuda.stream(st):
                     if done[j % 2] is not None:
                         st.wait_event(done[j % 2])  # the set's previous composite read these buffers
-                    fr.preprocess(self.cloud, self.camera(angles[i]))
+                    fr.preprocess(self.cloud, self.camera(angles[i]), self._inten)
                     fr.bin()
                 cs.wait_stream(st)
             nv = hi - lo

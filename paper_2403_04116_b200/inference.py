@@ -16,6 +16,7 @@ ranks with no collective (see ``parallel.py``).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -50,7 +51,9 @@ class SweepRenderer:
         if not 1 <= self.batch <= nat.XG_MAX_BATCH:
             raise ValueError(f"batch must be in [1, {nat.XG_MAX_BATCH}]")
         n = self.batch if self.batch > 1 else max(1, n_streams)
-        self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(n)]
+        # (high-priority binning streams measured 1-3 % slower: XG_BIN_PRIORITY=1)
+        prio = -1 if (self.batch > 1 and os.environ.get("XG_BIN_PRIORITY", "0") == "1") else 0
+        self.streams = [torch.cuda.Stream(device=cloud.device, priority=prio) for _ in range(n)]
         self.comp_stream = torch.cuda.Stream(device=cloud.device) if self.batch > 1 else None
         self.capacity_factor = capacity_factor
         self.frames: list[Frame] = []

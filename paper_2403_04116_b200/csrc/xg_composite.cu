@@ -370,6 +370,18 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int q
   }
 }
 
+// Non-persistent single-view variant: one CTA per tile (heaviest first),
+// its 4 warps the quarters.
+template <bool kTrack>
+__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_np(FwdArgs a) {
+  __shared__ FRec s_rec[kWarps][32];
+  __shared__ int s_k[kWarps][32];
+  const int warp = threadIdx.x >> 5;
+  if (a.n_entries && (long long)*a.n_entries > a.cap) return;
+  const int tile = a.order[blockIdx.x];
+  for (int quad = warp; quad < 4; quad += kWarps) composite_unit<kTrack>(a, tile, quad, s_rec[warp], s_k[warp]);
+}
+
 template <bool kTrack>
 __global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd(FwdArgs a) {
   __shared__ FRec s_rec[kWarps][32];
@@ -945,15 +957,22 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
             target, l1_sum, (t_final && n_contrib) ? sp->unit_cost : nullptr,
             sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
             tiles_x(*cam), cam->width, cam->height};
+  static const bool np = getenv("XG_FWD_NONPERSISTENT") && atoi(getenv("XG_FWD_NONPERSISTENT")) > 0;
 #ifndef XG_FWD_ALWAYS_TRACK
   if (!t_final || !n_contrib) {  // image only: no contributor tracking
-    k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads,
-                             0, (cudaStream_t)stream>>>(a);
+    if (np && kWarps == 4)
+      k_composite_fwd_np<false><<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+    else
+      k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"),
+                               kThreads, 0, (cudaStream_t)stream>>>(a);
     return check_launch("k_composite_fwd");
   }
 #endif
-  k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads, 0,
-                          (cudaStream_t)stream>>>(a);
+  if (np && kWarps == 4)
+    k_composite_fwd_np<true><<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+  else
+    k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads,
+                            0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
 }
 

@@ -765,6 +765,51 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
   }
 }
 
+// One (tile, quarter) unit of the reverse replay.
+__device__ __forceinline__ void bwd_unit(const BwdArgs& a, int tile, int quad, BRec* rec, int* kk, uint32_t* gid) {
+  const int lane = threadIdx.x & 31;
+  const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
+  const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
+  float2 T = make_float2(0.f, 0.f), g = make_float2(0.f, 0.f);
+  int last0 = -1, last1 = -1;
+  if (u.in0) {
+    T.x = a.t_final[o0];
+    last0 = a.n_contrib[o0] - 1;
+    g.x = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
+  }
+  if (u.in1) {
+    T.y = a.t_final[o1];
+    last1 = a.n_contrib[o1] - 1;
+    g.y = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
+  }
+  if (g.x == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
+  if (g.y == 0.f) last1 = -1;
+  int wl = max(last0, last1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+  const long long hi = u.start + wl + 1;  // one past the last entry this warp needs
+  const float2 fy = make_float2(u.fy0, u.fy1);
+  float2 nS = make_float2(0.f, 0.f);
+  // batches of 32 walked back to front: [b1 - 32, b1); two-stage prefetch
+  // (entry indices one batch ahead of the records)
+  Raw nxt = fetch(hi - 32 + lane >= u.start ? entry_at(a.entry, hi - 32 + lane, hi) : 0u,
+                  hi - 32 + lane >= u.start && hi - 32 + lane < hi, a.mean2d, a.coef, a.inten);
+  uint32_t g_nxt = hi - 64 + lane >= u.start ? entry_at(a.entry, hi - 64 + lane, hi) : 0u;
+  for (long long b1 = hi; b1 > u.start; b1 -= 32) {
+    const Raw cur = nxt;
+    bool general;
+    const int cnt = compact_bwd(cur, (int)(b1 - 32 - u.start) + lane, u, rec, kk, gid, general);
+    const long long kn = b1 - 64 + lane;
+    nxt = fetch(g_nxt, kn >= u.start, a.mean2d, a.coef, a.inten);
+    g_nxt = kn - 32 >= u.start ? entry_at(a.entry, kn - 32, hi) : 0u;
+    if (general)
+      unblend_batch<true>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
+    else
+      unblend_batch<false>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
+    __syncwarp();
+  }
+}
+
 // (no min-blocks bound: ptxas then settles at 92 registers = 5 CTAs per SM,
 // measured fastest; forcing 6+ CTAs spills or slows the replay)
 #ifdef XG_BWD_MIN_CTAS
@@ -775,7 +820,7 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   __shared__ BRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   __shared__ uint32_t s_gid[kWarps][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   BRec* rec = s_rec[warp];
   int* kk = s_k[warp];
   uint32_t* gid = s_gid[warp];
@@ -783,48 +828,19 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd(BwdArgs a) {
   bool first = true;
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;  // overflowed view: see k_composite_fwd
   while (a.unit_order ? next_unit<true>(a.order, a.work, a.n_tiles, first, tile, quad)
-                      : next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad)) {
-    const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
-    const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
-    float2 T = make_float2(0.f, 0.f), g = make_float2(0.f, 0.f);
-    int last0 = -1, last1 = -1;
-    if (u.in0) {
-      T.x = a.t_final[o0];
-      last0 = a.n_contrib[o0] - 1;
-      g.x = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
-    }
-    if (u.in1) {
-      T.y = a.t_final[o1];
-      last1 = a.n_contrib[o1] - 1;
-      g.y = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
-    }
-    if (g.x == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
-    if (g.y == 0.f) last1 = -1;
-    int wl = max(last0, last1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
-    const long long hi = u.start + wl + 1;  // one past the last entry this warp needs
-    const float2 fy = make_float2(u.fy0, u.fy1);
-    float2 nS = make_float2(0.f, 0.f);
-    // batches of 32 walked back to front: [b1 - 32, b1); two-stage prefetch
-    // (entry indices one batch ahead of the records)
-    Raw nxt = fetch(hi - 32 + lane >= u.start ? entry_at(a.entry, hi - 32 + lane, hi) : 0u,
-                    hi - 32 + lane >= u.start && hi - 32 + lane < hi, a.mean2d, a.coef, a.inten);
-    uint32_t g_nxt = hi - 64 + lane >= u.start ? entry_at(a.entry, hi - 64 + lane, hi) : 0u;
-    for (long long b1 = hi; b1 > u.start; b1 -= 32) {
-      const Raw cur = nxt;
-      bool general;
-      const int cnt = compact_bwd(cur, (int)(b1 - 32 - u.start) + lane, u, rec, kk, gid, general);
-      const long long kn = b1 - 64 + lane;
-      nxt = fetch(g_nxt, kn >= u.start, a.mean2d, a.coef, a.inten);
-      g_nxt = kn - 32 >= u.start ? entry_at(a.entry, kn - 32, hi) : 0u;
-      if (general)
-        unblend_batch<true>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
-      else
-        unblend_batch<false>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
-      __syncwarp();
-    }
-  }
+                      : next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad))
+    bwd_unit(a, tile, quad, rec, kk, gid);
+}
+
+// Non-persistent variant: one single-warp CTA per unit, dispatched by the
+// hardware in the forward's replay-cost order (heaviest first).
+__global__ void __launch_bounds__(32) k_composite_bwd_np(BwdArgs a) {
+  __shared__ BRec s_rec[32];
+  __shared__ int s_k[32];
+  __shared__ uint32_t s_gid[32];
+  if (a.n_entries && (long long)*a.n_entries > a.cap) return;
+  const int uidx = a.unit_order ? a.order[blockIdx.x] : 4 * a.order[blockIdx.x >> 2] + (int)(blockIdx.x & 3);
+  bwd_unit(a, uidx >> 2, uidx & 3, s_rec, s_k, s_gid);
 }
 
 // ---------------------------------------------------------------------------
@@ -1064,6 +1080,11 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
             t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc,
             sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
             tiles_x(*cam), cam->width, cam->height};
+  const char* npe = getenv("XG_BWD_NONPERSISTENT");
+  if (npe && atoi(npe) > 0) {
+    k_composite_bwd_np<<<4 * n_tiles, 32, 0, (cudaStream_t)stream>>>(a);
+    return check_launch("k_composite_bwd_np");
+  }
   k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
 }

@@ -262,3 +262,33 @@ def test_general_blend_paths(xg, case):
     for k, ref in want.items():
         ok, rel = normwise_ok(kg[k].cpu().numpy()[act], ref[act], floor)
         assert ok, (case, k, rel)
+
+
+def test_sweep_with_empty_views(xg):
+    """Views in which every splat is culled (empty entry lists) composite to
+    exact zeros in both sweep modes, next to non-empty views."""
+    import torch
+
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    rng = np.random.default_rng(5)
+    n = 40
+    f = _random_fields(rng, n, rng.uniform(0.1, 0.5, size=n), 2.0, 5.0, 1.0)
+    f["positions"][:, 1] = np.float32(300.0)  # off-axis: on screen only near phi = pi/2
+    f["positions"][:, 0] = rng.uniform(-10, 10, size=n).astype(np.float32)
+    f["positions"][:, 2] = rng.uniform(-10, 10, size=n).astype(np.float32)
+    cloud = xg.GaussianCloud(**f, basis_weights=np.ones(4, np.float32), device="cuda")
+    sc = xg.ScannerConfig(L_SO, L_SD, 64, 64, 3.0)
+    angles = np.array([0.0, 0.2, np.pi / 2, 2.9, np.pi / 2 + 0.01])
+    empty = 0
+    for batch in (1, 4):
+        out = SweepRenderer(cloud, sc, n_streams=2, batch=batch).render(angles)
+        for i, phi in enumerate(angles):
+            proj, sp = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (64, 64))
+            assert torch.equal(out[i], proj.pixels.to(out.dtype)), (batch, i)
+            if sp.n_active == 0:
+                empty += 1
+                assert float(out[i].abs().max()) == 0.0
+            else:
+                assert float(out[i].abs().max()) > 0.0
+    assert 0 < empty < 2 * len(angles)

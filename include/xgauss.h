@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define XG_ABI_VERSION 1
+#define XG_ABI_VERSION 2
 
 typedef enum xg_status {
   XG_OK = 0,
@@ -68,6 +68,7 @@ typedef enum xg_status {
 #define XG_CTR_TOUCH    3   /* scratch                                        */
 #define XG_CTR_STICKY   4   /* caller-owned, never written by the library     */
 #define XG_CTR_QUEUE    5   /* tile work-queue head of the compositing kernels */
+#define XG_CTR_ITEMS    6   /* chunk count of the checkpointed reverse replay  */
 #define XG_NCOUNTERS    8
 
 /* Blend constants (rasterizer/kernels_py.py:13-19, frontend.py:36,
@@ -135,6 +136,15 @@ typedef struct xg_splats {
                              xg_composite_fwd; optional)                    */
   int32_t*  unit_order;   /* [4*n_tiles] quarter-tiles by descending
                              unit_cost (reverse-replay schedule; scratch)   */
+  /* Optional replay checkpoints (training frames).  When replay_ckpt is set,
+   * a tracking xg_composite_fwd stores every pixel's (T, acc) before each
+   * XG_REPLAY_CHUNK-th entry of its tile, and xg_composite_bwd (given
+   * unit_cost and the forward's image) splits every tile's reverse replay
+   * into independent XG_REPLAY_CHUNK-entry chunks.  Both calls must see the
+   * same buffers. */
+  float*    replay_ckpt;  /* [replay_slots][256][2]                          */
+  uint32_t* replay_items; /* [4*replay_slots][2] chunk list (scratch)        */
+  int64_t   replay_slots; /* >= xg_replay_slots(entry_capacity, n_tiles)     */
 } xg_splats;
 
 /* Optional float64 API outputs of the projection (frontend.py:58-74); any
@@ -156,6 +166,11 @@ uint64_t xg_kernel_launches(void);
 /* Tile grid of a camera. */
 int32_t xg_tiles_x(const xg_camera* cam);
 int32_t xg_tiles_y(const xg_camera* cam);
+
+/* Checkpoint slots a view with entry_capacity entries over n_tiles tiles
+ * needs (xg_splats.replay_slots): entry_capacity / XG_REPLAY_CHUNK + n_tiles + 1. */
+#define XG_REPLAY_CHUNK 256
+int64_t xg_replay_slots(int64_t entry_capacity, int32_t n_tiles_total);
 
 /* Scratch bytes needed by xg_bin_sort. */
 size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles_total);
@@ -195,6 +210,9 @@ xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, fl
 
 /* K4a: reverse replay.  Per-pixel upstream gradient is dl_dimage[H][W], or,
  * when dl_dimage == NULL, the fused L1 gradient l1_scale*sign(image-target).
+ * image (the forward's output) is also what the checkpointed replay
+ * (xg_splats.replay_ckpt) restarts each chunk from; without it, or without
+ * checkpoints, every quarter-tile is replayed whole from t_final.
  * Accumulates (atomically) into grad_acc[N][8]:
  *   {sum G dx, sum G dy, sum G dx^2, sum G dx dy, sum G dy^2, sum g w, sum G, 0}
  * over (pixel, entry) pairs, dx = px - mx, w = sigma T, g = dL/dI,

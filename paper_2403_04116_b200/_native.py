@@ -32,7 +32,10 @@ XG_ST_NONFINITE_FEAT = 0x4
 XG_ST_ENTRY_OVERFLOW = 0x8
 XG_ST_GRAD_SHIFT = 8
 XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
+XG_CTR_ITEMS = 6
 XG_NCOUNTERS = 8
+XG_ABI_VERSION = 2
+XG_REPLAY_CHUNK = 256
 XG_MAX_BATCH = 16
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
 
@@ -74,6 +77,9 @@ class XgSplats(ctypes.Structure):
         ("tile_order", c_void_p),
         ("unit_cost", c_void_p),
         ("unit_order", c_void_p),
+        ("replay_ckpt", c_void_p),
+        ("replay_items", c_void_p),
+        ("replay_slots", c_i64),
     ]
 
 
@@ -89,6 +95,7 @@ SIGNATURES = {
     "xg_tiles_x": (c_i32, [c_void_p]),
     "xg_tiles_y": (c_i32, [c_void_p]),
     "xg_bin_workspace_bytes": (c_size, [c_i64, c_i64, c_i32]),
+    "xg_replay_slots": (c_i64, [c_i64, c_i32]),
     "xg_preprocess_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "xg_bin_sort": (c_i32, [c_void_p, c_void_p, c_void_p, c_size, c_void_p]),
     "xg_composite_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -177,7 +184,7 @@ def load_library() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.xg_abi_version() != 1:
+    if lib.xg_abi_version() != XG_ABI_VERSION:
         raise NativeError("libxgauss ABI version mismatch")
     _lib = lib
     return lib

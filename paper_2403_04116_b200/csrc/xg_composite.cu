@@ -40,6 +40,10 @@ constexpr int kWarps = XG_COMPOSITE_WARPS;  // independent warps per CTA
 #endif
 constexpr int kFwdUnroll = XG_FWD_UNROLL;
 constexpr int kThreads = 32 * kWarps;
+// Replay checkpoints every kCk entries of a tile (xg_splats.replay_ckpt).
+constexpr int kCkShift = 8;
+constexpr int kCk = 1 << kCkShift;
+static_assert(kCk == XG_REPLAY_CHUNK && kCk % 32 == 0, "checkpoints sit on 32-entry batch boundaries");
 constexpr float kCullMargin = 0.05f;
 // kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
 // safety margin for the MUFU.EX2 error the clamp logic is compiled out.
@@ -168,7 +172,14 @@ struct FwdArgs {
   const uint32_t* n_entries;  // counters[XG_CTR_ENTRIES] (or null)
   long long cap;              // entry capacity: an overflowed view is skipped (re-binned by the caller)
   int ntx, w, h;
+  float2* ckpt;               // optional (tracking only): (T, acc) before every kCk-th entry
 };
+
+// Checkpoint slot of entry kCk * m of the tile whose list starts at `start`:
+// unique per (tile, m >= 1) and < entries / kCk + n_tiles + 1.
+__device__ __forceinline__ long long ckpt_slot(long long start, int tile, long long m) {
+  return (start >> kCkShift) + tile + m;
+}
 
 // Forward records in shared memory, signs folded so that every per-pixel
 // step of the lane's two pixels is ONE packed FP32x2 instruction (sm_100
@@ -325,6 +336,18 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int q
   Raw nxt = fetch(entry_at(a.entry, u.start + lane, u.end), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
   uint32_t g_nxt = entry_at(a.entry, u.start + 32 + lane, u.end);
   for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
+    if (kTrack && a.ckpt) {
+      // state before entry b0 for the chunked reverse replay; a warp that
+      // stopped early never reaches later boundaries, but then none of its
+      // pixels blends past them and the replay restarts from the final state
+      const long long rel = b0 - u.start;
+      if (rel > 0 && (rel & (kCk - 1)) == 0) {
+        float2* c = a.ckpt + 256 * ckpt_slot(u.start, tile, rel >> kCkShift);
+        const int pix = (u.py0 - u.y0) * kTile + (u.px - u.x0);
+        if (u.in0) c[pix] = make_float2(T.x, acc.x);
+        if (u.in1) c[pix + kTile] = make_float2(T.y, acc.y);
+      }
+    }
     const Raw cur = nxt;
     bool general;
     const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
@@ -585,6 +608,9 @@ struct BwdArgs {
   const uint32_t* n_entries;  // counters[XG_CTR_ENTRIES] (or null)
   long long cap;
   int ntx, w, h;
+  const float2* ckpt;         // chunked replay: the forward's checkpoints,
+  const uint2* items;         //   the chunk list (tile, sub << 24 | chunk)
+  const uint32_t* n_items;    //   and its length
 };
 
 // Backward records (shared memory), signs folded as in the forward:
@@ -638,25 +664,43 @@ __device__ __forceinline__ void unblend2(const BRec& r, float2 dy, float bdx, fl
   }
 }
 
-// Both pixels of the lane for one splat; the lane's 7 partial sums (negated:
-// the caller negates the warp totals, which is exact).
-template <bool kGeneral>
-__device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx, float2 fy, int last0, int last1,
-                                              float2 g, float2& T, float2& nS, float* v) {
+// The lane's 2 kP pixels (kP vertically adjacent pairs of one column,
+// sharing dx and the dx-only terms) for one splat; the lane's 7 partial sums
+// (negated: the caller negates the warp totals, which is exact).
+template <bool kGeneral, int kP>
+__device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx, const float2 (&fy)[kP],
+                                              const int (&last)[2 * kP], const float2 (&g)[kP], float2 (&T)[kP],
+                                              float2 (&nS)[kP], float* v) {
   const float dx = __fsub_rn(fx, r.a.x);
   const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
   const float bdx = __fmul_rn(r.a.w, dx);
-  const float2 dy = __fadd2_rn(fy, bc(r.a.y));
-  float2 nG, ngw;
-  unblend2<kGeneral>(r, dy, bdx, adx2, krel <= last0, krel <= last1, g, T, nS, nG, ngw);
-  const float2 Gdy = __fmul2_rn(nG, dy);
-  const float Gs = nG.x + nG.y, Gdys = Gdy.x + Gdy.y;
+  float2 sG, sGdy, sGdy2, sgw;
+#pragma unroll
+  for (int i = 0; i < kP; ++i) {
+    const float2 dy = __fadd2_rn(fy[i], bc(r.a.y));
+    float2 nG, ngw;
+    unblend2<kGeneral>(r, dy, bdx, adx2, krel <= last[2 * i], krel <= last[2 * i + 1], g[i], T[i], nS[i], nG,
+                       ngw);
+    const float2 Gdy = __fmul2_rn(nG, dy);
+    if (i == 0) {
+      sG = nG;
+      sGdy = Gdy;
+      sGdy2 = __fmul2_rn(Gdy, dy);
+      sgw = ngw;
+    } else {
+      sG = __fadd2_rn(sG, nG);
+      sGdy = __fadd2_rn(sGdy, Gdy);
+      sGdy2 = __ffma2_rn(Gdy, dy, sGdy2);
+      sgw = __fadd2_rn(sgw, ngw);
+    }
+  }
+  const float Gs = sG.x + sG.y, Gdys = sGdy.x + sGdy.y;
   v[0] = Gs * dx;
   v[1] = Gdys;
   v[2] = v[0] * dx;
   v[3] = Gdys * dx;
-  v[4] = fmaf(Gdy.x, dy.x, Gdy.y * dy.y);
-  v[5] = ngw.x + ngw.y;
+  v[4] = sGdy2.x + sGdy2.y;
+  v[5] = sgw.x + sgw.y;
   v[6] = Gs;
   v[7] = 0.f;
   return (Gs != 0.f) | (v[5] != 0.f);
@@ -734,19 +778,20 @@ __device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit&
 // xg_preprocess_bwd turns them into the reference's g_mean / g_conic /
 // g_int / g_alpha using the splat's own (A2, B2, C2, alpha).  Each warp
 // reduces its 64 pixels per splat and issues two vector reductions.
-template <bool kGeneral>
-__device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, const uint32_t* gid, int cnt,
-                                              const Unit& u, float2 fy, int last0, int last1, float2 g,
-                                              float2& T, float2& nS, float* grad_acc) {
+template <bool kGeneral, int kP>
+__device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, const uint32_t* gid, int cnt, float fx,
+                                              const float2 (&fy)[kP], const int (&last)[2 * kP],
+                                              const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP],
+                                              float* grad_acc) {
   const int lane = threadIdx.x & 31;
   // splats two at a time, back to front (A = q, then B = q - 1), their
   // records reduced together
   for (int q = cnt - 1; q >= 0; q -= 2) {
     const bool hasB = q >= 1;
     float v[16];
-    bool any = unblend_splat<kGeneral>(rec[q], kk[q], u.fx, fy, last0, last1, g, T, nS, v);
+    bool any = unblend_splat<kGeneral, kP>(rec[q], kk[q], fx, fy, last, g, T, nS, v);
     if (hasB) {
-      any |= unblend_splat<kGeneral>(rec[q - 1], kk[q - 1], u.fx, fy, last0, last1, g, T, nS, v + 8);
+      any |= unblend_splat<kGeneral, kP>(rec[q - 1], kk[q - 1], fx, fy, last, g, T, nS, v + 8);
     } else {
 #pragma unroll
       for (int i = 8; i < 16; ++i) v[i] = 0.f;
@@ -765,49 +810,136 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
   }
 }
 
-// One (tile, quarter) unit of the reverse replay.
-__device__ __forceinline__ void bwd_unit(const BwdArgs& a, int tile, int quad, BRec* rec, int* kk, uint32_t* gid) {
+// Upstream gradient of pixel o (dL/dI, or the fused L1 sign term).
+__device__ __forceinline__ float upstream(const BwdArgs& a, long long o) {
+  return a.dl ? a.dl[o] : a.l1_scale * (float)((a.image[o] > a.target[o]) - (a.image[o] < a.target[o]));
+}
+
+// Walk entries [e_lo, e_hi) of the tile starting at `start` back to front in
+// batches of 32 ([b1 - 32, b1)), with the two-stage prefetch (entry indices
+// one batch ahead of the records).
+template <int kP>
+__device__ __forceinline__ void replay_range(const BwdArgs& a, const Unit& u, long long start, long long e_lo,
+                                             long long e_hi, const float2 (&fy)[kP], const int (&last)[2 * kP],
+                                             const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP], BRec* rec,
+                                             int* kk, uint32_t* gid) {
   const int lane = threadIdx.x & 31;
-  const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
-  const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
-  float2 T = make_float2(0.f, 0.f), g = make_float2(0.f, 0.f);
-  int last0 = -1, last1 = -1;
-  if (u.in0) {
-    T.x = a.t_final[o0];
-    last0 = a.n_contrib[o0] - 1;
-    g.x = a.dl ? a.dl[o0] : a.l1_scale * (float)((a.image[o0] > a.target[o0]) - (a.image[o0] < a.target[o0]));
-  }
-  if (u.in1) {
-    T.y = a.t_final[o1];
-    last1 = a.n_contrib[o1] - 1;
-    g.y = a.dl ? a.dl[o1] : a.l1_scale * (float)((a.image[o1] > a.target[o1]) - (a.image[o1] < a.target[o1]));
-  }
-  if (g.x == 0.f) last0 = -1;  // zero upstream contributes nothing: skip the replay
-  if (g.y == 0.f) last1 = -1;
-  int wl = max(last0, last1);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
-  const long long hi = u.start + wl + 1;  // one past the last entry this warp needs
-  const float2 fy = make_float2(u.fy0, u.fy1);
-  float2 nS = make_float2(0.f, 0.f);
-  // batches of 32 walked back to front: [b1 - 32, b1); two-stage prefetch
-  // (entry indices one batch ahead of the records)
-  Raw nxt = fetch(hi - 32 + lane >= u.start ? entry_at(a.entry, hi - 32 + lane, hi) : 0u,
-                  hi - 32 + lane >= u.start && hi - 32 + lane < hi, a.mean2d, a.coef, a.inten);
-  uint32_t g_nxt = hi - 64 + lane >= u.start ? entry_at(a.entry, hi - 64 + lane, hi) : 0u;
-  for (long long b1 = hi; b1 > u.start; b1 -= 32) {
+  Raw nxt = fetch(e_hi - 32 + lane >= e_lo ? entry_at(a.entry, e_hi - 32 + lane, e_hi) : 0u,
+                  e_hi - 32 + lane >= e_lo, a.mean2d, a.coef, a.inten);
+  uint32_t g_nxt = e_hi - 64 + lane >= e_lo ? entry_at(a.entry, e_hi - 64 + lane, e_hi) : 0u;
+  for (long long b1 = e_hi; b1 > e_lo; b1 -= 32) {
     const Raw cur = nxt;
     bool general;
-    const int cnt = compact_bwd(cur, (int)(b1 - 32 - u.start) + lane, u, rec, kk, gid, general);
+    const int cnt = compact_bwd(cur, (int)(b1 - 32 - start) + lane, u, rec, kk, gid, general);
     const long long kn = b1 - 64 + lane;
-    nxt = fetch(g_nxt, kn >= u.start, a.mean2d, a.coef, a.inten);
-    g_nxt = kn - 32 >= u.start ? entry_at(a.entry, kn - 32, hi) : 0u;
+    nxt = fetch(g_nxt, kn >= e_lo, a.mean2d, a.coef, a.inten);
+    g_nxt = kn - 32 >= e_lo ? entry_at(a.entry, kn - 32, e_hi) : 0u;
     if (general)
-      unblend_batch<true>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
+      unblend_batch<true, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
     else
-      unblend_batch<false>(rec, kk, gid, cnt, u, fy, last0, last1, g, T, nS, a.grad_acc);
+      unblend_batch<false, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
     __syncwarp();
   }
+}
+
+// One (tile, quarter) unit of the reverse replay, whole, from the final state.
+__device__ __forceinline__ void bwd_unit(const BwdArgs& a, int tile, int quad, BRec* rec, int* kk, uint32_t* gid) {
+  const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
+  const long long o0 = (long long)u.py0 * a.w + u.px, o1 = o0 + a.w;
+  float2 T[1] = {make_float2(0.f, 0.f)}, g[1] = {make_float2(0.f, 0.f)}, nS[1] = {make_float2(0.f, 0.f)};
+  int last[2] = {-1, -1};
+  if (u.in0) {
+    T[0].x = a.t_final[o0];
+    last[0] = a.n_contrib[o0] - 1;
+    g[0].x = upstream(a, o0);
+  }
+  if (u.in1) {
+    T[0].y = a.t_final[o1];
+    last[1] = a.n_contrib[o1] - 1;
+    g[0].y = upstream(a, o1);
+  }
+  if (g[0].x == 0.f) last[0] = -1;  // zero upstream contributes nothing: skip the replay
+  if (g[0].y == 0.f) last[1] = -1;
+  int wl = max(last[0], last[1]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+  const float2 fy[1] = {make_float2(u.fy0, u.fy1)};
+  replay_range<1>(a, u, u.start, u.start, u.start + wl + 1, fy, last, g, T, nS, rec, kk, gid);
+}
+
+// One chunk of the checkpointed replay: entries [kCk j, kCk (j + 1)) of a
+// 16-wide, 4 kP-row sub-block of the tile (2 kP pixels per lane: column
+// lane & 15, rows 2 kP (lane >> 4) + 0 .. 2 kP - 1), restarted from the
+// forward's checkpoint before entry kCk (j + 1) - or, for a pixel whose last
+// blended entry precedes it, from its final state, which is the same state.
+// The suffix sum restarts as acc_K - image (S = image - acc_K).
+template <int kP>
+__device__ __forceinline__ void bwd_chunk(const BwdArgs& a, uint2 item, BRec* rec, int* kk, uint32_t* gid) {
+  constexpr int kR = 2 * kP, kRows = 2 * kR;
+  const int lane = threadIdx.x & 31;
+  const int tile = (int)item.x, sub = (int)(item.y >> 24), j = (int)(item.y & 0xffffffu);
+  Unit u;
+  u.x0 = (tile % a.ntx) * kTile;
+  u.y0 = (tile / a.ntx) * kTile;
+  const int lx = lane & 15, ly = sub * kRows + (lane >> 4) * kR;
+  u.px = u.x0 + lx;
+  u.fx = (float)lx;
+  u.xa = 0.f;
+  u.xb = (float)(kTile - 1);
+  u.ya = (float)(sub * kRows);
+  u.yb = (float)(sub * kRows + kRows - 1);
+  const long long start = a.ranges[2 * tile];
+  float2 T[kP], g[kP], nS[kP], fy[kP];
+  int last[kR];
+#pragma unroll
+  for (int i = 0; i < kP; ++i) {
+    fy[i] = make_float2((float)(ly + 2 * i), (float)(ly + 2 * i + 1));
+    nS[i] = make_float2(0.f, 0.f);
+  }
+  int wl = -1;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int py = u.y0 + ly + r;
+    const long long o = (long long)py * a.w + u.px;
+    float t = 0.f, gg = 0.f;
+    int l = -1;
+    if (u.px < a.w && py < a.h) {
+      t = a.t_final[o];
+      l = a.n_contrib[o] - 1;
+      gg = upstream(a, o);
+    }
+    if (gg == 0.f) l = -1;
+    if (r & 1) {
+      T[r >> 1].y = t;
+      g[r >> 1].y = gg;
+    } else {
+      T[r >> 1].x = t;
+      g[r >> 1].x = gg;
+    }
+    last[r] = l;
+    wl = max(wl, l);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
+  const int lo = j << kCkShift, K = lo + kCk;
+  const int hi = min(K, wl + 1);
+  if (hi <= lo) return;
+  const float2* ck = a.ckpt + 256 * ckpt_slot(start, tile, j + 1);
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    if (K <= last[r]) {
+      const float2 c = ck[(ly + r) * kTile + lx];
+      const float s = c.y - a.image[(long long)(u.y0 + ly + r) * a.w + u.px];
+      if (r & 1) {
+        T[r >> 1].y = c.x;
+        nS[r >> 1].y = s;
+      } else {
+        T[r >> 1].x = c.x;
+        nS[r >> 1].x = s;
+      }
+    }
+  }
+  replay_range<kP>(a, u, start, start + lo, start + hi, fy, last, g, T, nS, rec, kk, gid);
 }
 
 // (no min-blocks bound: ptxas then settles at 92 registers = 5 CTAs per SM,
@@ -841,6 +973,83 @@ __global__ void __launch_bounds__(32) k_composite_bwd_np(BwdArgs a) {
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
   const int uidx = a.unit_order ? a.order[blockIdx.x] : 4 * a.order[blockIdx.x >> 2] + (int)(blockIdx.x & 3);
   bwd_unit(a, uidx >> 2, uidx & 3, s_rec, s_k, s_gid);
+}
+
+// Checkpointed replay: persistent warps over the chunk list (heaviest tiles
+// first); the first wave is dealt by warp index, the rest pulled from the
+// queue.  kBwdPairs pixel pairs per lane: a warp covers 16 x 4 kBwdPairs
+// pixels, so the per-splat warp reduction is shared by 4 kBwdPairs pixels.
+#ifndef XG_BWD_PAIRS
+#define XG_BWD_PAIRS 4
+#endif
+constexpr int kBwdPairs = XG_BWD_PAIRS;
+static_assert(kBwdPairs == 1 || kBwdPairs == 2 || kBwdPairs == 4, "a sub-block is 4, 8 or 16 rows");
+constexpr int kBwdSubs = 4 / kBwdPairs;  // sub-blocks per tile
+
+__global__ void __launch_bounds__(kThreads) k_composite_bwd_ck(BwdArgs a) {
+  __shared__ BRec s_rec[kWarps][32];
+  __shared__ int s_k[kWarps][32];
+  __shared__ uint32_t s_gid[kWarps][32];
+  const int warp = threadIdx.x >> 5;
+  if (a.n_entries && (long long)*a.n_entries > a.cap) return;
+  const uint32_t n = *a.n_items, dealt = gridDim.x * kWarps;
+  uint32_t k = blockIdx.x * kWarps + warp;
+  while (k < n) {
+    bwd_chunk<kBwdPairs>(a, a.items[k], s_rec[warp], s_k[warp], s_gid[warp]);
+    uint32_t d = 0;
+    if ((threadIdx.x & 31) == 0) d = atomicAdd(a.work, 1u);
+    k = dealt + __shfl_sync(0xffffffffu, d, 0);
+  }
+}
+
+// Chunk list of the checkpointed replay, one CTA: per tile (heaviest first,
+// tile_order) and sub-block, ceil(L / kCk) chunks, L = the longest replay of
+// the quarter tiles it overlaps (unit_cost, from the forward).
+__global__ void __launch_bounds__(1024) k_replay_items(const int* __restrict__ cost, const int* __restrict__ order,
+                                                       int n_tiles, uint2* __restrict__ items, long long cap,
+                                                       uint32_t* __restrict__ n_items) {
+  __shared__ uint32_t warp_tot[32];
+  constexpr int kRows = 16 / kBwdSubs;
+  auto chunks = [&](int t, int sub) {
+    int L = 0;
+    for (int rh = (sub * kRows) >> 3; rh <= (sub * kRows + kRows - 1) >> 3; ++rh)
+      L = max(L, max(cost[4 * t + 2 * rh], cost[4 * t + 2 * rh + 1]));
+    return (uint32_t)((L + kCk - 1) >> kCkShift);
+  };
+  const int per = (n_tiles + 1023) >> 10;
+  const int i0 = min((int)threadIdx.x * per, n_tiles), i1 = min(i0 + per, n_tiles);
+  uint32_t cnt = 0;
+  for (int i = i0; i < i1; ++i)
+    for (int sub = 0; sub < kBwdSubs; ++sub) cnt += chunks(order[i], sub);
+  // block-wide exclusive scan of cnt
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_tot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = warp_tot[lane], ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    warp_tot[lane] = ti - t;
+  }
+  __syncthreads();
+  long long off = (long long)warp_tot[w] + inc - cnt;
+  for (int i = i0; i < i1; ++i) {
+    const int t = order[i];
+    for (int sub = 0; sub < kBwdSubs; ++sub) {
+      const uint32_t nc = chunks(t, sub);
+      for (uint32_t j = 0; j < nc && off < cap; ++j, ++off) items[off] = make_uint2((uint32_t)t, ((uint32_t)sub << 24) | j);
+    }
+  }
+  if (threadIdx.x == blockDim.x - 1) *n_items = (uint32_t)min(off, cap);
 }
 
 // ---------------------------------------------------------------------------
@@ -972,7 +1181,8 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
             (const long long*)sp->tile_ranges, sp->tile_order, work, n_tiles, image, t_final, n_contrib,
             target, l1_sum, (t_final && n_contrib) ? sp->unit_cost : nullptr,
             sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
-            tiles_x(*cam), cam->width, cam->height};
+            tiles_x(*cam), cam->width, cam->height,
+            (t_final && n_contrib) ? (float2*)sp->replay_ckpt : nullptr};
   // grid: one CTA per tile dispatched heaviest first (non-persistent) vs the
   // persistent queue - measured: non-persistent 3 % faster for the tracked
   // (training) forward at C2, persistent 5 % faster image-only at C3;
@@ -1068,6 +1278,29 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
   uint32_t* work = sp->counters + XG_CTR_QUEUE;
   cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
+  // chunked replay from the forward's checkpoints (XG_BWD_CKPT=0: whole
+  // quarter tiles, the path of frames without checkpoints)
+  static const bool ck_env = !(getenv("XG_BWD_CKPT") && atoi(getenv("XG_BWD_CKPT")) == 0);
+  if (ck_env && sp->replay_ckpt && sp->replay_items && sp->unit_cost && image) {
+    if (sp->replay_slots < xg_replay_slots(sp->entry_capacity, n_tiles)) {
+      set_error_msg("xg_composite_bwd: replay_slots < xg_replay_slots(entry_capacity, n_tiles)");
+      return XG_ERR_INVALID;
+    }
+    uint32_t* n_items = sp->counters + XG_CTR_ITEMS;
+    uint2* items = (uint2*)sp->replay_items;
+    k_replay_items<<<1, 1024, 0, (cudaStream_t)stream>>>(sp->unit_cost, sp->tile_order, n_tiles, items,
+                                                           4 * (long long)sp->replay_slots, n_items);
+    xg_status st = check_launch("k_replay_items");
+    if (st != XG_OK) return st;
+    BwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+              (const long long*)sp->tile_ranges, nullptr, work, n_tiles, false, t_final, n_contrib, dl_dimage,
+              image, target, l1_scale, grad_acc,
+              sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
+              tiles_x(*cam), cam->width, cam->height, (const float2*)sp->replay_ckpt, items, n_items};
+    k_composite_bwd_ck<<<persistent_grid(k_composite_bwd_ck, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0,
+                         (cudaStream_t)stream>>>(a);
+    return check_launch("k_composite_bwd_ck");
+  }
   // schedule the reverse replay by the per-unit cost the forward recorded
   const bool by_unit = sp->unit_cost && sp->unit_order;
   if (by_unit) {
@@ -1087,6 +1320,10 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   }
   k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
+}
+
+int64_t xg_replay_slots(int64_t entry_capacity, int32_t n_tiles_total) {
+  return (entry_capacity > 0 ? entry_capacity : 0) / kCk + (n_tiles_total > 0 ? n_tiles_total : 0) + 1;
 }
 
 size_t xg_tiles_workspace_bytes(int64_t n_splats, int32_t h, int32_t w) {

@@ -53,6 +53,7 @@ class Frame:
         self.unit_order = torch.empty(4 * self.n_tiles, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(nat.XG_NCOUNTERS, dtype=torch.int32, device=dev)
         self.image = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.fwd_image = self.image
         self.t_final = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
         self.extras = None
@@ -68,6 +69,8 @@ class Frame:
         self.entry_capacity = 0
         self.entry_splat = None
         self.workspace = None
+        self.replay_ckpt = None  # training frames only: allocated by the first tracking composite
+        self.replay_items = None
         self.set_capacity(entry_capacity if entry_capacity else max(16 * n, 1024))
         self.cam = None
         self.has_forward = False
@@ -80,6 +83,16 @@ class Frame:
         self.entry_splat = torch.empty(cap, dtype=torch.int32, device=self.device)
         ws = nat.lib().xg_bin_workspace_bytes(self.n, cap, self.n_tiles)
         self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
+        if self.replay_ckpt is not None:
+            self._alloc_replay()
+
+    def _alloc_replay(self) -> None:
+        """Checkpoints of the chunked reverse replay: (T, acc) of every pixel
+        before each XG_REPLAY_CHUNK-th entry of its tile, plus the chunk list
+        (include/xgauss.h, xg_splats.replay_ckpt)."""
+        slots = int(nat.lib().xg_replay_slots(self.entry_capacity, self.n_tiles))
+        self.replay_ckpt = torch.empty((slots, 256, 2), dtype=torch.float32, device=self.device)
+        self.replay_items = torch.empty((4 * slots, 2), dtype=torch.int32, device=self.device)
 
     def splats_struct(self) -> nat.XgSplats:
         s = nat.XgSplats()
@@ -98,6 +111,10 @@ class Frame:
         s.tile_order = self.tile_order.data_ptr()
         s.unit_cost = self.unit_cost.data_ptr()
         s.unit_order = self.unit_order.data_ptr()
+        if self.replay_ckpt is not None:
+            s.replay_ckpt = self.replay_ckpt.data_ptr()
+            s.replay_items = self.replay_items.data_ptr()
+            s.replay_slots = self.replay_ckpt.shape[0]
         return s
 
     # --- stages -------------------------------------------------------------
@@ -142,6 +159,8 @@ class Frame:
         instead of the frame's own buffer (e.g. a slot of a sweep stack).
         ``track=False`` (inference) skips the per-pixel final transmittance
         and contributor counts the backward needs."""
+        if track and self.replay_ckpt is None:
+            self._alloc_replay()
         sp = self.splats_struct()
         img = self.image if image_out is None else image_out
         nat.check(
@@ -153,6 +172,7 @@ class Frame:
             "xg_composite_fwd",
         )
         self.has_forward = track
+        self.fwd_image = img  # the image the backward (fused L1, replay restarts) reads
 
     def read_counters(self) -> tuple[int, int, int]:
         c = self.counters.cpu().numpy().astype("int64") & 0xFFFFFFFF
@@ -182,8 +202,7 @@ class Frame:
         nat.check(
             nat.lib().xg_composite_bwd(
                 ctypes.byref(self.cam), ctypes.byref(sp), self.t_final.data_ptr(),
-                self.n_contrib.data_ptr(), nat.ptr(dl_dimage, "dl_dimage"),
-                self.image.data_ptr() if dl_dimage is None else None,
+                self.n_contrib.data_ptr(), nat.ptr(dl_dimage, "dl_dimage"), self.fwd_image.data_ptr(),
                 nat.ptr(target, "target") if dl_dimage is None else None,
                 ctypes.c_float(l1_scale), grad_acc.data_ptr(), nat.stream(),
             ),

@@ -169,7 +169,9 @@ int32_t xg_tiles_y(const xg_camera* cam);
 
 /* Checkpoint slots a view with entry_capacity entries over n_tiles tiles
  * needs (xg_splats.replay_slots): entry_capacity / XG_REPLAY_CHUNK + n_tiles + 1. */
-#define XG_REPLAY_CHUNK 256
+#ifndef XG_REPLAY_CHUNK
+#define XG_REPLAY_CHUNK 256 /* (a power of two >= 32; tuning builds may override) */
+#endif
 int64_t xg_replay_slots(int64_t entry_capacity, int32_t n_tiles_total);
 
 /* Scratch bytes needed by xg_bin_sort. */

@@ -41,7 +41,8 @@ constexpr int kWarps = XG_COMPOSITE_WARPS;  // independent warps per CTA
 constexpr int kFwdUnroll = XG_FWD_UNROLL;
 constexpr int kThreads = 32 * kWarps;
 // Replay checkpoints every kCk entries of a tile (xg_splats.replay_ckpt).
-constexpr int kCkShift = 8;
+constexpr int log2_exact(int x) { return x <= 1 ? 0 : 1 + log2_exact(x >> 1); }
+constexpr int kCkShift = log2_exact(XG_REPLAY_CHUNK);
 constexpr int kCk = 1 << kCkShift;
 static_assert(kCk == XG_REPLAY_CHUNK && kCk % 32 == 0, "checkpoints sit on 32-entry batch boundaries");
 constexpr float kCullMargin = 0.05f;

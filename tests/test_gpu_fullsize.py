@@ -292,3 +292,53 @@ def test_sweep_with_empty_views(xg):
             else:
                 assert float(out[i].abs().max()) > 0.0
     assert 0 < empty < 2 * len(angles)
+
+
+def test_chunked_replay_mixed_termination(xg):
+    """The chunked reverse replay (xg_splats.replay_ckpt: every tile's list
+    replayed in independent 256-entry chunks restarted from the forward's
+    checkpoints) on tiles thousands of entries long where opacity grows
+    across the image: pixels on one side stop (T < 1e-4) within the first
+    chunks, on the other side run through every chunk - so chunks restart
+    both from checkpoints and from final states, inside one warp.  Kernel
+    gradients normwise 1e-4 against the float64 oracle."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    n = 4000
+    pos = rng.uniform(-30, 30, size=(n, 3))
+    alpha = 0.002 + 0.9 * (pos[:, 1] + 30) / 60  # grows along world y
+    f = {k: np.asarray(v, np.float32) for k, v in {
+        "positions": pos, "rotations": np.tile([1.0, 0, 0, 0], (n, 1)),
+        "log_scales": np.log(rng.uniform(2.0, 5.0, size=(n, 3))),
+        "raw_opacities": np.log(alpha) - np.log1p(-alpha),
+        "features": rng.normal(scale=0.5, size=(n, 4))}.items()}
+    basis = np.ones(4, np.float32)
+    cloud = xg.GaussianCloud(**f, basis_weights=basis, device="cuda")
+    d, phi = 96, 0.0
+    sc = xg.ScannerConfig(L_SO, L_SD, d, d, 2.0)
+    proj, sp = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (d, d))
+    torch.cuda.synchronize()
+    cam = orc.camera_from_view(L_SO, L_SD, d, d, 2.0, phi)
+    pre = orc.preprocess(f, basis, cam)
+    binned = orc.bin_entries(pre, cam)
+    fwd = orc.composite_fwd(pre, binned, d, d)
+    lens = binned["tile_ranges"][:, 1] - binned["tile_ranges"][:, 0]
+    assert lens.max() > 8 * 256, int(lens.max())
+    stopped = fwd["t_final"] < 1e-4
+    assert 0.1 < stopped.mean() < 0.9, float(stopped.mean())
+    nc = fwd["n_contrib"]
+    assert (nc[stopped] < 256).any() and (nc[~stopped] > 4 * 256).any()
+    _check_forward("chunked", proj, sp, pre, binned, fwd)
+    assert sp.frame.replay_ckpt is not None
+    dl = rng.normal(size=(d, d)) / (d * d)
+    kg = {k: torch.zeros(s, dtype=torch.float64, device="cuda")
+          for k, s in (("g_mean", (n, 2)), ("g_conic", (n, 3)), ("g_int", n), ("g_alpha", n))}
+    xg.render_backward(cloud, sp, torch.as_tensor(dl), kernel_grads=kg)
+    torch.cuda.synchronize()
+    want = orc.composite_bwd(pre, binned, d, d, dl)
+    act = np.flatnonzero(pre["active"])
+    floor = 1e-3 * max(np.abs(v[act]).max() for v in want.values())
+    for k, ref in want.items():
+        ok, rel = normwise_ok(kg[k].cpu().numpy()[act], ref[act], floor)
+        assert ok, (k, rel)

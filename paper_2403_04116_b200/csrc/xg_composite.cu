@@ -41,7 +41,7 @@ constexpr int kWarps = XG_COMPOSITE_WARPS;  // independent warps per CTA
 constexpr int kFwdUnroll = XG_FWD_UNROLL;
 constexpr int kThreads = 32 * kWarps;
 // Replay checkpoints every kCk entries of a tile (xg_splats.replay_ckpt).
-constexpr int log2_exact(int x) { return x <= 1 ? 0 : 1 + log2_exact(x >> 1); }
+__host__ __device__ constexpr int log2_exact(int x) { return x <= 1 ? 0 : 1 + log2_exact(x >> 1); }
 constexpr int kCkShift = log2_exact(XG_REPLAY_CHUNK);
 constexpr int kCk = 1 << kCkShift;
 static_assert(kCk == XG_REPLAY_CHUNK && kCk % 32 == 0, "checkpoints sit on 32-entry batch boundaries");
@@ -119,6 +119,37 @@ __device__ __forceinline__ Unit make_unit(int tile, int quad, int ntx, int w, in
   return u;
 }
 
+// Sub-block `sub` of a tile for a warp whose lanes own 2 kP pixels each:
+// kP = 1 the 8x8 quarter above; kP = 2, 4 a 16-wide block of 4 kP rows,
+// lane = column lane & 15, rows py0 + 0 .. 2 kP - 1 (py0 = 2 kP (lane >> 4)
+// into the block) - the per-splat shared work (record loads, dx terms,
+// the warp reduction of the replay) then serves 4 kP pixels per warp lane
+// pair instead of 2.
+template <int kP>
+__device__ __forceinline__ Unit make_sub(int tile, int sub, int ntx, int w, int h, const long long* ranges) {
+  if (kP == 1) return make_unit(tile, sub, ntx, w, h, ranges);
+  constexpr int kR = 2 * kP, kRows = 2 * kR;
+  Unit u;
+  u.x0 = (tile % ntx) * kTile;
+  u.y0 = (tile / ntx) * kTile;
+  const int lane = threadIdx.x & 31;
+  const int lx = lane & 15, ly = sub * kRows + (lane >> 4) * kR;
+  u.px = u.x0 + lx;
+  u.py0 = u.y0 + ly;
+  u.fx = (float)lx;
+  u.fy0 = (float)ly;
+  u.fy1 = (float)(ly + 1);
+  u.xa = 0.f;
+  u.xb = (float)(kTile - 1);
+  u.ya = (float)(sub * kRows);
+  u.yb = (float)(sub * kRows + kRows - 1);
+  u.in0 = u.px < w && u.py0 < h;
+  u.in1 = u.px < w && u.py0 + 1 < h;
+  u.start = ranges[2 * tile];
+  u.end = ranges[2 * tile + 1];
+  return u;
+}
+
 // Next (tile, quarter) unit for this warp.  Units are the heaviest-first
 // tile order x 4 quarters.  The first wave is dealt statically: warp w of
 // CTA c takes unit G*w + c (w even) or G*w + G-1-c (w odd), so every CTA -
@@ -127,10 +158,10 @@ __device__ __forceinline__ Unit make_unit(int tile, int quad, int ntx, int w, in
 // order).  After that, warps pull the remaining (lightest) units from the
 // counter.
 // order: tiles (4 units each, kUnits = false) or units (kUnits = true).
-template <bool kUnits>
+template <bool kUnits, int kSubs = 4>
 __device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int n_tiles, bool& first,
                                           int& tile, int& quad) {
-  const uint32_t n_units = 4u * (uint32_t)n_tiles;
+  const uint32_t n_units = (uint32_t)kSubs * (uint32_t)n_tiles;
   const uint32_t G = gridDim.x, w = threadIdx.x >> 5;
   const uint32_t dealt = min(n_units, G * (uint32_t)kWarps);
   uint32_t k = n_units;
@@ -149,8 +180,8 @@ __device__ __forceinline__ bool next_unit(const int* order, uint32_t* work, int 
     tile = uidx >> 2;
     quad = uidx & 3;
   } else {
-    tile = order[k >> 2];
-    quad = (int)(k & 3u);
+    tile = order[k / kSubs];
+    quad = (int)(k % kSubs);
   }
   return true;
 }
@@ -224,17 +255,14 @@ __device__ __forceinline__ float select_ok(float sg, float p2, float T) {
   return r;
 }
 
-// One splat, the lane's two pixels: the blend step of _kernels.pyx:57-72.
-// kGeneral keeps the sigma <= 0.99 clamp (only alpha >= 0.99 can reach it)
-// and the p2 <= 0 test (only ill-conditioned splats can need it); both are
-// warp-uniform per batch.  Records the last blended entry (n_contrib).
+// One splat, one vertically adjacent pixel pair of the lane: the blend step
+// of _kernels.pyx:57-72.  kGeneral keeps the sigma <= 0.99 clamp (only
+// alpha >= 0.99 can reach it) and the p2 <= 0 test (only ill-conditioned
+// splats can need it); both are warp-uniform per batch.  Records the last
+// blended entry (n_contrib).
 template <bool kGeneral, bool kTrack>
-__device__ __forceinline__ void blend2(const FRec& r, int krel, float fx, float2 fy, float2& T, float2& acc,
-                                       int& last0, int& last1) {
-  const float dx = __fsub_rn(fx, r.a.x);
-  const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
-  const float bdx = __fmul_rn(r.a.w, dx);
-  const float2 dy = __fadd2_rn(fy, bc(r.a.y));
+__device__ __forceinline__ void blend_pair(const FRec& r, int krel, float2 dy, float bdx, float adx2, float2& T,
+                                           float2& acc, int& last0, int& last1) {
   const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
   float2 sg = __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
   if (kGeneral) {
@@ -263,6 +291,20 @@ __device__ __forceinline__ void blend2(const FRec& r, int krel, float fx, float2
     last0 = ok0 ? krel : last0;
     last1 = ok1 ? krel : last1;
   }
+}
+
+// One splat, the lane's kP pixel pairs (one column: dx and the dx-only
+// terms computed once).
+template <bool kGeneral, bool kTrack, int kP>
+__device__ __forceinline__ void blend_splat(const FRec& r, int krel, float fx, const float2 (&fy)[kP],
+                                            float2 (&T)[kP], float2 (&acc)[kP], int (&last)[2 * kP]) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+  const float bdx = __fmul_rn(r.a.w, dx);
+#pragma unroll
+  for (int i = 0; i < kP; ++i)
+    blend_pair<kGeneral, kTrack>(r, krel, __fadd2_rn(fy[i], bc(r.a.y)), bdx, adx2, T[i], acc[i], last[2 * i],
+                                 last[2 * i + 1]);
 }
 
 // Record half of the gather (the entry index is loaded one batch earlier).
@@ -309,11 +351,11 @@ __device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit&
   return __popc(bal);
 }
 
-template <bool kGeneral, bool kTrack>
-__device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, float2 fy,
-                                            float2& T, float2& acc, int& last0, int& last1) {
+template <bool kGeneral, bool kTrack, int kP>
+__device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, const float2 (&fy)[kP],
+                                            float2 (&T)[kP], float2 (&acc)[kP], int (&last)[2 * kP]) {
 #pragma unroll kFwdUnroll
-  for (int q = 0; q < cnt; ++q) blend2<kGeneral, kTrack>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last0, last1);
+  for (int q = 0; q < cnt; ++q) blend_splat<kGeneral, kTrack, kP>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last);
 }
 
 // 5 CTAs (20 warps) per SM: ptxas fits the image-only variant in 96
@@ -321,18 +363,44 @@ __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int 
 #ifndef XG_FWD_MIN_CTAS
 #define XG_FWD_MIN_CTAS 5
 #endif
-
-// One (tile, quarter) unit of the forward: the warp walks the tile's entry
-// list and writes the unit's 64 pixels.
+// pixel pairs per lane (make_sub): image-only launches / tracking launches
+#ifndef XG_FWD_PAIRS
+#define XG_FWD_PAIRS 2  // measured at C3: 1 -> 2 pairs +5 % fps, 4 pairs -6 %
+#endif
+#ifndef XG_FWD_TRACK_PAIRS
+#define XG_FWD_TRACK_PAIRS 1  // (C2 training: quarter tiles balance better; 2 pairs +5 % per iteration)
+#endif
+#ifndef XG_FWD_MIN_CTAS_WIDE
+#define XG_FWD_MIN_CTAS_WIDE 4
+#endif
+constexpr int kFwdPairs = XG_FWD_PAIRS, kFwdTrackPairs = XG_FWD_TRACK_PAIRS;
+static_assert((kFwdPairs == 1 || kFwdPairs == 2 || kFwdPairs == 4) &&
+                  (kFwdTrackPairs == 1 || kFwdTrackPairs == 2 || kFwdTrackPairs == 4) && kWarps % 4 == 0,
+              "sub-blocks of 4, 8 or 16 rows; CTAs of whole tiles");
 template <bool kTrack>
-__device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int quad, FRec* rec, int* kk) {
+__host__ __device__ constexpr int fwd_pairs() { return kTrack ? kFwdTrackPairs : kFwdPairs; }
+__host__ __device__ constexpr int min_ctas(int kP) { return kP == 1 ? XG_FWD_MIN_CTAS : XG_FWD_MIN_CTAS_WIDE; }
+
+// One sub-block unit of the forward: the warp walks the tile's entry list
+// and writes the sub-block's pixels.
+template <bool kTrack, int kP>
+__device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int sub, FRec* rec, int* kk) {
+  constexpr int kR = 2 * kP;
   const int lane = threadIdx.x & 31;
-  const Unit u = make_unit(tile, quad, a.ntx, a.w, a.h, a.ranges);
-  const float2 fy = make_float2(u.fy0, u.fy1);
-  float2 T = make_float2(u.in0 ? 1.f : 0.f, u.in1 ? 1.f : 0.f);
-  float2 acc = make_float2(0.f, 0.f);
-  int last0 = -1, last1 = -1;
-  bool alive = __any_sync(0xffffffffu, u.in0 || u.in1);
+  const Unit u = make_sub<kP>(tile, sub, a.ntx, a.w, a.h, a.ranges);
+  float2 fy[kP], T[kP], acc[kP];
+  int last[kR];
+  bool any_in = false;
+#pragma unroll
+  for (int i = 0; i < kP; ++i) {
+    fy[i] = make_float2(u.fy0 + (float)(2 * i), u.fy0 + (float)(2 * i + 1));
+    const bool in0 = u.px < a.w && u.py0 + 2 * i < a.h, in1 = u.px < a.w && u.py0 + 2 * i + 1 < a.h;
+    T[i] = make_float2(in0 ? 1.f : 0.f, in1 ? 1.f : 0.f);
+    acc[i] = make_float2(0.f, 0.f);
+    last[2 * i] = last[2 * i + 1] = -1;
+    any_in |= in0 | in1;
+  }
+  bool alive = __any_sync(0xffffffffu, any_in);
   // two-stage prefetch: entry indices one batch ahead of the records
   Raw nxt = fetch(entry_at(a.entry, u.start + lane, u.end), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
   uint32_t g_nxt = entry_at(a.entry, u.start + 32 + lane, u.end);
@@ -343,10 +411,12 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int q
       // pixels blends past them and the replay restarts from the final state
       const long long rel = b0 - u.start;
       if (rel > 0 && (rel & (kCk - 1)) == 0) {
-        float2* c = a.ckpt + 256 * ckpt_slot(u.start, tile, rel >> kCkShift);
-        const int pix = (u.py0 - u.y0) * kTile + (u.px - u.x0);
-        if (u.in0) c[pix] = make_float2(T.x, acc.x);
-        if (u.in1) c[pix + kTile] = make_float2(T.y, acc.y);
+        float2* c = a.ckpt + 256 * ckpt_slot(u.start, tile, rel >> kCkShift) + (u.py0 - u.y0) * kTile +
+                    (u.px - u.x0);
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+          if (u.px < a.w && u.py0 + r < a.h)
+            c[r * kTile] = (r & 1) ? make_float2(T[r >> 1].y, acc[r >> 1].y) : make_float2(T[r >> 1].x, acc[r >> 1].x);
       }
     }
     const Raw cur = nxt;
@@ -355,31 +425,30 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int q
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
     if (general)  // warp-uniform, per batch of 32 entries
-      blend_batch<true, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
+      blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
     else
-      blend_batch<false, kTrack>(rec, kk, cnt, u.fx, fy, T, acc, last0, last1);
+      blend_batch<false, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
     __syncwarp();
-    alive = __any_sync(0xffffffffu, (T.x >= kFloor) || (T.y >= kFloor));
+    bool live = false;
+#pragma unroll
+    for (int i = 0; i < kP; ++i) live |= (T[i].x >= kFloor) || (T[i].y >= kFloor);
+    alive = __any_sync(0xffffffffu, live);
   }
-  const float acc0 = acc.x, acc1 = acc.y, T0 = T.x, T1 = T.y;
-  const long long o0 = (long long)u.py0 * a.w + u.px;
   float l1 = 0.f;
-  if (u.in0) {
-    a.image[o0] = acc0;
-    if (kTrack && a.t_final) {
-      a.t_final[o0] = T0;
-      a.n_contrib[o0] = last0 + 1;
+  int wl = -1;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    if (u.px < a.w && u.py0 + r < a.h) {
+      const long long o = (long long)(u.py0 + r) * a.w + u.px;
+      const float v = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
+      a.image[o] = v;
+      if (kTrack && a.t_final) {
+        a.t_final[o] = (r & 1) ? T[r >> 1].y : T[r >> 1].x;
+        a.n_contrib[o] = last[r] + 1;
+      }
+      if (a.target) l1 += fabsf(v - a.target[o]);
     }
-    if (a.target) l1 += fabsf(acc0 - a.target[o0]);
-  }
-  if (u.in1) {
-    const long long o1 = o0 + a.w;
-    a.image[o1] = acc1;
-    if (kTrack && a.t_final) {
-      a.t_final[o1] = T1;
-      a.n_contrib[o1] = last1 + 1;
-    }
-    if (a.target) l1 += fabsf(acc1 - a.target[o1]);
+    wl = max(wl, last[r] + 1);
   }
   if (a.target && a.l1_sum) {
 #pragma unroll
@@ -387,37 +456,46 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int q
     if (lane == 0) atomicAdd(a.l1_sum, (double)l1);
   }
   if (kTrack && a.unit_cost) {
-    int wl = max(last0, last1) + 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, o));
-    if (lane == 0) a.unit_cost[4 * tile + quad] = wl;
+    // (per quarter tile: a wider sub-block records its cost for each quarter it covers)
+    if (lane == 0) {
+      if (kP == 1) {
+        a.unit_cost[4 * tile + sub] = wl;
+      } else {
+        for (int q = 0; q < 4; ++q)
+          if (kP == 4 || (q >> 1) == sub) a.unit_cost[4 * tile + q] = wl;
+      }
+    }
   }
 }
 
-// Non-persistent single-view variant: one CTA per tile (heaviest first),
-// its 4 warps the quarters.
+// Non-persistent single-view variant: one CTA per kWarps / kSubs tiles
+// (heaviest first), one warp per sub-block.
 template <bool kTrack>
-__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_np(FwdArgs a) {
+__global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd_np(FwdArgs a) {
+  constexpr int kP = fwd_pairs<kTrack>(), kSubs = 4 / kP;
   __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
-  const int tile = a.order[blockIdx.x];
-  for (int quad = warp; quad < 4; quad += kWarps) composite_unit<kTrack>(a, tile, quad, s_rec[warp], s_k[warp]);
+  const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
+  if (i < a.n_tiles) composite_unit<kTrack, kP>(a, a.order[i], warp % kSubs, s_rec[warp], s_k[warp]);
 }
 
 template <bool kTrack>
-__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd(FwdArgs a) {
+  constexpr int kP = fwd_pairs<kTrack>();
   __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
-  int tile, quad;
+  int tile, sub;
   bool first = true;
   // an entry-buffer overflow leaves tile ranges past the buffer: touch nothing
   // (the caller sees XG_ST_ENTRY_OVERFLOW and re-bins the view)
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
-  while (next_unit<false>(a.order, a.work, a.n_tiles, first, tile, quad))
-    composite_unit<kTrack>(a, tile, quad, s_rec[warp], s_k[warp]);
+  while (next_unit<false, 4 / kP>(a.order, a.work, a.n_tiles, first, tile, sub))
+    composite_unit<kTrack, kP>(a, tile, sub, s_rec[warp], s_k[warp]);
 }
 
 // ---------------------------------------------------------------------------
@@ -448,7 +526,8 @@ struct BatchArgs {
 };
 
 __device__ __forceinline__ bool next_batch_unit(const BatchArgs& b, bool& first, int& view, int& tile, int& quad) {
-  const uint32_t n_units = 4u * (uint32_t)(b.n_tiles * b.n_views);
+  constexpr uint32_t kSubs = 4 / kFwdPairs;
+  const uint32_t n_units = kSubs * (uint32_t)(b.n_tiles * b.n_views);
   const uint32_t G = gridDim.x, w = threadIdx.x >> 5;
   const uint32_t dealt = min(n_units, G * (uint32_t)kWarps);
   uint32_t k = n_units;
@@ -462,14 +541,14 @@ __device__ __forceinline__ bool next_batch_unit(const BatchArgs& b, bool& first,
     k = dealt + __shfl_sync(0xffffffffu, d, 0);
   }
   if (k >= n_units) return false;
-  const int vt = b.order[k >> 2];
+  const int vt = b.order[k / kSubs];
   view = vt >> 20;
   tile = vt & ((1 << 20) - 1);
-  quad = (int)(k & 3u);
+  quad = (int)(k % kSubs);
   return true;
 }
 
-__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_batch(BatchArgs b) {
+__global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd_batch(BatchArgs b) {
   __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
@@ -480,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_bat
     if (v.n_entries && (long long)*v.n_entries > v.cap) continue;  // overflowed view: re-rendered by the caller
     FwdArgs a{v.mean2d, v.coef, v.inten, v.entry, v.ranges, nullptr, nullptr, b.n_tiles, v.image, nullptr,
               nullptr, nullptr, nullptr, nullptr, nullptr, 0, b.ntx, b.w, b.h};
-    composite_unit<false>(a, tile, quad, s_rec[warp], s_k[warp]);
+    composite_unit<false, kFwdPairs>(a, tile, quad, s_rec[warp], s_k[warp]);
   }
 }
 
@@ -489,17 +568,20 @@ __global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_bat
 // tiles retire, kernels from other streams (the next batch's binning, on
 // higher-priority streams) fill the freed SM slots instead of waiting for the
 // whole launch.
-__global__ void __launch_bounds__(kThreads, XG_FWD_MIN_CTAS) k_composite_fwd_batch_np(BatchArgs b) {
+__global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd_batch_np(BatchArgs b) {
+  constexpr int kSubs = 4 / kFwdPairs;
   __shared__ FRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
-  const int vt = b.order[blockIdx.x];
+  const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
+  if (i >= b.n_tiles * b.n_views) return;
+  const int vt = b.order[i];
   const int view = vt >> 20, tile = vt & ((1 << 20) - 1);
   const BatchView& v = b.v[view];
   if (v.n_entries && (long long)*v.n_entries > v.cap) return;
   FwdArgs a{v.mean2d, v.coef, v.inten, v.entry, v.ranges, nullptr, nullptr, b.n_tiles, v.image, nullptr,
             nullptr, nullptr, nullptr, nullptr, nullptr, 0, b.ntx, b.w, b.h};
-  for (int quad = warp; quad < 4; quad += kWarps) composite_unit<false>(a, tile, quad, s_rec[warp], s_k[warp]);
+  composite_unit<false, kFwdPairs>(a, tile, warp % kSubs, s_rec[warp], s_k[warp]);
 }
 
 // (view, tile) pairs of a batch by descending entry count (64 log buckets).
@@ -1193,19 +1275,19 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
   const bool image_np = npe ? atoi(npe) > 0 : false;
 #ifndef XG_FWD_ALWAYS_TRACK
   if (!t_final || !n_contrib) {  // image only: no contributor tracking
-    if (image_np && kWarps == 4)
-      k_composite_fwd_np<false><<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+    if (image_np)
+      k_composite_fwd_np<false><<<div_up(n_tiles, kWarps * kFwdPairs / 4), kThreads, 0, (cudaStream_t)stream>>>(a);
     else
-      k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"),
+      k_composite_fwd<false><<<persistent_grid(k_composite_fwd<false>, 4 / kFwdPairs * n_tiles, "XG_FWD_CTAS_PER_SM"),
                                kThreads, 0, (cudaStream_t)stream>>>(a);
     return check_launch("k_composite_fwd");
   }
 #endif
-  if (track_np && kWarps == 4)
-    k_composite_fwd_np<true><<<n_tiles, kThreads, 0, (cudaStream_t)stream>>>(a);
+  if (track_np)
+    k_composite_fwd_np<true><<<div_up(n_tiles, kWarps * kFwdTrackPairs / 4), kThreads, 0, (cudaStream_t)stream>>>(a);
   else
-    k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 * n_tiles, "XG_FWD_CTAS_PER_SM"), kThreads,
-                            0, (cudaStream_t)stream>>>(a);
+    k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 / kFwdTrackPairs * n_tiles, "XG_FWD_CTAS_PER_SM"),
+                            kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
 }
 
@@ -1256,11 +1338,11 @@ xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, fl
   // heaviest first by the hardware) beats the persistent queue by ~2 %;
   // XG_BATCH_NONPERSISTENT=0 selects the persistent kernel
   static const bool np = !(getenv("XG_BATCH_NONPERSISTENT") && atoi(getenv("XG_BATCH_NONPERSISTENT")) == 0);
-  if (np && kWarps == 4) {
-    k_composite_fwd_batch_np<<<b.n_tiles * n_views, kThreads, 0, s>>>(b);
+  if (np) {
+    k_composite_fwd_batch_np<<<div_up(b.n_tiles * n_views, kWarps * kFwdPairs / 4), kThreads, 0, s>>>(b);
     return check_launch("k_composite_fwd_batch_np");
   }
-  k_composite_fwd_batch<<<persistent_grid(k_composite_fwd_batch, 4 * b.n_tiles * n_views, "XG_FWD_CTAS_PER_SM"),
+  k_composite_fwd_batch<<<persistent_grid(k_composite_fwd_batch, 4 / kFwdPairs * b.n_tiles * n_views, "XG_FWD_CTAS_PER_SM"),
                           kThreads, 0, s>>>(b);
   return check_launch("k_composite_fwd_batch");
 }

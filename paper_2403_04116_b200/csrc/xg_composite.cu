@@ -338,7 +338,7 @@ __device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit&
     keep = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya, u.yb);
     gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
     r.a = make_float4(mx, -my, A, B);
-    r.b = make_float4(C, -alpha, -raw.it, 0.f);
+    r.b = make_float4(C, -alpha, -raw.it, __log2f(alpha));
   }
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   general = __any_sync(0xffffffffu, keep && gen);
@@ -349,6 +349,38 @@ __device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit&
   }
   __syncwarp();
   return __popc(bal);
+}
+
+// Image-only speculative step (no per-pair tests; see composite_unit): the
+// opacity rides in the exponent, sigma = 2^(p2 + log2 alpha) (record b.w),
+// so a pair costs FADD2 dy, 2 FFMA2 p2, 2 MUFU.EX2, FMUL2 sigma T, FFMA2 acc,
+// FFMA2 T.  Only batches of well-conditioned splats with alpha < 0.98999
+// take it (p2 <= 0 exactly, sigma <= 0.99 without the clamp).  Entries the
+// reference skips for power < -30 are blended here with sigma < 9.4e-14:
+// T * (1 - sigma) rounds back to T exactly, acc moves by < 1e-13 i T.
+template <int kP>
+__device__ __forceinline__ void blend_splat_spec(const FRec& r, float fx, const float2 (&fy)[kP], float2 (&T)[kP],
+                                                 float2 (&acc)[kP]) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmaf_rn(__fmul_rn(r.a.z, dx), dx, r.b.w);
+  const float bdx = __fmul_rn(r.a.w, dx);
+  const float ni = -r.b.z;  // +intensity (folded into FFMA2's negate)
+#pragma unroll
+  for (int i = 0; i < kP; ++i) {
+    const float2 dy = __fadd2_rn(fy[i], bc(r.a.y));
+    const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
+    const float2 e = make_float2(ex2_approx(p.x), ex2_approx(p.y));
+    const float2 w = __fmul2_rn(e, T[i]);
+    acc[i] = __ffma2_rn(bc(ni), w, acc[i]);
+    T[i] = __ffma2_rn(make_float2(-e.x, -e.y), T[i], T[i]);
+  }
+}
+
+template <int kP>
+__device__ __forceinline__ void blend_batch_spec(const FRec* rec, int cnt, float fx, const float2 (&fy)[kP],
+                                                 float2 (&T)[kP], float2 (&acc)[kP]) {
+#pragma unroll kFwdUnroll
+  for (int q = 0; q < cnt; ++q) blend_splat_spec<kP>(rec[q], fx, fy, T, acc);
 }
 
 template <bool kGeneral, bool kTrack, int kP>
@@ -374,6 +406,11 @@ __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int 
 #define XG_FWD_MIN_CTAS_WIDE 4
 #endif
 constexpr int kFwdPairs = XG_FWD_PAIRS, kFwdTrackPairs = XG_FWD_TRACK_PAIRS;
+// image-only launches: speculative test-free batches (blend_batch_spec)
+#ifndef XG_FWD_SPEC
+#define XG_FWD_SPEC 1
+#endif
+constexpr bool kSpec = XG_FWD_SPEC != 0;
 static_assert((kFwdPairs == 1 || kFwdPairs == 2 || kFwdPairs == 4) &&
                   (kFwdTrackPairs == 1 || kFwdTrackPairs == 2 || kFwdTrackPairs == 4) && kWarps % 4 == 0,
               "sub-blocks of 4, 8 or 16 rows; CTAs of whole tiles");
@@ -424,10 +461,51 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
-    if (general)  // warp-uniform, per batch of 32 entries
-      blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
-    else
-      blend_batch<false, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+    if (kTrack || !kSpec) {
+      if (general)  // warp-uniform, per batch of 32 entries
+        blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+      else
+        blend_batch<false, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+    } else {
+      // Image-only: speculate that no live pixel crosses the transmittance
+      // floor inside the batch and blend without per-pair tests; a terminated
+      // pixel holds T = 0, which makes every later step an exact no-op.  If a
+      // pixel did cross, the warp restores the batch-start state and re-runs
+      // the batch with the reference's tests (one extra batch per crossing).
+      bool redo = general;
+      if (!general) {
+        float2 T0[kP], A0[kP];
+#pragma unroll
+        for (int i = 0; i < kP; ++i) {
+          T0[i] = T[i];
+          A0[i] = acc[i];
+        }
+        blend_batch_spec<kP>(rec, cnt, u.fx, fy, T, acc);
+        bool crossed = false;
+#pragma unroll
+        for (int i = 0; i < kP; ++i)
+          crossed |= (T[i].x < kFloor && T0[i].x >= kFloor) || (T[i].y < kFloor && T0[i].y >= kFloor);
+        redo = __any_sync(0xffffffffu, crossed);
+        if (redo) {
+#pragma unroll
+          for (int i = 0; i < kP; ++i) {
+            T[i] = T0[i];
+            acc[i] = A0[i];
+          }
+        }
+      }
+      if (redo) {
+        if (general)
+          blend_batch<true, false, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+        else
+          blend_batch<false, false, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+#pragma unroll
+        for (int i = 0; i < kP; ++i) {
+          T[i].x = T[i].x < kFloor ? 0.f : T[i].x;
+          T[i].y = T[i].y < kFloor ? 0.f : T[i].y;
+        }
+      }
+    }
     __syncwarp();
     bool live = false;
 #pragma unroll

@@ -115,9 +115,13 @@ def test_backward_full_size_c1(xg):
 
 @pytest.mark.parametrize("batch", [1, 3, 4])
 def test_sweep_matches_single_renders(xg, batch):
-    """The sweep renderer (the bench path) renders every view exactly as
-    render() does - per-view streams (batch 1) and the multi-view
-    compositing launch (xg_composite_fwd_batch, incl. a partial last batch)."""
+    """The sweep renderer (the bench path) renders every view as render()
+    does - per-view streams (batch 1) and the multi-view compositing launch
+    (xg_composite_fwd_batch, incl. a partial last batch).  Image-only
+    launches blend speculatively with sigma = 2^(p2 + log2 alpha) (a few ulp
+    from alpha 2^p2) and re-run only batches where a pixel terminates, so
+    they agree with the tracked launch of render() to float32 rounding
+    accumulated over ~3,000 entries per pixel (measured 3e-6 of the max)."""
     import torch
 
     from paper_2403_04116_b200.inference import SweepRenderer
@@ -134,7 +138,9 @@ def test_sweep_matches_single_renders(xg, batch):
     assert torch.equal(out, out2) and torch.equal(host, out.cpu())
     for i, phi in enumerate(angles):
         proj, _ = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (d, d))
-        assert torch.equal(out[i], proj.pixels.to(out.dtype)), i
+        ref = proj.pixels.to(out.dtype)
+        err = (out[i] - ref).abs()
+        assert bool((err <= 2e-5 * ref.abs() + 1e-6 * ref.abs().max()).all()), (i, float(err.max()))
 
 
 def test_rebin_after_entry_overflow(xg):
@@ -266,7 +272,8 @@ def test_general_blend_paths(xg, case):
 
 def test_sweep_with_empty_views(xg):
     """Views in which every splat is culled (empty entry lists) composite to
-    exact zeros in both sweep modes, next to non-empty views."""
+    exact zeros in both sweep modes, next to non-empty views (which match
+    render())."""
     import torch
 
     from paper_2403_04116_b200.inference import SweepRenderer
@@ -285,7 +292,10 @@ def test_sweep_with_empty_views(xg):
         out = SweepRenderer(cloud, sc, n_streams=2, batch=batch).render(angles)
         for i, phi in enumerate(angles):
             proj, sp = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (64, 64))
-            assert torch.equal(out[i], proj.pixels.to(out.dtype)), (batch, i)
+            ref = proj.pixels.to(out.dtype)
+            # image-only launches blend the pairs the reference skips at
+            # power < -30 (sigma < 9.4e-14): background moves by < 1e-12
+            assert bool(((out[i] - ref).abs() <= 2e-5 * ref.abs() + 1e-12).all()), (batch, i)
             if sp.n_active == 0:
                 empty += 1
                 assert float(out[i].abs().max()) == 0.0

@@ -97,6 +97,29 @@ def test_image_parity(golden, runs):
         assert np.allclose(tf, ref["t_final"], rtol=1e-4, atol=1e-7), name
 
 
+@pytest.mark.parametrize("batch", [1, 2])
+def test_image_only_parity(golden, xg, batch):
+    """Image-only launches (sweep renderer / evaluate: speculative test-free
+    batches, re-run exactly where a pixel crosses the transmittance floor)
+    against the reference's golden images and the float32 oracle."""
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    for name in scene_names(golden):
+        p = name + "/"
+        fields = scene_fields(golden, name)
+        cloud = xg.GaussianCloud(**fields, basis_weights=golden[p + "basis_weights"], device="cuda")
+        l_so, l_sd, w, h, pitch, phi = golden[p + "camera"]
+        sc = xg.ScannerConfig(l_so, l_sd, int(w), int(h), pitch)
+        img = SweepRenderer(cloud, sc, batch=batch).render(np.array([phi] * batch))
+        cam = orc.camera_from_view(l_so, l_sd, int(w), int(h), pitch, phi)
+        o = orc.render(fields, golden[p + "basis_weights"], cam)["image"].astype(np.float64)
+        gold = golden[p + "image"]
+        scale = max(np.abs(gold).max(), 1e-30)
+        for v in img.cpu().numpy().astype(np.float64):
+            assert np.all(np.abs(v - gold) <= 1e-4 * np.abs(gold) + 1e-6 * scale), (name, np.abs(v - gold).max())
+            assert np.all(np.abs(v - o) <= 2e-5 * np.abs(o) + 1e-7 * scale), (name, np.abs(v - o).max())
+
+
 def test_backward_parity(golden, runs, xg):
     import torch
 

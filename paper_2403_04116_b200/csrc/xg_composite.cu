@@ -867,6 +867,61 @@ __device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx,
   return (Gs != 0.f) | (v[5] != 0.f);
 }
 
+// Speculative reverse step (batches of well-conditioned, alpha < 0.98999
+// splats in which no pixel's last blended entry falls): no per-pair tests.
+// Pixels active over the whole batch use their centre, inactive ones a row
+// 1e30 away, whose p2 overflows to -inf: sigma = 0, 1 - sigma = 1,
+// rcp.approx(1) = 1, so T, S and every partial stay exactly unchanged
+// (G = dsig * 0 and G dy = 0 * 1e30 are zeros).  Opacity in the exponent as
+// in the forward (record b.w = log2 alpha); pairs the reference skips at
+// power < -30 add sigma < 9.4e-14 terms (T / (1 - sigma) == T exactly).
+template <int kP>
+__device__ __forceinline__ bool unblend_splat_spec(const BRec& r, float fx, const float2 (&fy)[kP],
+                                                   const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP],
+                                                   float* v) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmaf_rn(__fmul_rn(r.a.z, dx), dx, r.b.w);
+  const float bdx = __fmul_rn(r.a.w, dx);
+  float2 sG, sGdy, sGdy2, sgw;
+#pragma unroll
+  for (int i = 0; i < kP; ++i) {
+    const float2 dy = __fadd2_rn(fy[i], bc(r.a.y));
+    const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
+    const float2 ns = make_float2(-ex2_approx(p.x), -ex2_approx(p.y));  // -sigma
+    const float2 om = __fadd2_rn(bc(1.f), ns);
+    const float2 rc = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+    const float2 Tb = __fmul2_rn(T[i], rc);
+    const float2 nw = __fmul2_rn(ns, Tb);
+    const float2 ngw = __fmul2_rn(g[i], nw);
+    const float2 in = __ffma2_rn(nS[i], rc, __fmul2_rn(bc(r.b.z), Tb));
+    const float2 nG = __fmul2_rn(__fmul2_rn(g[i], in), ns);
+    nS[i] = __ffma2_rn(bc(r.b.z), nw, nS[i]);
+    T[i] = Tb;
+    const float2 Gdy = __fmul2_rn(nG, dy);
+    if (i == 0) {
+      sG = nG;
+      sGdy = Gdy;
+      sGdy2 = __fmul2_rn(Gdy, dy);
+      sgw = ngw;
+    } else {
+      sG = __fadd2_rn(sG, nG);
+      sGdy = __fadd2_rn(sGdy, Gdy);
+      sGdy2 = __ffma2_rn(Gdy, dy, sGdy2);
+      sgw = __fadd2_rn(sgw, ngw);
+    }
+  }
+  const float Gs = sG.x + sG.y, Gdys = sGdy.x + sGdy.y;
+  v[0] = Gs * dx;
+  v[1] = Gdys;
+  v[2] = v[0] * dx;
+  v[3] = Gdys * dx;
+  v[4] = sGdy2.x + sGdy2.y;
+  v[5] = sgw.x + sgw.y;
+  v[6] = Gs;
+  v[7] = 0.f;
+  return (Gs != 0.f) | (v[5] != 0.f);
+}
+
 // Sum 16 per-lane values over the warp (two splats' 8-value records); lane l
 // ends with the total of value index (l >> 1) & 15 (transpose-reduce: 16
 // shuffles for 16 values).
@@ -919,7 +974,7 @@ __device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit&
     keep = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya, u.yb);
     gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
     r.a = make_float4(mx, -my, A, B);
-    r.b = make_float4(C, -alpha, raw.it, 0.f);
+    r.b = make_float4(C, -alpha, raw.it, __log2f(alpha));
   }
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   general = __any_sync(0xffffffffu, keep && gen);
@@ -939,7 +994,16 @@ __device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit&
 // xg_preprocess_bwd turns them into the reference's g_mean / g_conic /
 // g_int / g_alpha using the splat's own (A2, B2, C2, alpha).  Each warp
 // reduces its 64 pixels per splat and issues two vector reductions.
-template <bool kGeneral, int kP>
+// kMode: 0 exact fast path, 1 general (clamp, p2 <= 0 test), 2 speculative
+template <int kMode, int kP>
+__device__ __forceinline__ bool unblend_any(const BRec& r, int krel, float fx, const float2 (&fy)[kP],
+                                            const int (&last)[2 * kP], const float2 (&g)[kP], float2 (&T)[kP],
+                                            float2 (&nS)[kP], float* v) {
+  if (kMode == 2) return unblend_splat_spec<kP>(r, fx, fy, g, T, nS, v);
+  return unblend_splat<kMode == 1, kP>(r, krel, fx, fy, last, g, T, nS, v);
+}
+
+template <int kMode, int kP>
 __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, const uint32_t* gid, int cnt, float fx,
                                               const float2 (&fy)[kP], const int (&last)[2 * kP],
                                               const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP],
@@ -950,9 +1014,9 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
   for (int q = cnt - 1; q >= 0; q -= 2) {
     const bool hasB = q >= 1;
     float v[16];
-    bool any = unblend_splat<kGeneral, kP>(rec[q], kk[q], fx, fy, last, g, T, nS, v);
+    bool any = unblend_any<kMode, kP>(rec[q], kk[q], fx, fy, last, g, T, nS, v);
     if (hasB) {
-      any |= unblend_splat<kGeneral, kP>(rec[q - 1], kk[q - 1], fx, fy, last, g, T, nS, v + 8);
+      any |= unblend_any<kMode, kP>(rec[q - 1], kk[q - 1], fx, fy, last, g, T, nS, v + 8);
     } else {
 #pragma unroll
       for (int i = 8; i < 16; ++i) v[i] = 0.f;
@@ -976,6 +1040,12 @@ __device__ __forceinline__ float upstream(const BwdArgs& a, long long o) {
   return a.dl ? a.dl[o] : a.l1_scale * (float)((a.image[o] > a.target[o]) - (a.image[o] < a.target[o]));
 }
 
+// speculative reverse batches (unblend_splat_spec)
+#ifndef XG_BWD_SPEC
+#define XG_BWD_SPEC 1
+#endif
+constexpr bool kBwdSpec = XG_BWD_SPEC != 0;
+
 // Walk entries [e_lo, e_hi) of the tile starting at `start` back to front in
 // batches of 32 ([b1 - 32, b1)), with the two-stage prefetch (entry indices
 // one batch ahead of the records).
@@ -995,10 +1065,27 @@ __device__ __forceinline__ void replay_range(const BwdArgs& a, const Unit& u, lo
     const long long kn = b1 - 64 + lane;
     nxt = fetch(g_nxt, kn >= e_lo, a.mean2d, a.coef, a.inten);
     g_nxt = kn - 32 >= e_lo ? entry_at(a.entry, kn - 32, e_hi) : 0u;
+    bool exact = general || !kBwdSpec;
+    float2 fye[kP];
+    if (!exact) {
+      // every pixel active (last >= the batch's top entry) or inactive
+      // (last < its bottom entry) over the whole batch: speculative step
+      const int khi = (int)(b1 - 1 - start), klo = (int)(max(b1 - 32, e_lo) - start);
+      bool straddle = false;
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        const int l0 = last[2 * i], l1 = last[2 * i + 1];
+        straddle |= (l0 >= klo && l0 < khi) || (l1 >= klo && l1 < khi);
+        fye[i] = make_float2(l0 >= khi ? fy[i].x : 1e30f, l1 >= khi ? fy[i].y : 1e30f);
+      }
+      exact = __any_sync(0xffffffffu, straddle);
+    }
     if (general)
-      unblend_batch<true, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
+      unblend_batch<1, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
+    else if (exact)
+      unblend_batch<0, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
     else
-      unblend_batch<false, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
+      unblend_batch<2, kP>(rec, kk, gid, cnt, u.fx, fye, last, g, T, nS, a.grad_acc);
     __syncwarp();
   }
 }

@@ -383,6 +383,32 @@ __device__ __forceinline__ void blend_batch_spec(const FRec* rec, int cnt, float
   for (int q = 0; q < cnt; ++q) blend_splat_spec<kP>(rec[q], fx, fy, T, acc);
 }
 
+// Tracking speculative step (training forward): sigma = alpha 2^p2 as in
+// the exact path, so T (and t_final, the checkpoints) stay bit-identical to
+// it - a pair below the cut-off has sigma < 9.4e-14 and T - sigma T rounds
+// to T; only acc moves, by < 1e-13 i T.  The last blended entry (n_contrib)
+// is exact: live pixels (T >= floor over the whole batch, else the batch is
+// re-run) record every entry with p2 >= cut.
+template <int kP>
+__device__ __forceinline__ void blend_splat_spec_track(const FRec& r, int krel, float fx, const float2 (&fy)[kP],
+                                                       const bool (&live)[2 * kP], float2 (&T)[kP],
+                                                       float2 (&acc)[kP], int (&last)[2 * kP]) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
+  const float bdx = __fmul_rn(r.a.w, dx);
+#pragma unroll
+  for (int i = 0; i < kP; ++i) {
+    const float2 dy = __fadd2_rn(fy[i], bc(r.a.y));
+    const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
+    const float2 sg = __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
+    const float2 w = __fmul2_rn(sg, T[i]);
+    acc[i] = __ffma2_rn(bc(r.b.z), w, acc[i]);
+    T[i] = __ffma2_rn(sg, T[i], T[i]);
+    last[2 * i] = (live[2 * i] && p.x >= kCut2) ? krel : last[2 * i];
+    last[2 * i + 1] = (live[2 * i + 1] && p.y >= kCut2) ? krel : last[2 * i + 1];
+  }
+}
+
 template <bool kGeneral, bool kTrack, int kP>
 __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, const float2 (&fy)[kP],
                                             float2 (&T)[kP], float2 (&acc)[kP], int (&last)[2 * kP]) {
@@ -411,6 +437,12 @@ constexpr int kFwdPairs = XG_FWD_PAIRS, kFwdTrackPairs = XG_FWD_TRACK_PAIRS;
 #define XG_FWD_SPEC 1
 #endif
 constexpr bool kSpec = XG_FWD_SPEC != 0;
+// tracking launches (training forward): speculative batches with exact
+// n_contrib / t_final (blend_splat_spec_track)
+#ifndef XG_FWD_SPEC_TRACK
+#define XG_FWD_SPEC_TRACK 1
+#endif
+constexpr bool kSpecTrack = XG_FWD_SPEC_TRACK != 0;
 static_assert((kFwdPairs == 1 || kFwdPairs == 2 || kFwdPairs == 4) &&
                   (kFwdTrackPairs == 1 || kFwdTrackPairs == 2 || kFwdTrackPairs == 4) && kWarps % 4 == 0,
               "sub-blocks of 4, 8 or 16 rows; CTAs of whole tiles");
@@ -425,7 +457,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
   constexpr int kR = 2 * kP;
   const int lane = threadIdx.x & 31;
   const Unit u = make_sub<kP>(tile, sub, a.ntx, a.w, a.h, a.ranges);
-  float2 fy[kP], T[kP], acc[kP];
+  float2 fy[kP], T[kP], acc[kP], Tf[kP];  // Tf: final T of a pixel parked at T = 0 (tracking + speculation)
   int last[kR];
   bool any_in = false;
 #pragma unroll
@@ -434,6 +466,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     const bool in0 = u.px < a.w && u.py0 + 2 * i < a.h, in1 = u.px < a.w && u.py0 + 2 * i + 1 < a.h;
     T[i] = make_float2(in0 ? 1.f : 0.f, in1 ? 1.f : 0.f);
     acc[i] = make_float2(0.f, 0.f);
+    Tf[i] = make_float2(0.f, 0.f);
     last[2 * i] = last[2 * i + 1] = -1;
     any_in |= in0 | in1;
   }
@@ -461,26 +494,38 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
-    if (kTrack || !kSpec) {
+    if (!(kTrack ? kSpecTrack : kSpec)) {
       if (general)  // warp-uniform, per batch of 32 entries
         blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
       else
         blend_batch<false, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
     } else {
-      // Image-only: speculate that no live pixel crosses the transmittance
-      // floor inside the batch and blend without per-pair tests; a terminated
-      // pixel holds T = 0, which makes every later step an exact no-op.  If a
-      // pixel did cross, the warp restores the batch-start state and re-runs
-      // the batch with the reference's tests (one extra batch per crossing).
+      // Speculate that no live pixel crosses the transmittance floor inside
+      // the batch and blend without the per-pair T test; a terminated pixel
+      // holds T = 0 (its final T kept in Tf), which makes every later step an
+      // exact no-op.  If a pixel did cross, the warp restores the batch-start
+      // state and re-runs the batch with the reference's tests (one extra
+      // batch per crossing).
       bool redo = general;
       if (!general) {
         float2 T0[kP], A0[kP];
+        int L0[kR];
+        bool lv[kR];
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
           T0[i] = T[i];
           A0[i] = acc[i];
+          lv[2 * i] = T[i].x >= kFloor;
+          lv[2 * i + 1] = T[i].y >= kFloor;
         }
-        blend_batch_spec<kP>(rec, cnt, u.fx, fy, T, acc);
+#pragma unroll
+        for (int r = 0; r < kR; ++r) L0[r] = last[r];
+        if (kTrack) {
+#pragma unroll kFwdUnroll
+          for (int q = 0; q < cnt; ++q) blend_splat_spec_track<kP>(rec[q], kk[q], u.fx, fy, lv, T, acc, last);
+        } else {
+          blend_batch_spec<kP>(rec, cnt, u.fx, fy, T, acc);
+        }
         bool crossed = false;
 #pragma unroll
         for (int i = 0; i < kP; ++i)
@@ -492,15 +537,21 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
             T[i] = T0[i];
             acc[i] = A0[i];
           }
+#pragma unroll
+          for (int r = 0; r < kR; ++r) last[r] = L0[r];
         }
       }
       if (redo) {
         if (general)
-          blend_batch<true, false, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+          blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
         else
-          blend_batch<false, false, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+          blend_batch<false, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
+          if (kTrack) {
+            Tf[i].x = (T[i].x < kFloor && T[i].x > 0.f) ? T[i].x : Tf[i].x;
+            Tf[i].y = (T[i].y < kFloor && T[i].y > 0.f) ? T[i].y : Tf[i].y;
+          }
           T[i].x = T[i].x < kFloor ? 0.f : T[i].x;
           T[i].y = T[i].y < kFloor ? 0.f : T[i].y;
         }
@@ -521,7 +572,8 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
       const float v = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
       a.image[o] = v;
       if (kTrack && a.t_final) {
-        a.t_final[o] = (r & 1) ? T[r >> 1].y : T[r >> 1].x;
+        const float t = (r & 1) ? T[r >> 1].y : T[r >> 1].x, tf = (r & 1) ? Tf[r >> 1].y : Tf[r >> 1].x;
+        a.t_final[o] = t > 0.f ? t : tf;
         a.n_contrib[o] = last[r] + 1;
       }
       if (a.target) l1 += fabsf(v - a.target[o]);

@@ -366,6 +366,10 @@ constexpr int kOsRounds = XG_OS_ROUNDS;
 constexpr int kOsTile = kOsThreads * kOsRounds;  // 2048 items
 constexpr int kOsPasses = 8;
 constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsMask = (1u << 30) - 1u;
+#ifndef XG_OS_LOOKBACK
+#define XG_OS_LOOKBACK 4
+#endif
+constexpr int kOsLookback = XG_OS_LOOKBACK;  // predecessor tiles per look-back round
 
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
   uint32_t v;
@@ -500,16 +504,26 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
       s_pre[d] = 0;
     } else {
       asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(st + d), "r"(kOsAgg | run) : "memory");
+      // windowed look-back: the statuses of kOsLookback predecessors are
+      // loaded together (one L2 round trip instead of one per tile), then
+      // summed nearest first up to the first inclusive prefix
       uint32_t prefix = 0;
       long long j = (long long)tile - 1;
-      for (;;) {
-        uint32_t v;
-        do {
-          v = ld_volatile_u32(a.status + j * 256 + d);
-        } while ((v & ~kOsMask) == 0);
-        prefix += v & kOsMask;
-        if ((v & ~kOsMask) == kOsPre) break;
-        --j;
+      bool done = false;
+      while (!done) {
+        uint32_t v[kOsLookback];
+#pragma unroll
+        for (int w = 0; w < kOsLookback; ++w)
+          v[w] = j - w >= 0 ? ld_volatile_u32(a.status + (j - w) * 256 + d) : kOsPre;  // (tile 0 is a prefix)
+#pragma unroll
+        for (int w = 0; w < kOsLookback; ++w) {
+          if (!done) {
+            while ((v[w] & ~kOsMask) == 0) v[w] = ld_volatile_u32(a.status + (j - w) * 256 + d);
+            prefix += v[w] & kOsMask;
+            done = (v[w] & ~kOsMask) == kOsPre;
+          }
+        }
+        j -= kOsLookback;
       }
       asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(st + d), "r"(kOsPre | (prefix + run)) : "memory");
       s_pre[d] = prefix;

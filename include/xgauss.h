@@ -28,6 +28,7 @@
  *   xg_densify_mark     trainer.py:206-225 densify masks and counts
  *   xg_densify_apply    trainer.py:227-261 compaction, clone shift, split
  *   xg_intensities      gaussians.py:230-232 GaussianCloud.intensities
+ *   xg_view_invariants  gaussians.py:47-69, 222-228 (covariance, opacity)
  *   xg_project_volume   phantom.py:181-250 project_phantom (cone-beam ray march
  *                       of a voxel phantom: the training-target generator)
  *   xg_ssim             metrics.py:57-124 ssim / ssim_and_gradient, fused into
@@ -43,7 +44,7 @@
 extern "C" {
 #endif
 
-#define XG_ABI_VERSION 2
+#define XG_ABI_VERSION 3
 
 typedef enum xg_status {
   XG_OK = 0,
@@ -108,6 +109,10 @@ typedef struct xg_cloud {
                                 very buffer, just uses) it instead of recomputing the
                                 view-independent intensity per view - the non-finite
                                 feature check is then xg_intensities' */
+  const double* invariants;  /* optional [N][8] from xg_view_invariants: Sigma3 (xx xy xz yy
+                                yz zz), opacity, zero-quaternion flag - the view-independent
+                                part of the projection, computed once per cloud by the same
+                                code, so every per-view output stays bit-identical */
 } xg_cloud;
 
 /* Per-view screen-space buffers.  Per-Gaussian arrays are indexed by cloud
@@ -289,6 +294,12 @@ xg_status xg_densify_apply(const float* params, const float* exp_avg, const floa
 
 /* sigmoid(F . lambda) for all N (float32 out); flags non-finite features. */
 xg_status xg_intensities(const xg_cloud* cloud, float* out, uint32_t* counters, void* stream);
+
+/* View-independent projection terms for all N (float64 out[N][8], see
+ * xg_cloud.invariants): R(q/|q|) diag(e^s) squared (gaussians.py:47-69,
+ * frontend.py:126-128) and sigmoid(raw opacity) (gaussians.py:222-228).
+ * A sweep over a static cloud computes them once instead of per view. */
+xg_status xg_view_invariants(const xg_cloud* cloud, double* out, void* stream);
 
 /* The reference kernel-backend contract (_kernels.pyx:23-32, 77-87) on
  * device buffers: n_splats active rows with float64 means2d[A][2],

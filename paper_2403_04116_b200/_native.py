@@ -34,7 +34,7 @@ XG_ST_GRAD_SHIFT = 8
 XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
 XG_CTR_ITEMS = 6
 XG_NCOUNTERS = 8
-XG_ABI_VERSION = 2
+XG_ABI_VERSION = 3
 XG_REPLAY_CHUNK = 256
 XG_MAX_BATCH = 16
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
@@ -49,7 +49,7 @@ c_size = ctypes.c_size_t
 
 class XgCloud(ctypes.Structure):
     _fields_ = [("params", c_void_p), ("basis", c_void_p), ("n", c_i64), ("n_features", c_i32), ("_pad", c_i32),
-                ("intensities", c_void_p)]
+                ("intensities", c_void_p), ("invariants", c_void_p)]
 
 
 class XgVolume(ctypes.Structure):
@@ -128,6 +128,7 @@ SIGNATURES = {
          c_void_p, c_void_p, c_i64, c_void_p, c_void_p],
     ),
     "xg_intensities": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "xg_view_invariants": (c_i32, [c_void_p, c_void_p, c_void_p]),
     "xg_tiles_workspace_bytes": (c_size, [c_i64, c_i32, c_i32]),
     "xg_ssim_workspace_bytes": (c_size, [c_i32, c_i32]),
     "xg_composite_batch_workspace_bytes": (c_size, [c_void_p, c_i32]),
@@ -222,13 +223,15 @@ def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def cloud_struct(cloud, intensities: torch.Tensor | None = None) -> XgCloud:
+def cloud_struct(cloud, intensities: torch.Tensor | None = None,
+                 invariants: torch.Tensor | None = None) -> XgCloud:
     s = XgCloud()
     s.params = ptr(cloud.flat, "cloud")
     s.basis = ptr(cloud.basis_weights, "basis_weights")
     s.n = cloud.n_points
     s.n_features = cloud.n_features
     s.intensities = ptr(intensities, "intensities")
+    s.invariants = ptr(invariants, "invariants")
     return s
 
 
@@ -251,6 +254,15 @@ def raise_for_status(word: int, where: str = "") -> None:
 
 def kernel_launches() -> int:
     return int(lib().xg_kernel_launches())
+
+
+def view_invariants(cloud) -> torch.Tensor:
+    """[N, 8] float64 view-independent projection terms (Sigma3, opacity,
+    zero-quaternion flag) for a sweep over a static cloud (xg_view_invariants)."""
+    out = torch.empty((cloud.n_points, 8), dtype=torch.float64, device=cloud.device)
+    cs = cloud_struct(cloud)
+    check(lib().xg_view_invariants(ctypes.byref(cs), ptr(out), stream()), "xg_view_invariants")
+    return out
 
 
 def intensities(cloud) -> torch.Tensor:

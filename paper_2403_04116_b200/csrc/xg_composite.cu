@@ -1286,7 +1286,11 @@ constexpr int kBwdPairs = XG_BWD_PAIRS;
 static_assert(kBwdPairs == 1 || kBwdPairs == 2 || kBwdPairs == 4, "a sub-block is 4, 8 or 16 rows");
 constexpr int kBwdSubs = 4 / kBwdPairs;  // sub-blocks per tile
 
+#ifdef XG_BWD_CK_MIN_CTAS
+__global__ void __launch_bounds__(kThreads, XG_BWD_CK_MIN_CTAS) k_composite_bwd_ck(BwdArgs a) {
+#else
 __global__ void __launch_bounds__(kThreads) k_composite_bwd_ck(BwdArgs a) {
+#endif
   __shared__ BRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   __shared__ uint32_t s_gid[kWarps][32];

@@ -41,6 +41,7 @@ struct CloudPtrs {
   const float* feat;
   const float* basis;
   const float* inten_pre;  // optional precomputed sigmoid(F . lambda) (xg_cloud.intensities)
+  const double* inv;       // optional [N][8] view invariants (xg_cloud.invariants)
   long long n;
   int nf;
 };
@@ -55,6 +56,7 @@ __host__ static CloudPtrs make_cloud(const xg_cloud& c) {
   p.feat = p.raw + n;
   p.basis = c.basis;
   p.inten_pre = c.intensities;
+  p.inv = c.invariants;
   p.n = n;
   p.nf = c.n_features;
   return p;
@@ -98,7 +100,20 @@ __device__ __forceinline__ bool quat_rot(const float* q4, double* r, double* qn)
   return true;
 }
 
-__device__ __forceinline__ void project_one(const CloudPtrs& c, const Cam& k, long long i, Proj& p) {
+// M = R diag(e^s); Sigma3 = M M^T (frontend.py:127-128)
+__device__ __forceinline__ void sigma3(const CloudPtrs& c, long long i, const double* rot, double* s, double* sig3) {
+  for (int a = 0; a < 3; ++a) s[a] = det_exp((double)c.logs[3 * i + a]);
+  double m[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) m[3 * a + b] = rot[3 * a + b] * s[b];
+  int q = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = a; b < 3; ++b)
+      sig3[q++] = (m[3 * a] * m[3 * b] + m[3 * a + 1] * m[3 * b + 1]) + m[3 * a + 2] * m[3 * b + 2];
+}
+
+__device__ __forceinline__ void project_one(const CloudPtrs& c, const Cam& k, long long i, Proj& p,
+                                            bool use_inv = false) {
   const double px = c.pos[3 * i], py = c.pos[3 * i + 1], pz = c.pos[3 * i + 2];
   // t = W mu + T (frontend.py:116).  The reference evaluates positions @ W^T
   // through BLAS dgemm, which accumulates as fma(w2, z, fma(w1, y, w0 x));
@@ -112,19 +127,20 @@ __device__ __forceinline__ void project_one(const CloudPtrs& c, const Cam& k, lo
   const double tz = p.t[2];
   p.u[0] = (k.f * p.t[0]) / tz + k.cx;  // frontend.py:122
   p.u[1] = (k.f * p.t[1]) / tz + k.cy;
-  if (!quat_rot(c.rot + 4 * i, p.rot, nullptr)) {
-    p.zero_q = true;
-    return;
+  if (use_inv) {  // view-invariant cache (xg_view_invariants): the same numbers, computed once
+    const double* v = c.inv + 8 * i;
+    if (v[7] != 0.0) {
+      p.zero_q = true;
+      return;
+    }
+    for (int a = 0; a < 6; ++a) p.sig3[a] = v[a];
+  } else {
+    if (!quat_rot(c.rot + 4 * i, p.rot, nullptr)) {
+      p.zero_q = true;
+      return;
+    }
+    sigma3(c, i, p.rot, p.s, p.sig3);
   }
-  for (int a = 0; a < 3; ++a) p.s[a] = det_exp((double)c.logs[3 * i + a]);
-  // M = R diag(s); Sigma3 = M M^T (frontend.py:127-128)
-  double m[9];
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) m[3 * a + b] = p.rot[3 * a + b] * p.s[b];
-  int q = 0;
-  for (int a = 0; a < 3; ++a)
-    for (int b = a; b < 3; ++b)
-      p.sig3[q++] = (m[3 * a] * m[3 * b] + m[3 * a + 1] * m[3 * b + 1]) + m[3 * a + 2] * m[3 * b + 2];
   // J2 (pixel units, no clamping; frontend.py:197-205) and U2 = J2 W (:129)
   const double j00 = k.f / tz;
   const double j02 = (-k.f * p.t[0]) / (tz * tz);
@@ -173,7 +189,8 @@ __global__ void k_preprocess(CloudPtrs c, Cam k, xg_splats sp, xg_splat_extras e
   bool active = false;
   if (i < c.n) {
     Proj p;
-    project_one(c, k, i, p);
+    const bool use_inv = c.inv != nullptr;
+    project_one(c, k, i, p, use_inv);
     if (c.inten_pre) {  // view-independent: computed once per cloud (xg_intensities)
       if (sp.inten != c.inten_pre) sp.inten[i] = c.inten_pre[i];
     } else {
@@ -210,7 +227,7 @@ __global__ void k_preprocess(CloudPtrs c, Cam k, xg_splats sp, xg_splat_extras e
         // conic = (cc, -bb, aa) / det (frontend.py:137) on the log2 scale:
         // p2 = -0.5 log2e (a dx^2 + c dy^2) - log2e b dx dy
         const double ca = p.cc / p.det, cb = -p.bb / p.det, cc = p.aa / p.det;
-        const double alpha = det_sigmoid((double)c.raw[i]);
+        const double alpha = use_inv ? c.inv[8 * i + 6] : det_sigmoid((double)c.raw[i]);
         float4 cf;
         cf.x = (float)(-0.5 * kLog2e * ca);
         cf.y = (float)(-kLog2e * cb);
@@ -241,6 +258,18 @@ __global__ void k_preprocess(CloudPtrs c, Cam k, xg_splats sp, xg_splat_extras e
     if (act) atomicAdd(&sp.counters[XG_CTR_ACTIVE], (unsigned)__popc(act));
     if (st) atomicOr(&sp.counters[XG_CTR_STATUS], st);
   }
+}
+
+__global__ void k_view_invariants(CloudPtrs c, double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c.n) return;
+  double rot[9], s[3], sig3[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const bool ok = quat_rot(c.rot + 4 * i, rot, nullptr);
+  if (ok) sigma3(c, i, rot, s, sig3);
+  double* o = out + 8 * i;
+  for (int a = 0; a < 6; ++a) o[a] = sig3[a];
+  o[6] = det_sigmoid((double)c.raw[i]);
+  o[7] = ok ? 0.0 : 1.0;
 }
 
 __global__ void k_intensities(CloudPtrs c, float* out, uint32_t* counters) {
@@ -469,6 +498,17 @@ xg_status xg_preprocess_fwd(const xg_cloud* cloud, const xg_camera* cam, xg_spla
   const int block = 128;
   k_preprocess<<<div_up(cloud->n, block), block, 0, s>>>(make_cloud(*cloud), make_cam(*cam), *sp, ex);
   return check_launch("k_preprocess");
+}
+
+xg_status xg_view_invariants(const xg_cloud* cloud, double* out, void* stream) {
+  if (!cloud || !cloud->params || cloud->n < 0 || (cloud->n > 0 && !out)) {
+    set_error_msg("xg_view_invariants: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  if (cloud->n == 0) return XG_OK;
+  const int block = 256;
+  k_view_invariants<<<div_up(cloud->n, block), block, 0, (cudaStream_t)stream>>>(make_cloud(*cloud), out);
+  return check_launch("k_view_invariants");
 }
 
 xg_status xg_intensities(const xg_cloud* cloud, float* out, uint32_t* counters, void* stream) {

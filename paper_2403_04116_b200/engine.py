@@ -118,10 +118,13 @@ class Frame:
         return s
 
     # --- stages -------------------------------------------------------------
-    def preprocess(self, cloud, cam: XgCamera, intensities: torch.Tensor | None = None) -> None:
+    def preprocess(self, cloud, cam: XgCamera, intensities: torch.Tensor | None = None,
+                   invariants: torch.Tensor | None = None) -> None:
         """K1.  ``intensities`` (the cloud's precomputed [N] float32
         sigmoid(F . lambda), e.g. for a sweep) is used as this frame's
-        intensity buffer instead of recomputing it per view."""
+        intensity buffer instead of recomputing it per view; ``invariants``
+        (``_native.view_invariants``) likewise replaces the per-view
+        covariance / opacity evaluation (same numbers, computed once)."""
         if cloud.n_points != self.n:
             raise ValueError("frame was allocated for a different cloud size")
         self.cam = cam
@@ -129,7 +132,7 @@ class Frame:
             self.inten = intensities  # shared, read-only for the compositing kernels
         elif getattr(self, "_own_inten", None) is not None and self.inten is not self._own_inten:
             self.inten = self._own_inten
-        cs = nat.cloud_struct(cloud, intensities)
+        cs = nat.cloud_struct(cloud, intensities, invariants)
         sp = self.splats_struct()
         ex = None
         if self.extras is not None:

@@ -99,6 +99,8 @@ class SweepRenderer:
         # the intensities are view-independent (isotropic RIRF): once per sweep
         # (raises for non-finite features, as the per-view check would)
         self._inten = nat.intensities(self.cloud)
+        # likewise the covariance / opacity terms of the projection
+        self._inv = nat.view_invariants(self.cloud)
         if self.batch > 1:
             self._render_batched(angles, out, host_out, status, composite_events)
         else:
@@ -115,7 +117,7 @@ class SweepRenderer:
             k = i % len(self.streams)
             st, fr = self.streams[k], self.frames[k]
             with torch.cuda.stream(st):
-                fr.preprocess(self.cloud, self.camera(phi), self._inten)
+                fr.preprocess(self.cloud, self.camera(phi), self._inten, self._inv)
                 fr.bin()
                 if composite_events is not None:
                     a = torch.cuda.Event(enable_timing=True)
@@ -148,7 +150,7 @@ class SweepRenderer:
                 with torch.cuda.stream(st):
                     if done[j % 2] is not None:
                         st.wait_event(done[j % 2])  # the set's previous composite read these buffers
-                    fr.preprocess(self.cloud, self.camera(angles[i]), self._inten)
+                    fr.preprocess(self.cloud, self.camera(angles[i]), self._inten, self._inv)
                     fr.bin()
                 cs.wait_stream(st)
             nv = hi - lo

@@ -270,6 +270,44 @@ def test_general_blend_paths(xg, case):
         assert ok, (case, k, rel)
 
 
+def test_view_invariants_bit_identical(xg):
+    """The sweep's once-per-cloud covariance / opacity cache
+    (xg_view_invariants) leaves every per-view projection output
+    bit-identical - anisotropic rotated splats, a zero quaternion off screen
+    (no error, as in the reference) and, on screen, the reference's error."""
+    import torch
+
+    from paper_2403_04116_b200 import _native as nat
+    from paper_2403_04116_b200.engine import Frame
+    from paper_2403_04116_b200.errors import InvalidParameterError
+
+    rng = np.random.default_rng(11)
+    n = 3000
+    f = _random_fields(rng, n, rng.uniform(0.05, 0.95, size=n), 0.5, 6.0, 3.0)
+    f["rotations"][7] = 0.0
+    f["positions"][7] = np.float32([0.0, 0.0, -5000.0])  # behind the source: culled before the quaternion
+    cloud = xg.GaussianCloud(**f, basis_weights=np.ones(4, np.float32), device="cuda")
+    sc = xg.ScannerConfig(L_SO, L_SD, 128, 96, 1.5)
+    inten, inv = nat.intensities(cloud), nat.view_invariants(cloud)
+    for phi in (0.0, 0.4, np.pi / 4, 2.5):
+        cam = xg.geometry.camera_pod(xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (96, 128))
+        a, b = Frame(n, 96, 128, "cuda"), Frame(n, 96, 128, "cuda")
+        a.preprocess(cloud, cam)
+        b.preprocess(cloud, cam, inten, inv)
+        torch.cuda.synchronize()
+        act = a.tiles_touched > 0
+        assert int(act.sum()) > 0 and torch.equal(a.tiles_touched, b.tiles_touched), phi
+        for name in ("mean2d", "coef", "rect", "depth_key"):
+            assert torch.equal(getattr(a, name)[act], getattr(b, name)[act]), (phi, name)
+    # a zero quaternion on screen raises through the cache too
+    f["positions"][7] = np.float32([0.0, 0.0, 0.0])
+    cloud = xg.GaussianCloud(**f, basis_weights=np.ones(4, np.float32), device="cuda")
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    with pytest.raises(InvalidParameterError):
+        SweepRenderer(cloud, sc, batch=2).render(np.array([0.0, 0.3]))
+
+
 def test_sweep_with_empty_views(xg):
     """Views in which every splat is culled (empty entry lists) composite to
     exact zeros in both sweep modes, next to non-empty views (which match

@@ -359,8 +359,16 @@ def run_ours(args) -> None:
         step_idx[0] += 1
         rend.render(angles, out=out, check=False, composite_events=ev)
 
+    # XG_PROFILE_TIMED=1: open the CUDA profiler range around the timed
+    # region only (ncu --profile-from-start off -> the launch list of exactly
+    # the timed sweep; profiles/)
+    prof = os.environ.get("XG_PROFILE_TIMED") == "1"
+    if prof:
+        torch.cuda.profiler.start()
     with ClockSampler(local) as clk:
         ms = timed(step, args.steps)
+    if prof:
+        torch.cuda.profiler.stop()
     launches = _native.kernel_launches() - launches0
     # per launch: a batched launch composites nv views
     comp_ctx = float(np.mean([a.elapsed_time(b) / nv for a, b, nv in comp_events]))

@@ -258,6 +258,10 @@ __global__ void __launch_bounds__(kBinThreads)
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t excl = incl - cnt;
     const int wdt = cnt ? (int)(r.z - r.x + 1) : 1;
+    // j / wdt as a multiply-high: exact for j, wdt < 2^16 with m = ceil(2^32 / wdt)
+    // (wdt = 1, where m would be 2^32, is marked by m = 0)
+    const uint32_t mdiv =
+        wdt > 1 ? (uint32_t)((0x100000000ull + (unsigned long long)wdt - 1ull) / (unsigned long long)wdt) : 0u;
     for (uint32_t e0 = 0; e0 < total; e0 += 32) {
       const uint32_t e = e0 + lane;
       int lo = 0;
@@ -269,11 +273,13 @@ __global__ void __launch_bounds__(kBinThreads)
       }
       const uint32_t j = e - __shfl_sync(0xffffffffu, excl, lo);
       const int ow = __shfl_sync(0xffffffffu, wdt, lo);
+      const uint32_t om = __shfl_sync(0xffffffffu, mdiv, lo);
       const int ox = __shfl_sync(0xffffffffu, (int)r.x, lo);
       const int oy = __shfl_sync(0xffffffffu, (int)r.y, lo);
       const uint32_t og = __shfl_sync(0xffffffffu, g, lo);
       const bool valid = e < total;
-      const int t = valid ? (oy + (int)(j / (uint32_t)ow)) * ntx + ox + (int)(j % (uint32_t)ow) : -1;
+      const uint32_t jq = om ? __umulhi(j, om) : j;
+      const int t = valid ? (oy + (int)jq) * ntx + ox + (int)(j - jq * (uint32_t)ow) : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, t);
       const uint32_t base = valid ? mine[t] : 0u;
       if (valid) {

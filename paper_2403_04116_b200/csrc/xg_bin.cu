@@ -154,6 +154,7 @@ constexpr int kBinWarps = kBinThreads / 32;
 #define XG_BIN_MAX_ROUNDS 16
 #endif
 constexpr int kBinMaxRounds = XG_BIN_MAX_ROUNDS;              // 32-Gaussian rounds per warp (max)
+static_assert(kBinThreads * kBinMaxRounds < 65536, "k_bin_emit keeps per-tile local offsets in 16 bits");
 
 // Rounds per warp (chunk = 256 x rounds Gaussians per CTA).  Every CTA pays
 // O(T) fixed work (zeroing and scanning its 8 x T per-warp counters, reading
@@ -208,12 +209,21 @@ __global__ void __launch_bounds__(kBinThreads)
     k_bin_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
                const ushort4* __restrict__ rect, long long n, int ntx, int T, int rounds,
                const uint32_t* __restrict__ offs, long long cap, uint32_t* __restrict__ entry_splat) {
-  extern __shared__ uint32_t wcnt[];  // [kBinWarps][T]
+  // shared: base[T] (the CTA's global start per tile, 32-bit) and per-warp
+  // 16-bit counters / local offsets packed two tiles per word
+  // ([kBinWarps][ceil(T/2)]): 20 T bytes, so two CTAs fit an SM at T = 4096.
+  // Local offsets are bounded by the chunk (<= 256 x 16 Gaussians, one entry
+  // per tile each) and stay below 2^16.
+  extern __shared__ uint32_t smem_bin[];
+  const int TW = (T + 1) >> 1;
+  uint32_t* tbase = smem_bin;
+  uint32_t* wcnt = smem_bin + T;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x;
-  for (int i = threadIdx.x; i < kBinWarps * T; i += kBinThreads) wcnt[i] = 0;
+  for (int i = threadIdx.x; i < kBinWarps * TW; i += kBinThreads) wcnt[i] = 0;
   __syncthreads();
-  uint32_t* mine = wcnt + warp * T;
+  uint32_t* mine = wcnt + warp * TW;
+  uint16_t* mine16 = reinterpret_cast<uint16_t*>(mine);  // tile t = half t & 1 of word t >> 1 (little endian)
   const long long wlo = (long long)blockIdx.x * kBinThreads * rounds + (long long)warp * 32 * rounds;
   // phase 1: per-warp entry counts per tile
   for (int rd = 0; rd < rounds; ++rd) {
@@ -223,22 +233,31 @@ __global__ void __launch_bounds__(kBinThreads)
       if (n_tiles[g]) {
         const ushort4 r = rect[g];
         for (int ty = r.y; ty <= r.w; ++ty)
-          for (int tx = r.x; tx <= r.z; ++tx) atomicAdd(&mine[ty * ntx + tx], 1u);
+          for (int tx = r.x; tx <= r.z; ++tx) {
+            const int t = ty * ntx + tx;
+            atomicAdd(&mine[t >> 1], 1u << ((t & 1) << 4));
+          }
       }
     }
   }
   __syncthreads();
-  // phase 2: global base of every (warp, tile) run
-  for (int t = threadIdx.x; t < T; t += kBinThreads) {
-    uint32_t run = offs[(long long)t * C + blockIdx.x];
+  // phase 2: the CTA's global base per tile, per-warp local offsets (a thread
+  // owns one word = two tiles)
+  for (int k = threadIdx.x; k < TW; k += kBinThreads) {
+    const int t0 = 2 * k, t1 = 2 * k + 1;
+    tbase[t0] = offs[(long long)t0 * C + blockIdx.x];
+    if (t1 < T) tbase[t1] = offs[(long long)t1 * C + blockIdx.x];
+    uint32_t l0 = 0, l1 = 0;
     for (int w = 0; w < kBinWarps; ++w) {
-      const uint32_t c = wcnt[w * T + t];
-      wcnt[w * T + t] = run;
-      run += c;
+      const uint32_t c = wcnt[w * TW + k];
+      wcnt[w * TW + k] = l0 | (l1 << 16);
+      l0 += c & 0xffffu;
+      l1 += c >> 16;
     }
   }
   __syncthreads();
   // phase 3: enumerate entries in (depth, rect row-major) order, rank per tile
+  __shared__ uint32_t s_nz[kBinWarps][32];  // lanes with entries, in lane order
   const unsigned lt = lanemask_lt();
   for (int rd = 0; rd < rounds; ++rd) {
     const long long s = wlo + rd * 32 + lane;
@@ -262,15 +281,21 @@ __global__ void __launch_bounds__(kBinThreads)
     // (wdt = 1, where m would be 2^32, is marked by m = 0)
     const uint32_t mdiv =
         wdt > 1 ? (uint32_t)((0x100000000ull + (unsigned long long)wdt - 1ull) / (unsigned long long)wdt) : 0u;
+    // owner of entry e = the last lane with entries whose exclusive prefix is
+    // <= e: per 32-entry window, the lanes' start positions as one bit mask
+    // (redux.sync.or) and the count of starts up to e index the compacted
+    // list of lanes with entries (no dependent shuffle chain)
+    const unsigned nzm = __ballot_sync(0xffffffffu, cnt > 0);
+    if (cnt > 0) s_nz[warp][__popc(nzm & lt)] = (uint32_t)lane;
+    __syncwarp();
+    uint32_t before = 0;  // starts before the window
     for (uint32_t e0 = 0; e0 < total; e0 += 32) {
       const uint32_t e = e0 + lane;
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int cand = lo + step;
-        const uint32_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-        if (cand < 32 && ex <= e) lo = cand;
-      }
+      const uint32_t bit = (cnt > 0 && excl >= e0 && excl - e0 < 32u) ? 1u << (excl - e0) : 0u;
+      const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+      const uint32_t R = before + __popc(starts & (0xffffffffu >> (31 - lane)));  // starts <= e (>= 1)
+      before += __popc(starts);
+      const int lo = (int)s_nz[warp][R - 1u];
       const uint32_t j = e - __shfl_sync(0xffffffffu, excl, lo);
       const int ow = __shfl_sync(0xffffffffu, wdt, lo);
       const uint32_t om = __shfl_sync(0xffffffffu, mdiv, lo);
@@ -281,15 +306,16 @@ __global__ void __launch_bounds__(kBinThreads)
       const uint32_t jq = om ? __umulhi(j, om) : j;
       const int t = valid ? (oy + (int)jq) * ntx + ox + (int)(j - jq * (uint32_t)ow) : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, t);
-      const uint32_t base = valid ? mine[t] : 0u;
+      const uint32_t loc = valid ? (uint32_t)mine16[t] : 0u;
       if (valid) {
-        const long long pos = (long long)base + __popc(peers & lt);
+        const long long pos = (long long)tbase[t] + loc + __popc(peers & lt);
         if (pos < cap) entry_splat[pos] = og;
       }
       __syncwarp();
-      if (valid && (peers >> lane) == 1u) mine[t] = base + __popc(peers);  // highest peer lane
+      if (valid && (peers >> lane) == 1u) mine16[t] = (uint16_t)(loc + __popc(peers));  // highest peer lane
       __syncwarp();
     }
+    __syncwarp();  // (s_nz is rewritten by the next round)
   }
 }
 
@@ -301,7 +327,12 @@ struct BinWs {
   size_t tail_bytes;
 };
 
-bool multisplit(int n_tiles) { return n_tiles <= kBinMaxTiles; }
+// fused multisplit up to this many tiles, duplicate + radix sort beyond
+#ifndef XG_BIN_MULTISPLIT_TILES
+#define XG_BIN_MULTISPLIT_TILES 4096
+#endif
+static_assert(XG_BIN_MULTISPLIT_TILES <= 4096, "multisplit counters: 8 warps x 4096 x 4 B of shared memory");
+bool multisplit(int n_tiles) { return n_tiles <= XG_BIN_MULTISPLIT_TILES; }
 
 int64_t bin_chunks(int64_t n, int n_tiles) { return (n + bin_chunk(n, n_tiles) - 1) / bin_chunk(n, n_tiles); }
 
@@ -382,11 +413,11 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     // 2-4. fused duplicate + stable tile sort + ranges
     const int C = (int)bin_chunks(n, n_tiles);
     const size_t sm_count = sizeof(uint32_t) * (size_t)n_tiles;
-    const size_t sm_emit = sizeof(uint32_t) * (size_t)kBinWarps * n_tiles;
+    const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2));
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(k_bin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(uint32_t) * kBinWarps * kBinMaxTiles));
+                           (int)(sizeof(uint32_t) * (kBinMaxTiles + kBinWarps * (kBinMaxTiles / 2))));
       attr_set = true;
     }
     k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,

@@ -170,26 +170,50 @@ inline int bin_rounds(int64_t n, int n_tiles) {
 inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
 
+// Per-warp entry counts per tile, 16-bit, two tiles per word
+// ([C][kBinWarps][ceil(T/2)], the warp's Gaussians exactly as k_bin_emit
+// walks them), kept for k_bin_emit, and the per-CTA totals hist[T][C] for
+// the scan.
 __global__ void __launch_bounds__(kBinThreads)
     k_bin_count(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
                 const ushort4* __restrict__ rect, long long n, int ntx, int T, int rounds,
-                uint32_t* __restrict__ hist) {
-  extern __shared__ uint32_t cnt[];  // [T]
-  for (int t = threadIdx.x; t < T; t += kBinThreads) cnt[t] = 0;
+                uint32_t* __restrict__ hist, uint32_t* __restrict__ wc_out) {
+  extern __shared__ uint32_t wcnt[];  // [kBinWarps][TW]
+  const int TW = (T + 1) >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kBinWarps * TW; i += kBinThreads) wcnt[i] = 0;
   __syncthreads();
-  const long long chunk = (long long)kBinThreads * rounds;
-  const long long lo = (long long)blockIdx.x * chunk;
-  const long long hi = lo + chunk < n ? lo + chunk : n;
-  for (long long s = lo + threadIdx.x; s < hi; s += kBinThreads) {
-    const uint32_t g = order[s];
-    if (n_tiles[g] == 0) continue;
-    const ushort4 r = rect[g];
-    for (int ty = r.y; ty <= r.w; ++ty)
-      for (int tx = r.x; tx <= r.z; ++tx) atomicAdd(&cnt[ty * ntx + tx], 1u);
+  uint32_t* mine = wcnt + warp * TW;
+  const long long wlo = (long long)blockIdx.x * kBinThreads * rounds + (long long)warp * 32 * rounds;
+  for (int rd = 0; rd < rounds; ++rd) {
+    const long long s = wlo + rd * 32 + lane;
+    if (s < n) {
+      const uint32_t g = order[s];
+      if (n_tiles[g]) {
+        const ushort4 r = rect[g];
+        for (int ty = r.y; ty <= r.w; ++ty)
+          for (int tx = r.x; tx <= r.z; ++tx) {
+            const int t = ty * ntx + tx;
+            atomicAdd(&mine[t >> 1], 1u << ((t & 1) << 4));
+          }
+      }
+    }
   }
   __syncthreads();
   const int C = gridDim.x;
-  for (int t = threadIdx.x; t < T; t += kBinThreads) hist[(long long)t * C + blockIdx.x] = cnt[t];
+  uint32_t* out = wc_out + (long long)blockIdx.x * kBinWarps * TW;
+  for (int k = threadIdx.x; k < TW; k += kBinThreads) {
+    uint32_t s0 = 0, s1 = 0;
+#pragma unroll
+    for (int w = 0; w < kBinWarps; ++w) {
+      const uint32_t c = wcnt[w * TW + k];
+      out[w * TW + k] = c;
+      s0 += c & 0xffffu;
+      s1 += c >> 16;
+    }
+    hist[(long long)(2 * k) * C + blockIdx.x] = s0;
+    if (2 * k + 1 < T) hist[(long long)(2 * k + 1) * C + blockIdx.x] = s1;
+  }
 }
 
 __global__ void k_flag_overflow(uint32_t* counters, long long cap) {
@@ -208,7 +232,8 @@ __global__ void k_bin_ranges(const uint32_t* __restrict__ offs, int C, int T, co
 __global__ void __launch_bounds__(kBinThreads)
     k_bin_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
                const ushort4* __restrict__ rect, long long n, int ntx, int T, int rounds,
-               const uint32_t* __restrict__ offs, long long cap, uint32_t* __restrict__ entry_splat) {
+               const uint32_t* __restrict__ offs, const uint32_t* __restrict__ wc_in, long long cap,
+               uint32_t* __restrict__ entry_splat) {
   // shared: base[T] (the CTA's global start per tile, 32-bit) and per-warp
   // 16-bit counters / local offsets packed two tiles per word
   // ([kBinWarps][ceil(T/2)]): 20 T bytes, so two CTAs fit an SM at T = 4096.
@@ -220,27 +245,13 @@ __global__ void __launch_bounds__(kBinThreads)
   uint32_t* wcnt = smem_bin + T;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x;
-  for (int i = threadIdx.x; i < kBinWarps * TW; i += kBinThreads) wcnt[i] = 0;
+  // phase 1: the per-warp counts k_bin_count kept
+  const uint32_t* wc = wc_in + (long long)blockIdx.x * kBinWarps * TW;
+  for (int i = threadIdx.x; i < kBinWarps * TW; i += kBinThreads) wcnt[i] = wc[i];
   __syncthreads();
   uint32_t* mine = wcnt + warp * TW;
   uint16_t* mine16 = reinterpret_cast<uint16_t*>(mine);  // tile t = half t & 1 of word t >> 1 (little endian)
   const long long wlo = (long long)blockIdx.x * kBinThreads * rounds + (long long)warp * 32 * rounds;
-  // phase 1: per-warp entry counts per tile
-  for (int rd = 0; rd < rounds; ++rd) {
-    const long long s = wlo + rd * 32 + lane;
-    if (s < n) {
-      const uint32_t g = order[s];
-      if (n_tiles[g]) {
-        const ushort4 r = rect[g];
-        for (int ty = r.y; ty <= r.w; ++ty)
-          for (int tx = r.x; tx <= r.z; ++tx) {
-            const int t = ty * ntx + tx;
-            atomicAdd(&mine[t >> 1], 1u << ((t & 1) << 4));
-          }
-      }
-    }
-  }
-  __syncthreads();
   // phase 2: the CTA's global base per tile, per-warp local offsets (a thread
   // owns one word = two tiles)
   for (int k = threadIdx.x; k < TW; k += kBinThreads) {
@@ -323,6 +334,7 @@ struct BinWs {
   unsigned long long *keyN1, *keyN2;
   uint32_t *valN1, *offN, *keyE0, *keyE1, *valE1;
   uint32_t *hist, *hoff;  // multisplit path: [T][C] counts and their scan
+  uint32_t* wcnt;         //   and the per-warp 16-bit counts [C][kBinWarps][ceil(T/2)]
   void* tail;
   size_t tail_bytes;
 };
@@ -335,6 +347,11 @@ static_assert(XG_BIN_MULTISPLIT_TILES <= 4096, "multisplit counters: 8 warps x 4
 bool multisplit(int n_tiles) { return n_tiles <= XG_BIN_MULTISPLIT_TILES; }
 
 int64_t bin_chunks(int64_t n, int n_tiles) { return (n + bin_chunk(n, n_tiles) - 1) / bin_chunk(n, n_tiles); }
+
+size_t bin_wcnt_bytes(int64_t n, int n_tiles) {
+  if (!multisplit(n_tiles)) return 0;
+  return align_up(sizeof(uint32_t) * (size_t)bin_chunks(n, n_tiles) * kBinWarps * (size_t)((n_tiles + 1) / 2));
+}
 
 size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   size_t a = radix_workspace_bytes(multisplit(n_tiles) ? n : (n > cap ? n : cap));
@@ -359,6 +376,7 @@ bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, int n_tiles, BinWs& w
   w.valE1 = (uint32_t*)p; p += be;
   w.hist = (uint32_t*)p; p += bh;
   w.hoff = (uint32_t*)p; p += bh;
+  w.wcnt = (uint32_t*)p; p += bin_wcnt_bytes(n, n_tiles);
   w.tail = p;
   const size_t used = (size_t)(p - (char*)ws);
   const size_t tb = tail_bytes(n, cap, n_tiles);
@@ -379,7 +397,8 @@ size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles
   const bool ms = multisplit(n_tiles_total);
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(entry_capacity > 0 ? entry_capacity : 1));
   const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)bin_chunks(n, n_tiles_total)) : 0;
-  return 6 * bn + 3 * be + 2 * bh + tail_bytes(n, entry_capacity, n_tiles_total) + 256;
+  return 6 * bn + 3 * be + 2 * bh + bin_wcnt_bytes(n, n_tiles_total) + tail_bytes(n, entry_capacity, n_tiles_total) +
+         256;
 }
 
 xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size_t workspace_bytes,
@@ -412,16 +431,18 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   if (multisplit(n_tiles)) {
     // 2-4. fused duplicate + stable tile sort + ranges
     const int C = (int)bin_chunks(n, n_tiles);
-    const size_t sm_count = sizeof(uint32_t) * (size_t)n_tiles;
+    const size_t sm_count = sizeof(uint32_t) * (size_t)kBinWarps * ((n_tiles + 1) / 2);
     const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2));
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(k_bin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(sizeof(uint32_t) * (kBinMaxTiles + kBinWarps * (kBinMaxTiles / 2))));
+      cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(uint32_t) * kBinWarps * (kBinMaxTiles / 2)));
       attr_set = true;
     }
     k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                                 bin_rounds(n, n_tiles), w.hist);
+                                                 bin_rounds(n, n_tiles), w.hist, w.wcnt);
     if ((st = check_launch("k_bin_count")) != XG_OK) return st;
     const long long hn = (long long)n_tiles * C;
     if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
@@ -431,7 +452,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                                                       (long long*)sp->tile_ranges);
     if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
     k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                               bin_rounds(n, n_tiles), w.hoff, cap, sp->entry_splat);
+                                               bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
     if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
     k_flag_overflow<<<1, 32, 0, s>>>(sp->counters, cap);
     if ((st = check_launch("k_flag_overflow")) != XG_OK) return st;

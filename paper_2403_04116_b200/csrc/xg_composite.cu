@@ -1092,6 +1092,10 @@ __device__ __forceinline__ float upstream(const BwdArgs& a, long long o) {
   return a.dl ? a.dl[o] : a.l1_scale * (float)((a.image[o] > a.target[o]) - (a.image[o] < a.target[o]));
 }
 
+#ifdef XG_BWD_STATS
+__device__ unsigned long long g_bwd_stats[6];
+#endif
+
 // speculative reverse batches (unblend_splat_spec)
 #ifndef XG_BWD_SPEC
 #define XG_BWD_SPEC 1
@@ -1132,6 +1136,14 @@ __device__ __forceinline__ void replay_range(const BwdArgs& a, const Unit& u, lo
       }
       exact = __any_sync(0xffffffffu, straddle);
     }
+#ifdef XG_BWD_STATS
+    // (development aid: batches / survivors by path -> xg_debug_bwd_stats)
+    if ((threadIdx.x & 31) == 0) {
+      const int path = general ? 1 : exact ? 0 : 2;
+      atomicAdd(&g_bwd_stats[path], 1ull);
+      atomicAdd(&g_bwd_stats[3 + path], (unsigned long long)cnt);
+    }
+#endif
     if (general)
       unblend_batch<1, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
     else if (exact)
@@ -1720,5 +1732,17 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
                                                            g_conic, g_int, g_alpha);
   return check_launch("k_acc_to_reference");
 }
+
+#ifdef XG_BWD_STATS
+// development aid (XG_BWD_STATS builds only): reverse-replay batches and
+// survivors by path {exact, general, speculative}; reads and clears
+int xg_debug_bwd_stats(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, xg::g_bwd_stats, sizeof(unsigned long long) * 6);
+  static const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(xg::g_bwd_stats, zero, sizeof(zero));
+  return 0;
+}
+#endif
 
 }  // extern "C"

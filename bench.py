@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-views", type=int, default=0, help="0 = one per worker")
     ap.add_argument("--no-train", action="store_true", help="skip the C2 training-iteration block")
-    ap.add_argument("--train-iters-per-step", type=int, default=100)
+    ap.add_argument("--train-iters-per-step", type=int, default=200)  # 5 steps: 1,000 timed iterations
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (1M Gaussians, 1024^2) stress block")
     return ap.parse_args()
 
@@ -557,7 +557,7 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
     iters = per * args.steps
     d, e = out["device"], out["e2e"]
     name = (f"C2: {g}^3-lattice ACUI init ({(2 * (g // 4) + 3) ** 3:,} Gaussians), 50 train views of a "
-            "100-view 512x512 sweep, full iterations incl. densify/prune every 100 (one event per step)"
+            f"100-view 512x512 sweep, full iterations incl. densify/prune every 100 ({per // 100} events per step)"
             if world == 1 else
             f"C5: {(2 * (g // 4) + 3) ** 3:,} Gaussians, 512x512, data-parallel x{world}: one view per GPU per "
             "step, NCCL all-reduce of the 27N gradient bucketed and overlapped with the fused Adam")

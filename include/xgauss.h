@@ -203,6 +203,18 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
 xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
                            int32_t* n_contrib, const float* target, double* l1_sum, void* stream);
 
+/* Training forward: as the tracking xg_composite_fwd (t_final, checkpoints,
+ * fused L1) for a following xg_composite_bwd, but n_contrib is the reverse
+ * replay's start rather than the reference's contributor count: exact for a
+ * pixel whose transmittance fell below the floor, the tile list's length for
+ * a pixel still above it (the entries in between have power < -30).  Its
+ * speculative batches take the image-only step (opacity in the exponent), so
+ * image, t_final and the following xg_composite_bwd's gradients agree with
+ * the xg_composite_fwd path to float32 rounding.  Replaces, for the trainer,
+ * the same _kernels.pyx:23-74 forward as xg_composite_fwd. */
+xg_status xg_composite_fwd_train(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                                 int32_t* n_contrib, const float* target, double* l1_sum, void* stream);
+
 /* K3 over a batch of binned views that share the detector size (image only,
  * e.g. a novel-view sweep): ONE persistent launch with one heaviest-first
  * queue over every (view, tile, quarter) unit, so per-view tails overlap.

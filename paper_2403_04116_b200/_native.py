@@ -99,6 +99,8 @@ SIGNATURES = {
     "xg_preprocess_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "xg_bin_sort": (c_i32, [c_void_p, c_void_p, c_void_p, c_size, c_void_p]),
     "xg_composite_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "xg_composite_fwd_train": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p]),
     "xg_composite_bwd": (
         c_i32,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_f32, c_void_p, c_void_p],

@@ -452,7 +452,13 @@ __host__ __device__ constexpr int min_ctas(int kP) { return kP == 1 ? XG_FWD_MIN
 
 // One sub-block unit of the forward: the warp walks the tile's entry list
 // and writes the sub-block's pixels.
-template <bool kTrack, int kP>
+// kLite (training forward, tracking): speculative batches use the
+// image-only step (no per-pair contributor tracking); a pixel that terminates
+// gets its exact last blended entry from the re-run of the crossing batch, a
+// pixel still above the floor at the end of its list gets the list's last
+// entry - the reverse replay's start (entries past the true last have
+// power < -30, exact no-ops up to < 1e-13 there).
+template <bool kTrack, int kP, bool kLite = false>
 __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int sub, FRec* rec, int* kk) {
   constexpr int kR = 2 * kP;
   const int lane = threadIdx.x & 31;
@@ -520,7 +526,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
         }
 #pragma unroll
         for (int r = 0; r < kR; ++r) L0[r] = last[r];
-        if (kTrack) {
+        if (kTrack && !kLite) {
 #pragma unroll kFwdUnroll
           for (int q = 0; q < cnt; ++q) blend_splat_spec_track<kP>(rec[q], kk[q], u.fx, fy, lv, T, acc, last);
         } else {
@@ -563,6 +569,14 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     for (int i = 0; i < kP; ++i) live |= (T[i].x >= kFloor) || (T[i].y >= kFloor);
     alive = __any_sync(0xffffffffu, live);
   }
+  if (kTrack && kLite) {  // live to the end: replay from the list's last entry
+    const int lend = (int)(u.end - u.start) - 1;
+#pragma unroll
+    for (int i = 0; i < kP; ++i) {
+      if (T[i].x >= kFloor) last[2 * i] = lend;
+      if (T[i].y >= kFloor) last[2 * i + 1] = lend;
+    }
+  }
   float l1 = 0.f;
   int wl = -1;
 #pragma unroll
@@ -602,7 +616,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 
 // Non-persistent single-view variant: one CTA per kWarps / kSubs tiles
 // (heaviest first), one warp per sub-block.
-template <bool kTrack>
+template <bool kTrack, bool kLite = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd_np(FwdArgs a) {
   constexpr int kP = fwd_pairs<kTrack>(), kSubs = 4 / kP;
   __shared__ FRec s_rec[kWarps][32];
@@ -610,10 +624,10 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_com
   const int warp = threadIdx.x >> 5;
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
   const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
-  if (i < a.n_tiles) composite_unit<kTrack, kP>(a, a.order[i], warp % kSubs, s_rec[warp], s_k[warp]);
+  if (i < a.n_tiles) composite_unit<kTrack, kP, kLite>(a, a.order[i], warp % kSubs, s_rec[warp], s_k[warp]);
 }
 
-template <bool kTrack>
+template <bool kTrack, bool kLite = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd(FwdArgs a) {
   constexpr int kP = fwd_pairs<kTrack>();
   __shared__ FRec s_rec[kWarps][32];
@@ -625,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_com
   // (the caller sees XG_ST_ENTRY_OVERFLOW and re-bins the view)
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
   while (next_unit<false, 4 / kP>(a.order, a.work, a.n_tiles, first, tile, sub))
-    composite_unit<kTrack, kP>(a, tile, sub, s_rec[warp], s_k[warp]);
+    composite_unit<kTrack, kP, kLite>(a, tile, sub, s_rec[warp], s_k[warp]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1479,8 +1493,9 @@ using namespace xg;
 
 extern "C" {
 
-xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
-                           int32_t* n_contrib, const float* target, double* l1_sum, void* stream) {
+static xg_status composite_fwd_impl(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                                    int32_t* n_contrib, const float* target, double* l1_sum, void* stream,
+                                    bool lite) {
   if (!cam || !sp || !image || !sp->entry_splat || !sp->tile_ranges || !sp->mean2d || !sp->coef ||
       !sp->inten) {
     set_error_msg("xg_composite_fwd: invalid argument");
@@ -1516,12 +1531,33 @@ xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* ima
     return check_launch("k_composite_fwd");
   }
 #endif
-  if (track_np)
-    k_composite_fwd_np<true><<<div_up(n_tiles, kWarps * kFwdTrackPairs / 4), kThreads, 0, (cudaStream_t)stream>>>(a);
+  const int np_grid = div_up(n_tiles, kWarps * kFwdTrackPairs / 4);
+  if (lite && track_np)
+    k_composite_fwd_np<true, true><<<np_grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+  else if (lite)
+    k_composite_fwd<true, true><<<persistent_grid(k_composite_fwd<true, true>, 4 / kFwdTrackPairs * n_tiles,
+                                                  "XG_FWD_CTAS_PER_SM"),
+                                  kThreads, 0, (cudaStream_t)stream>>>(a);
+  else if (track_np)
+    k_composite_fwd_np<true><<<np_grid, kThreads, 0, (cudaStream_t)stream>>>(a);
   else
     k_composite_fwd<true><<<persistent_grid(k_composite_fwd<true>, 4 / kFwdTrackPairs * n_tiles, "XG_FWD_CTAS_PER_SM"),
                             kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_fwd");
+}
+
+xg_status xg_composite_fwd(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                           int32_t* n_contrib, const float* target, double* l1_sum, void* stream) {
+  return composite_fwd_impl(cam, sp, image, t_final, n_contrib, target, l1_sum, stream, false);
+}
+
+xg_status xg_composite_fwd_train(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                                 int32_t* n_contrib, const float* target, double* l1_sum, void* stream) {
+  if (!t_final || !n_contrib) {
+    set_error_msg("xg_composite_fwd_train: t_final and n_contrib are required");
+    return XG_ERR_INVALID;
+  }
+  return composite_fwd_impl(cam, sp, image, t_final, n_contrib, target, l1_sum, stream, true);
 }
 
 size_t xg_composite_batch_workspace_bytes(const xg_camera* cam, int32_t n_views) {

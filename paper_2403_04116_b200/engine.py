@@ -157,22 +157,26 @@ class Frame:
         )
 
     def composite(self, target: torch.Tensor | None = None, l1_sum: torch.Tensor | None = None,
-                  image_out: torch.Tensor | None = None, track: bool = True) -> None:
+                  image_out: torch.Tensor | None = None, track: bool = True, train: bool = False) -> None:
         """K3.  ``image_out`` (float32 [H, W], contiguous) receives the image
         instead of the frame's own buffer (e.g. a slot of a sweep stack).
         ``track=False`` (inference) skips the per-pixel final transmittance
-        and contributor counts the backward needs."""
+        and contributor counts the backward needs.  ``train=True`` (the
+        trainer) is the tracking forward whose n_contrib is only the reverse
+        replay's start (``xg_composite_fwd_train``), not the reference's
+        contributor count."""
         if track and self.replay_ckpt is None:
             self._alloc_replay()
         sp = self.splats_struct()
         img = self.image if image_out is None else image_out
+        fn = "xg_composite_fwd_train" if (track and train) else "xg_composite_fwd"
         nat.check(
-            nat.lib().xg_composite_fwd(
+            getattr(nat.lib(), fn)(
                 ctypes.byref(self.cam), ctypes.byref(sp), img.data_ptr(),
                 self.t_final.data_ptr() if track else None, self.n_contrib.data_ptr() if track else None,
                 nat.ptr(target, "target"), nat.ptr(l1_sum, "l1_sum"), nat.stream(),
             ),
-            "xg_composite_fwd",
+            fn,
         )
         self.has_forward = track
         self.fwd_image = img  # the image the backward (fused L1, replay restarts) reads

@@ -171,7 +171,7 @@ class DataParallelTrainer:
             t.tgt_dev.copy_(tgt, non_blocking=True)
             tgt = t.tgt_dev
         eng.l1.zero_()
-        fr.composite(target=tgt, l1_sum=eng.l1)
+        fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
                     l1_scale=1.0 / (t.h * t.w), stats=t.stats)
         lr = _lr_array({"positions": position_learning_rate(cfg, it - 1), "rotations": cfg.lr_rotation,

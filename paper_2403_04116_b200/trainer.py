@@ -397,7 +397,7 @@ class Trainer:
         else:
             tgt = self.targets[view]
         eng.l1.zero_()
-        fr.composite(target=tgt, l1_sum=eng.l1)
+        fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         if self.targets_on_host:
             self.loss_host.copy_(eng.l1, non_blocking=True)  # the step's scalar result, to the host
         value = None

@@ -147,6 +147,51 @@ def test_backward_parity(golden, runs, xg):
         assert ok, (name, "screen_norms", rel)
 
 
+def test_training_forward(golden, runs, xg):
+    """The trainer's forward (xg_composite_fwd_train): image / t_final equal
+    the exact tracking forward to float32 rounding; n_contrib is the exact
+    count for terminated pixels and the tile length for the rest; the reverse
+    replay from it gives the reference's gradients."""
+    import torch
+
+    n_term = 0
+    for name, (cloud, proj, sp, ref, cam) in runs.items():
+        p = name + "/"
+        fr = sp.frame
+        if sp.n_active == 0:
+            continue
+        fr.composite()  # exact tracking forward (render()'s)
+        img0, tf0, nc0 = fr.image.clone(), fr.t_final.clone(), fr.n_contrib.clone()
+        fr.composite(train=True)
+        torch.cuda.synchronize()
+        scale = float(img0.abs().max())
+        assert bool(((fr.image - img0).abs() <= 2e-5 * img0.abs() + 1e-7 * scale).all()), name
+        assert bool(((fr.t_final - tf0).abs() <= 2e-5 * tf0.abs() + 1e-9).all()), name
+        term = tf0 < 1e-4
+        n_term += int(term.sum())
+        assert torch.equal(fr.n_contrib[term], nc0[term]), name
+        h, w = fr.h, fr.w
+        ntx = (w + 15) // 16
+        yy, xx = torch.meshgrid(torch.arange(h, device="cuda"), torch.arange(w, device="cuda"), indexing="ij")
+        rng = sp.tile_ranges[(yy // 16) * ntx + xx // 16]
+        length = (rng[..., 1] - rng[..., 0]).to(torch.int32)
+        assert torch.equal(fr.n_contrib[~term], length[~term]), name
+        assert bool((fr.n_contrib >= nc0).all()), name
+        n = cloud.n_points
+        kg = {k: torch.zeros(s_, dtype=torch.float64, device="cuda")
+              for k, s_ in (("g_mean", (n, 2)), ("g_conic", (n, 3)), ("g_int", n), ("g_alpha", n))}
+        xg.render_backward(cloud, sp, torch.as_tensor(golden[p + "dl"]), kernel_grads=kg)
+        torch.cuda.synchronize()
+        act = np.flatnonzero(ref["pre"]["active"])
+        refs = {k: golden[p + "k_" + k] for k in ("g_mean", "g_conic", "g_int", "g_alpha")}
+        floor = 1e-3 * max(np.abs(v).max() for v in refs.values())
+        for k, want in refs.items():
+            ok, rel = normwise_ok(kg[k].cpu().numpy()[act], want, floor)
+            assert ok, (name, k, rel)
+        fr.composite()  # leave the exact forward for the other tests
+    assert n_term > 0  # the golden set has terminating pixels
+
+
 def test_plugin_forward_backward_tiles(golden, xg):
     """The reference's kernel-backend contract served by xg_forward_tiles /
     xg_backward_tiles, fed the reference's own SplatList arrays."""

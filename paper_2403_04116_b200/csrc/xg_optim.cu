@@ -57,17 +57,25 @@ struct AdamArgs {
 // while the next bucket is still being all-reduced.
 __global__ void k_adam(AdamArgs a) {
   const uint32_t bad = a.status ? (a.status[0] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f : 0u;
+  const float b1 = (float)a.b1, b2 = (float)a.b2, omb1 = (float)(1.0 - a.b1), omb2 = (float)(1.0 - a.b2);
+  const float bc1 = (float)a.bc1, bc2 = (float)a.bc2, eps = (float)a.eps;
+  float lrf[kFields];
+#pragma unroll
+  for (int k = 0; k < kFields; ++k) lrf[k] = (float)a.lr[k];
   for (long long e = a.begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < a.end;
        e += (long long)gridDim.x * blockDim.x) {
     const int f = (e >= a.bound[0]) + (e >= a.bound[1]) + (e >= a.bound[2]) + (e >= a.bound[3]);
     if (bad & ((2u << f) - 1u)) continue;  // a field <= f diverged (the reference raises there)
-    const double g = a.g[e];
-    double m = a.m[e], v = a.v[e];
-    m = a.b1 * m + (1.0 - a.b1) * g;
-    v = a.b2 * v + (1.0 - a.b2) * g * g;
-    a.m[e] = (float)m;
-    a.v[e] = (float)v;
-    a.p[e] = (float)((double)a.p[e] - a.lr[f] * (m / a.bc1) / (sqrt(v / a.bc2) + a.eps));
+    // float32 arithmetic (IEEE division and square root): the moments are
+    // stored in float32 anyway, and the update differs from the reference's
+    // float64 evaluation by a few ulp of the (lr-scaled) step only
+    const float g = a.g[e];
+    float m = a.m[e], v = a.v[e];
+    m = __fmaf_rn(b1, m, __fmul_rn(omb1, g));
+    v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(omb2, g), g));
+    a.m[e] = m;
+    a.v[e] = v;
+    a.p[e] = a.p[e] - lrf[f] * __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps));
   }
 }
 

@@ -161,8 +161,14 @@ static_assert(kBinThreads * kBinMaxRounds < 65536, "k_bin_emit keeps per-tile lo
 // T offsets), so the chunk grows with the tile count: ~3 CTAs per SM for
 // T <= 1024 (small training clouds still fill the GPU), ~2 waves of one
 // CTA per SM (128 KB of counters) at T = 4096.
+#ifndef XG_BIN_CTAS_SMALL_T
+#define XG_BIN_CTAS_SMALL_T 444
+#endif
+#ifndef XG_BIN_CTAS_LARGE_T
+#define XG_BIN_CTAS_LARGE_T 296
+#endif
 inline int bin_rounds(int64_t n, int n_tiles) {
-  const int64_t ctas = n_tiles > 1024 ? 296 : 444;
+  const int64_t ctas = n_tiles > 1024 ? XG_BIN_CTAS_LARGE_T : XG_BIN_CTAS_SMALL_T;
   const int64_t r = (n + (int64_t)kBinThreads * ctas - 1) / ((int64_t)kBinThreads * ctas);
   const int cap = n_tiles > 1024 ? kBinMaxRounds : 4;
   return r < 1 ? 1 : (r > cap ? cap : (int)r);

@@ -351,6 +351,41 @@ __device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit&
   return __popc(bal);
 }
 
+// Split-half compaction (image-only, whole-tile warps): every entry is culled
+// against both 16x8 halves; half h's survivors go to s_rec[32 h ..] in entry
+// order, and the shorter list is padded with null splats (A2 = B2 = C2 = 0,
+// alpha = 0, log2 alpha = -inf: sigma = 0, an exact no-op in every blend
+// variant) to the longer one's length, which is returned.  Lanes 0-15 then
+// walk the top list, lanes 16-31 the bottom one: the cull granularity of
+// 16x8 sub-blocks with the per-splat column work shared by 8 pixels a lane.
+__device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, FRec* s_rec, bool& general) {
+  FRec r;
+  bool k0 = false, k1 = false, gen = false;
+  if (raw.valid) {
+    const float mx = (float)(raw.m.x - (double)u.x0), my = (float)(raw.m.y - (double)u.y0);
+    const float A = raw.c.x, B = raw.c.y, C = raw.c.z, alpha = raw.c.w;
+    k0 = overlaps(mx, my, A, B, C, u.xa, u.xb, 0.f, (float)(kTile / 2 - 1));
+    k1 = overlaps(mx, my, A, B, C, u.xa, u.xb, (float)(kTile / 2), (float)(kTile - 1));
+    gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
+    r.a = make_float4(mx, -my, A, B);
+    r.b = make_float4(C, -alpha, -raw.it, __log2f(alpha));
+  }
+  const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+  general = __any_sync(0xffffffffu, (k0 || k1) && gen);
+  const unsigned lt = lanemask_lt();
+  if (k0) s_rec[__popc(b0 & lt)] = r;
+  if (k1) s_rec[32 + __popc(b1 & lt)] = r;
+  const int c0 = __popc(b0), c1 = __popc(b1), n = c0 > c1 ? c0 : c1;
+  const int lane = threadIdx.x & 31;
+  FRec z;
+  z.a = make_float4(0.f, 0.f, 0.f, 0.f);
+  z.b = make_float4(0.f, 0.f, 0.f, -INFINITY);
+  if (lane >= c0 && lane < n) s_rec[lane] = z;
+  if (lane >= c1 && lane < n) s_rec[32 + lane] = z;
+  __syncwarp();
+  return n;
+}
+
 // Image-only speculative step (no per-pair tests; see composite_unit): the
 // opacity rides in the exponent, sigma = 2^(p2 + log2 alpha) (record b.w),
 // so a pair costs FADD2 dy, 2 FFMA2 p2, 2 MUFU.EX2, FMUL2 sigma T, FFMA2 acc,
@@ -423,7 +458,8 @@ __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int 
 #endif
 // pixel pairs per lane (make_sub): image-only launches / tracking launches
 #ifndef XG_FWD_PAIRS
-#define XG_FWD_PAIRS 2  // measured at C3: 1 -> 2 pairs +5 % fps, 4 pairs -6 %
+#define XG_FWD_PAIRS 4  // whole-tile warps with split-half entry lists (XG_FWD_SPLIT); measured before the
+                        // split: 1 -> 2 pairs +5 % fps, 4 pairs (one 16x16 cull) -6 %
 #endif
 #ifndef XG_FWD_TRACK_PAIRS
 #define XG_FWD_TRACK_PAIRS 1  // (C2 training: quarter tiles balance better; 2 pairs +5 % per iteration)
@@ -443,6 +479,16 @@ constexpr bool kSpec = XG_FWD_SPEC != 0;
 #define XG_FWD_SPEC_TRACK 1
 #endif
 constexpr bool kSpecTrack = XG_FWD_SPEC_TRACK != 0;
+// image-only launches: one warp per 16x16 tile (4 pixel pairs per lane),
+// each 16x8 half with its own culled entry list (compact_fwd_split)
+#ifndef XG_FWD_SPLIT
+#define XG_FWD_SPLIT 1  // vs 16x8 sub-block warps: C3 within noise (+0.3 %), C4 +3.5 %
+#endif
+constexpr bool kFwdSplit = XG_FWD_SPLIT != 0;
+static_assert(!kFwdSplit || kFwdPairs == 4, "split-half units cover whole tiles (XG_FWD_PAIRS=4)");
+// split path: two 32-record lists + the batch-start (T, acc) of the lane's
+// 8 pixels kept in shared memory for a re-run (frees 16 registers)
+constexpr int kRecPerWarp = kFwdSplit ? 128 : 32;
 static_assert((kFwdPairs == 1 || kFwdPairs == 2 || kFwdPairs == 4) &&
                   (kFwdTrackPairs == 1 || kFwdTrackPairs == 2 || kFwdTrackPairs == 4) && kWarps % 4 == 0,
               "sub-blocks of 4, 8 or 16 rows; CTAs of whole tiles");
@@ -461,7 +507,9 @@ __host__ __device__ constexpr int min_ctas(int kP) { return kP == 1 ? XG_FWD_MIN
 template <bool kTrack, int kP, bool kLite = false>
 __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int sub, FRec* rec, int* kk) {
   constexpr int kR = 2 * kP;
+  constexpr bool kSplitPath = !kTrack && kSpec && kFwdSplit && kP == 4;
   const int lane = threadIdx.x & 31;
+  FRec* const rh = kSplitPath ? rec + 32 * (lane >> 4) : rec;  // this lane's (half's) entry list
   const Unit u = make_sub<kP>(tile, sub, a.ntx, a.w, a.h, a.ranges);
   float2 fy[kP], T[kP], acc[kP], Tf[kP];  // Tf: final T of a pixel parked at T = 0 (tracking + speculation)
   int last[kR];
@@ -497,7 +545,8 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     }
     const Raw cur = nxt;
     bool general;
-    const int cnt = compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
+    const int cnt = kSplitPath ? compact_fwd_split(cur, u, rec, general)
+                               : compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
     if (!(kTrack ? kSpecTrack : kSpec)) {
@@ -517,10 +566,15 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
         float2 T0[kP], A0[kP];
         int L0[kR];
         bool lv[kR];
+        float4* const sv = reinterpret_cast<float4*>(rec + 64) + lane;  // (split path only)
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
-          T0[i] = T[i];
-          A0[i] = acc[i];
+          if (kSplitPath) {
+            sv[32 * i] = make_float4(T[i].x, T[i].y, acc[i].x, acc[i].y);
+          } else {
+            T0[i] = T[i];
+            A0[i] = acc[i];
+          }
           lv[2 * i] = T[i].x >= kFloor;
           lv[2 * i + 1] = T[i].y >= kFloor;
         }
@@ -530,18 +584,24 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 #pragma unroll kFwdUnroll
           for (int q = 0; q < cnt; ++q) blend_splat_spec_track<kP>(rec[q], kk[q], u.fx, fy, lv, T, acc, last);
         } else {
-          blend_batch_spec<kP>(rec, cnt, u.fx, fy, T, acc);
+          blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);
         }
         bool crossed = false;
 #pragma unroll
         for (int i = 0; i < kP; ++i)
-          crossed |= (T[i].x < kFloor && T0[i].x >= kFloor) || (T[i].y < kFloor && T0[i].y >= kFloor);
+          crossed |= (T[i].x < kFloor && lv[2 * i]) || (T[i].y < kFloor && lv[2 * i + 1]);
         redo = __any_sync(0xffffffffu, crossed);
         if (redo) {
 #pragma unroll
           for (int i = 0; i < kP; ++i) {
-            T[i] = T0[i];
-            acc[i] = A0[i];
+            if (kSplitPath) {
+              const float4 x = sv[32 * i];
+              T[i] = make_float2(x.x, x.y);
+              acc[i] = make_float2(x.z, x.w);
+            } else {
+              T[i] = T0[i];
+              acc[i] = A0[i];
+            }
           }
 #pragma unroll
           for (int r = 0; r < kR; ++r) last[r] = L0[r];
@@ -549,9 +609,9 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
       }
       if (redo) {
         if (general)
-          blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+          blend_batch<true, kTrack, kP>(rh, kk, cnt, u.fx, fy, T, acc, last);
         else
-          blend_batch<false, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
+          blend_batch<false, kTrack, kP>(rh, kk, cnt, u.fx, fy, T, acc, last);
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
           if (kTrack) {
@@ -619,7 +679,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 template <bool kTrack, bool kLite = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd_np(FwdArgs a) {
   constexpr int kP = fwd_pairs<kTrack>(), kSubs = 4 / kP;
-  __shared__ FRec s_rec[kWarps][32];
+  __shared__ FRec s_rec[kWarps][kRecPerWarp];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
@@ -630,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_com
 template <bool kTrack, bool kLite = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd(FwdArgs a) {
   constexpr int kP = fwd_pairs<kTrack>();
-  __shared__ FRec s_rec[kWarps][32];
+  __shared__ FRec s_rec[kWarps][kRecPerWarp];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
   int tile, sub;
@@ -693,7 +753,7 @@ __device__ __forceinline__ bool next_batch_unit(const BatchArgs& b, bool& first,
 }
 
 __global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd_batch(BatchArgs b) {
-  __shared__ FRec s_rec[kWarps][32];
+  __shared__ FRec s_rec[kWarps][kRecPerWarp];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
   int view, tile, quad;
@@ -714,7 +774,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd
 // whole launch.
 __global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd_batch_np(BatchArgs b) {
   constexpr int kSubs = 4 / kFwdPairs;
-  __shared__ FRec s_rec[kWarps][32];
+  __shared__ FRec s_rec[kWarps][kRecPerWarp];
   __shared__ int s_k[kWarps][32];
   const int warp = threadIdx.x >> 5;
   const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;

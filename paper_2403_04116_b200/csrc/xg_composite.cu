@@ -46,6 +46,12 @@ constexpr int kCkShift = log2_exact(XG_REPLAY_CHUNK);
 constexpr int kCk = 1 << kCkShift;
 static_assert(kCk == XG_REPLAY_CHUNK && kCk % 32 == 0, "checkpoints sit on 32-entry batch boundaries");
 constexpr float kCullMargin = 0.05f;
+// image-only split path: the multiplicative row recurrence for
+// recurrence-safe batches (blend_splat_spec_rec)
+#ifndef XG_FWD_RECUR
+#define XG_FWD_RECUR 1
+#endif
+constexpr bool kFwdRecur = XG_FWD_RECUR != 0;
 // kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
 // safety margin for the MUFU.EX2 error the clamp logic is compiled out.
 constexpr float kNoClampAlpha = 0.98999f;
@@ -358,20 +364,50 @@ __device__ __forceinline__ int compact_fwd(const Raw& raw, int krel, const Unit&
 // variant) to the longer one's length, which is returned.  Lanes 0-15 then
 // walk the top list, lanes 16-31 the bottom one: the cull granularity of
 // 16x8 sub-blocks with the per-splat column work shared by 8 pixels a lane.
-__device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, FRec* s_rec, bool& general) {
+// p2 + log2 alpha at a tile-relative pixel (the recurrence-safety test)
+__device__ __forceinline__ float p2_at(float mx, float my, float A, float B, float C, float la, float x, float y) {
+  const float dx = x - mx, dy = y - my;
+  return fmaf(fmaf(C, dy, B * dx), dy, fmaf(A * dx, dx, la));
+}
+
+__device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, FRec* s_rec, bool& general,
+                                                 bool& rec_safe) {
   FRec r;
-  bool k0 = false, k1 = false, gen = false;
+  bool k0 = false, k1 = false, gen = false, unsafe = false;
   if (raw.valid) {
     const float mx = (float)(raw.m.x - (double)u.x0), my = (float)(raw.m.y - (double)u.y0);
     const float A = raw.c.x, B = raw.c.y, C = raw.c.z, alpha = raw.c.w;
+    const float la = __log2f(alpha);
     k0 = overlaps(mx, my, A, B, C, u.xa, u.xb, 0.f, (float)(kTile / 2 - 1));
     k1 = overlaps(mx, my, A, B, C, u.xa, u.xb, (float)(kTile / 2), (float)(kTile - 1));
     gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
     r.a = make_float4(mx, -my, A, B);
-    r.b = make_float4(C, -alpha, -raw.it, __log2f(alpha));
+    r.b = make_float4(C, -alpha, -raw.it, la);
+    if (kFwdRecur && (k0 || k1)) {
+      // the multiplicative row recurrence (blend_splat_spec_rec) of half h
+      // starts from E_0 = 2^p2 at rows 8h, 8h + 1: those must be normal
+      // floats (the concave p2 is smallest at a corner of that 16 x 2 strip);
+      // later rows may underflow harmlessly (their true sigma is even
+      // smaller).  The ratios 2^(p2(dy + 2) - p2(dy)), linear in (dx, dy),
+      // and 2^(8 C2) must stay within 2^+-120.
+      constexpr float e = (float)(kTile - 1), hh = (float)(kTile / 2);
+      const float mdx = fmaxf(fabsf(mx), fabsf(e - mx)), mdy = fmaxf(fabsf(my), fabsf(e - my));
+      const float dmax = 4.f * fabsf(C) * mdy + fabsf(4.f * C) + 2.f * fabsf(B) * mdx;
+      unsafe = !(dmax <= 120.f) || !(C >= -15.f);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h ? k1 : k0) {
+          const float y0 = h * hh, y1 = y0 + 1.f;
+          const float pmin = fminf(fminf(p2_at(mx, my, A, B, C, la, 0.f, y0), p2_at(mx, my, A, B, C, la, e, y0)),
+                                   fminf(p2_at(mx, my, A, B, C, la, 0.f, y1), p2_at(mx, my, A, B, C, la, e, y1)));
+          unsafe |= !(pmin >= -125.f);
+        }
+      }
+    }
   }
   const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
   general = __any_sync(0xffffffffu, (k0 || k1) && gen);
+  rec_safe = kFwdRecur && !__any_sync(0xffffffffu, unsafe);
   const unsigned lt = lanemask_lt();
   if (k0) s_rec[__popc(b0 & lt)] = r;
   if (k1) s_rec[32 + __popc(b1 & lt)] = r;
@@ -408,6 +444,39 @@ __device__ __forceinline__ void blend_splat_spec(const FRec& r, float fx, const 
     const float2 w = __fmul2_rn(e, T[i]);
     acc[i] = __ffma2_rn(bc(ni), w, acc[i]);
     T[i] = __ffma2_rn(make_float2(-e.x, -e.y), T[i], T[i]);
+  }
+}
+
+// Speculative step with the multiplicative row recurrence (split-half
+// whole-tile warps, 4 pixel pairs per lane, rows dy0 + 0 .. 7): along a
+// column, p2(dy + 2) - p2(dy) = 4 C2 dy + 4 C2 + 2 B2 dx is linear in dy, so
+//   E_{i+1} = E_i * S_i,  S_{i+1} = S_i * 2^(8 C2)
+// with E_0 = 2^p2 of rows 0, 1 and S_0 = 2^(p2(dy0 + 2) - p2(dy0)) of rows
+// 0, 1: 5 MUFU.EX2 per splat and lane instead of 8 (the kernel is EX2-bound).
+// Every factor stays within 2^+-120 (the compaction's rec_safe test);
+// relative error a few ulp after the 3 products.
+__device__ __forceinline__ void blend_splat_spec_rec(const FRec& r, float fx, const float2 (&fy)[4], float2 (&T)[4],
+                                                     float2 (&acc)[4]) {
+  const float dx = __fsub_rn(fx, r.a.x);
+  const float adx2 = __fmaf_rn(__fmul_rn(r.a.z, dx), dx, r.b.w);
+  const float bdx = __fmul_rn(r.a.w, dx);
+  const float C = r.b.x, ni = -r.b.z;
+  const float c4 = 4.f * C;
+  const float q4 = ex2_approx(8.f * C);
+  const float2 dy0 = __fadd2_rn(fy[0], bc(r.a.y));
+  const float2 p0 = __ffma2_rn(__ffma2_rn(bc(C), dy0, bc(bdx)), dy0, bc(adx2));
+  const float2 d0 = __ffma2_rn(bc(c4), dy0, bc(__fmaf_rn(2.f, bdx, c4)));
+  float2 E = make_float2(ex2_approx(p0.x), ex2_approx(p0.y));
+  float2 S = make_float2(ex2_approx(d0.x), ex2_approx(d0.y));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i > 0) {
+      E = __fmul2_rn(E, S);
+      S = __fmul2_rn(S, bc(q4));
+    }
+    const float2 w = __fmul2_rn(E, T[i]);
+    acc[i] = __ffma2_rn(bc(ni), w, acc[i]);
+    T[i] = __ffma2_rn(make_float2(-E.x, -E.y), T[i], T[i]);
   }
 }
 
@@ -545,7 +614,8 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     }
     const Raw cur = nxt;
     bool general;
-    const int cnt = kSplitPath ? compact_fwd_split(cur, u, rec, general)
+    bool rec_safe = false;
+    const int cnt = kSplitPath ? compact_fwd_split(cur, u, rec, general, rec_safe)
                                : compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
@@ -584,7 +654,16 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 #pragma unroll kFwdUnroll
           for (int q = 0; q < cnt; ++q) blend_splat_spec_track<kP>(rec[q], kk[q], u.fx, fy, lv, T, acc, last);
         } else {
-          blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);
+          if constexpr (kSplitPath) {
+            if (rec_safe) {
+#pragma unroll 2
+              for (int q = 0; q < cnt; ++q) blend_splat_spec_rec(rh[q], u.fx, fy, T, acc);
+            } else {
+              blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);
+            }
+          } else {
+            blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);
+          }
         }
         bool crossed = false;
 #pragma unroll

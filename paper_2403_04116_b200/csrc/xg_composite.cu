@@ -52,6 +52,10 @@ constexpr float kCullMargin = 0.05f;
 #define XG_FWD_RECUR 1
 #endif
 constexpr bool kFwdRecur = XG_FWD_RECUR != 0;
+#ifndef XG_FWD_REC_UNROLL
+#define XG_FWD_REC_UNROLL 4  // measured: 1 -0.8 %, 2, 4 +0.5 % (C3) / +1.4 % (C4)
+#endif
+constexpr int kRecUnroll = XG_FWD_REC_UNROLL;
 // kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
 // safety margin for the MUFU.EX2 error the clamp logic is compiled out.
 constexpr float kNoClampAlpha = 0.98999f;
@@ -656,7 +660,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
         } else {
           if constexpr (kSplitPath) {
             if (rec_safe) {
-#pragma unroll 2
+#pragma unroll kRecUnroll
               for (int q = 0; q < cnt; ++q) blend_splat_spec_rec(rh[q], u.fx, fy, T, acc);
             } else {
               blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);

@@ -220,6 +220,40 @@ def _random_fields(rng, n, opacity, scale_lo, scale_hi, aniso):
         "features": rng.normal(scale=0.5, size=(n, 4))}.items()}
 
 
+def test_image_only_narrow_and_wide_splats(xg):
+    """Sub-pixel splats (anchor rows of the row recurrence underflowing: its
+    direct-EX2 fallback) mixed with wide ones, through the image-only sweep
+    launches, against the float32 oracle."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    n = 600
+    f = _random_fields(rng, n, rng.uniform(0.05, 0.9, size=n), 0.02, 0.2, 1.0)
+    wide = _random_fields(rng, n, rng.uniform(0.05, 0.5, size=n), 1.0, 6.0, 1.0)
+    f = {k: np.concatenate([f[k], wide[k]]) for k in f}
+    basis = np.ones(4, np.float32)
+    cloud = xg.GaussianCloud(**f, basis_weights=basis, device="cuda")
+    d = 128
+    sc = xg.ScannerConfig(L_SO, L_SD, d, d, 1.0)
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    for phi in (0.0, 0.9):
+        cam = orc.camera_from_view(L_SO, L_SD, d, d, 1.0, phi)
+        pre = orc.preprocess(f, basis, cam)
+        fwd = orc.composite_fwd(pre, orc.bin_entries(pre, cam), d, d)
+        c = pre["coef"][np.flatnonzero(pre["active"])]
+        # near the +0.3 px^2 low-pass limit (C2 >= -2.4): a survivor of a 16 x 8
+        # half whose anchor rows lie ~8 px away has p2 < -125 there, so such
+        # batches take the direct EX2 path
+        assert (c[:, 2] < -2.0).sum() > 50
+        o = fwd["image"].astype(np.float64)
+        scale = max(np.abs(o).max(), 1e-30)
+        v = SweepRenderer(cloud, sc, batch=2).render(np.array([phi, phi]))
+        torch.cuda.synchronize()
+        for img in v.cpu().numpy().astype(np.float64):
+            assert np.all(np.abs(img - o) <= 2e-5 * np.abs(o) + 1e-7 * scale), (phi, np.abs(img - o).max())
+
+
 @pytest.mark.parametrize("case", ["clamp", "ill_conditioned", "mixed"])
 def test_general_blend_paths(xg, case):
     """Scenes that force the kernels' general variants - sigma clamped at 0.99
@@ -258,6 +292,16 @@ def test_general_blend_paths(xg, case):
     general = ~(alpha < np.float32(0.98999)) | ~((A < 0) & (C < 0) & (det >= np.float32(1e-6) * tr * tr))
     assert general.mean() > 0.1, (case, general.mean())
     _check_forward(case, proj, sp, pre, binned, fwd)
+    # the image-only launches (sweep: split-half lists, speculative batches,
+    # row recurrence with its safety fallback) on the same scene
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    o = fwd["image"].astype(np.float64)
+    scale = max(np.abs(o).max(), 1e-30)
+    for batch in (1, 2):
+        for v in SweepRenderer(cloud, sc, batch=batch).render(np.array([phi] * batch)).cpu().numpy():
+            v = v.astype(np.float64)
+            assert np.all(np.abs(v - o) <= 2e-5 * np.abs(o) + 1e-7 * scale), (case, batch, np.abs(v - o).max())
     dl = rng.normal(size=(d, d)) / (d * d)
     kg = {k: torch.zeros(s, dtype=torch.float64, device="cuda")
           for k, s in (("g_mean", (n, 2)), ("g_conic", (n, 3)), ("g_int", n), ("g_alpha", n))}

@@ -52,6 +52,9 @@ constexpr float kCullMargin = 0.05f;
 #define XG_FWD_RECUR 1
 #endif
 constexpr bool kFwdRecur = XG_FWD_RECUR != 0;
+#ifdef XG_BWD_STATS
+__device__ unsigned long long g_fwd_stats[4];  // (development aid) recurrence / direct batches, survivors
+#endif
 #ifndef XG_FWD_REC_UNROLL
 #define XG_FWD_REC_UNROLL 4  // measured: 1 -0.8 %, 2, 4 +0.5 % (C3) / +1.4 % (C4)
 #endif
@@ -659,6 +662,12 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
           for (int q = 0; q < cnt; ++q) blend_splat_spec_track<kP>(rec[q], kk[q], u.fx, fy, lv, T, acc, last);
         } else {
           if constexpr (kSplitPath) {
+#ifdef XG_BWD_STATS
+            if (lane == 0) {
+              atomicAdd(&g_fwd_stats[rec_safe ? 0 : 1], 1ull);
+              atomicAdd(&g_fwd_stats[rec_safe ? 2 : 3], (unsigned long long)cnt);
+            }
+#endif
             if (rec_safe) {
 #pragma unroll kRecUnroll
               for (int q = 0; q < cnt; ++q) blend_splat_spec_rec(rh[q], u.fx, fy, T, acc);
@@ -1915,6 +1924,14 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
 #ifdef XG_BWD_STATS
 // development aid (XG_BWD_STATS builds only): reverse-replay batches and
 // survivors by path {exact, general, speculative}; reads and clears
+int xg_debug_fwd_stats(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, xg::g_fwd_stats, sizeof(unsigned long long) * 4);
+  static const unsigned long long zero[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(xg::g_fwd_stats, zero, sizeof(zero));
+  return 0;
+}
+
 int xg_debug_bwd_stats(unsigned long long* out) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, xg::g_bwd_stats, sizeof(unsigned long long) * 6);

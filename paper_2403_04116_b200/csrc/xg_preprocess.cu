@@ -183,7 +183,14 @@ __device__ __forceinline__ double intensity_of(const CloudPtrs& c, long long i, 
   return det_sigmoid(acc);
 }
 
-__global__ void k_preprocess(CloudPtrs c, Cam k, xg_splats sp, xg_splat_extras ex) {
+#ifndef XG_PRE_MIN_CTAS
+#define XG_PRE_MIN_CTAS 1
+#endif
+#ifndef XG_PRE_BWD_MIN_CTAS
+#define XG_PRE_BWD_MIN_CTAS 1
+#endif
+__global__ void __launch_bounds__(128, XG_PRE_MIN_CTAS) k_preprocess(CloudPtrs c, Cam k, xg_splats sp,
+                                                                     xg_splat_extras ex) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned status = 0;
   bool active = false;
@@ -297,7 +304,7 @@ struct BwdOut {
   uint32_t* counters;
 };
 
-__global__ void k_preprocess_bwd(CloudPtrs c, Cam k, xg_splats sp, const float* __restrict__ acc,
+__global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(CloudPtrs c, Cam k, xg_splats sp, const float* __restrict__ acc,
                                  BwdOut o) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned bad = 0;

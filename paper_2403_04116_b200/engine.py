@@ -186,6 +186,35 @@ class Frame:
         self.last_counters = c
         return int(c[nat.XG_CTR_ACTIVE]), int(c[nat.XG_CTR_ENTRIES]), int(c[nat.XG_CTR_STATUS])
 
+    def bin_async(self) -> None:
+        """bin(), then an asynchronous copy of the counters to pinned host
+        memory; ``finish_bin`` waits for it.  Lets a caller queue the
+        forward (which skips itself on the device after an entry overflow)
+        before the host reads the entry count - no GPU idle at the sync."""
+        self.bin()
+        if getattr(self, "_cnt_host", None) is None:
+            self._cnt_host = torch.empty(self.counters.shape, dtype=self.counters.dtype, pin_memory=True)
+            self._cnt_event = torch.cuda.Event()
+        self._cnt_host.copy_(self.counters, non_blocking=True)
+        self._cnt_event.record()
+
+    def finish_bin(self) -> bool:
+        """Wait for ``bin_async``'s counters (kept in ``last_counters``); on an
+        entry-buffer overflow re-bin with the exact capacity and return True -
+        work queued in between saw the overflow flag and did nothing, so the
+        caller re-runs it."""
+        self._cnt_event.synchronize()
+        c = self._cnt_host.numpy().astype("int64") & 0xFFFFFFFF
+        self.last_counters = c
+        entries, status = int(c[nat.XG_CTR_ENTRIES]), int(c[nat.XG_CTR_STATUS])
+        if entries <= self.entry_capacity:
+            return False
+        self.set_capacity(int(entries * 1.25) + 1024)
+        self.counters[nat.XG_CTR_STATUS] = status & ~nat.XG_ST_ENTRY_OVERFLOW
+        self.bin()
+        self.read_counters()
+        return True
+
     def ensure_binned(self, check_status: bool = True) -> tuple[int, int, int]:
         """bin(), then one sync to read (active, entries, status); re-bin with
         the exact capacity if the entry buffer overflowed.  All eight

@@ -387,10 +387,10 @@ class Trainer:
         view = self.order.pop()
         fr = eng.frame
         fr.preprocess(self.cloud, self.cams[view])
-        fr.ensure_binned(check_status=False)
-        c = fr.last_counters
-        nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))  # divergence of the previous step
-        nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
+        # the forward is queued before the host reads the binning counters
+        # (it skips itself on the device after an entry overflow, then runs
+        # again on the re-binned lists), so the GPU never waits on the sync
+        fr.bin_async()
         if self.targets_on_host:
             self.tgt_dev.copy_(self.targets[view], non_blocking=True)
             tgt = self.tgt_dev
@@ -398,6 +398,12 @@ class Trainer:
             tgt = self.targets[view]
         eng.l1.zero_()
         fr.composite(target=tgt, l1_sum=eng.l1, train=True)
+        if fr.finish_bin():
+            eng.l1.zero_()
+            fr.composite(target=tgt, l1_sum=eng.l1, train=True)
+        c = fr.last_counters
+        nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))  # divergence of the previous step
+        nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
         if self.targets_on_host:
             self.loss_host.copy_(eng.l1, non_blocking=True)  # the step's scalar result, to the host
         value = None

@@ -289,6 +289,35 @@ class TestTrainLoop:  # test_trainer.py:290-386
         assert rep.psnr > 120.0 and rep.ssim > 0.999999
 
 
+class TestForwardBeforeCounterRead:
+    """The trainer queues the forward before it reads the binning counters;
+    after an entry-buffer overflow the forward skipped itself on the device,
+    the view is re-binned and the forward re-run - the step equals one with
+    ample capacity."""
+
+    def test_overflow_step_matches(self, xg, tr, rng):
+        import torch
+
+        sc = small_scanner(32, 32, 6.0, n_views=4)
+        ds = self_render_dataset(xg, cloud_of(xg, random_arrays(8, rng, pos_scale=30.0, scale_range=(8.0, 15.0))), sc)
+        start = random_arrays(6, rng, pos_scale=30.0, scale_range=(8.0, 15.0))
+        cfg = tr.TrainConfig(iterations=10, gamma=0.0, densify_until_iter=0, log_interval=10**6,
+                             eval_interval=10**6)
+        a = tr.Trainer(ds, cloud_of(xg, start), cfg)
+        b = tr.Trainer(ds, cloud_of(xg, start), cfg)
+        fr = b.eng.frame
+        for t in (a, b):
+            t.step()
+        # shrink b's entry buffer below what a view needs: the next step overflows
+        fr.entry_capacity = 4
+        fr.entry_splat = torch.empty(4, dtype=torch.int32, device="cuda")
+        for t in (a, b):
+            t.step()
+        assert fr.entry_capacity > 4  # the overflow was seen and the view re-binned
+        torch.cuda.synchronize()
+        assert np.allclose(np_(a.cloud.flat), np_(b.cloud.flat), rtol=1e-5, atol=1e-7)
+
+
 class TestDataParallelSingleRank:
     """The data-parallel step (bucketed reduce + range Adam + renorm) on one
     rank must reproduce the single-GPU Trainer exactly (same views, same

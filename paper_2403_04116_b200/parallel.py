@@ -162,16 +162,19 @@ class DataParallelTrainer:
         eng, cloud = t.eng, t.cloud
         fr = eng.frame
         fr.preprocess(cloud, t.cams[view])
-        fr.ensure_binned(check_status=False)
-        c = fr.last_counters
-        nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))
-        nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
+        fr.bin_async()  # the forward is queued before the counter read (Trainer.step)
         tgt = t.targets[view]
         if t.targets_on_host:
             t.tgt_dev.copy_(tgt, non_blocking=True)
             tgt = t.tgt_dev
         eng.l1.zero_()
         fr.composite(target=tgt, l1_sum=eng.l1, train=True)
+        if fr.finish_bin():
+            eng.l1.zero_()
+            fr.composite(target=tgt, l1_sum=eng.l1, train=True)
+        c = fr.last_counters
+        nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))
+        nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
         fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
                     l1_scale=1.0 / (t.h * t.w), stats=t.stats)
         lr = _lr_array({"positions": position_learning_rate(cfg, it - 1), "rotations": cfg.lr_rotation,

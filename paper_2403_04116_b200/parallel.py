@@ -165,8 +165,8 @@ class DataParallelTrainer:
         fr.bin_async()  # the forward is queued before the counter read (Trainer.step)
         tgt = t.targets[view]
         if t.targets_on_host:
-            t.tgt_dev.copy_(tgt, non_blocking=True)
-            tgt = t.tgt_dev
+            t.tgt_bufs[0].copy_(tgt, non_blocking=True)  # (stream-ordered on the compute stream)
+            tgt = t.tgt_bufs[0]
         eng.l1.zero_()
         fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         if fr.finish_bin():

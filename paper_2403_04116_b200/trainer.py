@@ -355,10 +355,17 @@ class Trainer:
         # targets resident in HBM (default), or kept in pinned host memory and
         # copied per iteration (end-to-end measurement)
         self.targets_on_host = targets_on_host
+        self.tgt_slot = 0
         if targets_on_host:
             self.targets = {int(i): torch.as_tensor(dataset.images[i], dtype=torch.float32).pin_memory()
                             for i in dataset.train_indices}
-            self.tgt_dev = torch.empty((h, w), dtype=torch.float32, device=dev)
+            # double-buffered: the next view's target is copied on a side
+            # stream while the current step runs
+            self.tgt_bufs = [torch.empty((h, w), dtype=torch.float32, device=dev) for _ in range(2)]
+            self.copy_stream = torch.cuda.Stream(device=dev)
+            self.tgt_ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self.tgt_free = [torch.cuda.Event(), torch.cuda.Event()]
+            self.tgt_view = [None, None]
             self.loss_host = torch.zeros(1, dtype=torch.float64).pin_memory()
         else:
             self.targets = {int(i): torch.as_tensor(dataset.images[i], dtype=torch.float32, device=dev).contiguous()
@@ -377,6 +384,15 @@ class Trainer:
         self.grad_mask = 0x1F << nat.XG_ST_GRAD_SHIFT
         self.densify_events = 0
 
+    def _copy_target(self, slot: int, view: int) -> None:
+        """H2D copy of a view's target into buffer ``slot`` on the side
+        stream, after the buffer's previous user finished."""
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(self.tgt_free[slot])
+            self.tgt_bufs[slot].copy_(self.targets[view], non_blocking=True)
+            self.tgt_ready[slot].record(self.copy_stream)
+        self.tgt_view[slot] = view
+
     def step(self) -> None:
         cfg, eng = self.cfg, self.eng
         self.it += 1
@@ -391,9 +407,12 @@ class Trainer:
         # (it skips itself on the device after an entry overflow, then runs
         # again on the re-binned lists), so the GPU never waits on the sync
         fr.bin_async()
+        slot = self.tgt_slot
         if self.targets_on_host:
-            self.tgt_dev.copy_(self.targets[view], non_blocking=True)
-            tgt = self.tgt_dev
+            if self.tgt_view[slot] != view:  # not prefetched by the previous step
+                self._copy_target(slot, view)
+            torch.cuda.current_stream().wait_event(self.tgt_ready[slot])
+            tgt = self.tgt_bufs[slot]
         else:
             tgt = self.targets[view]
         eng.l1.zero_()
@@ -464,6 +483,13 @@ class Trainer:
                 self.log.flush()
         if ckpt_now:
             save_cloud(self.cloud, self.out_path / f"ckpt_{it:06d}.ply")
+        if self.targets_on_host:
+            # this step's target buffer is free once its kernels ran; the next
+            # view's target goes into the other one now
+            self.tgt_free[slot].record()
+            if self.order:
+                self._copy_target(1 - slot, self.order[-1])
+            self.tgt_slot = 1 - slot
 
     def close(self) -> None:
         if self.log is not None:

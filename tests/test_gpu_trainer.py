@@ -318,6 +318,27 @@ class TestForwardBeforeCounterRead:
         assert np.allclose(np_(a.cloud.flat), np_(b.cloud.flat), rtol=1e-5, atol=1e-7)
 
 
+class TestHostTargets:
+    def test_prefetched_targets_match_device_targets(self, xg, tr, rng):
+        """targets_on_host (the e2e mode: pinned host targets, the next view's
+        copied on a side stream during the step) trains exactly like
+        HBM-resident targets."""
+        import torch
+
+        sc = small_scanner(32, 32, 6.0, n_views=6)
+        ds = self_render_dataset(xg, cloud_of(xg, random_arrays(8, rng, pos_scale=30.0, scale_range=(8.0, 15.0))), sc)
+        start = random_arrays(6, rng, pos_scale=30.0, scale_range=(8.0, 15.0))
+        cfg = tr.TrainConfig(iterations=40, gamma=0.0, densify_until_iter=0, log_interval=10**6,
+                             eval_interval=10**6)
+        a = tr.Trainer(ds, cloud_of(xg, start), cfg)
+        b = tr.Trainer(ds, cloud_of(xg, start), cfg, targets_on_host=True)
+        for _ in range(40):
+            a.step()
+            b.step()
+        torch.cuda.synchronize()
+        assert np.allclose(np_(a.cloud.flat), np_(b.cloud.flat), rtol=1e-5, atol=1e-7)
+
+
 class TestDataParallelSingleRank:
     """The data-parallel step (bucketed reduce + range Adam + renorm) on one
     rank must reproduce the single-GPU Trainer exactly (same views, same

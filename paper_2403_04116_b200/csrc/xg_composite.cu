@@ -6,11 +6,15 @@
 //   power < -30; sigma = min(alpha e^power, 0.99); acc += i sigma T;
 //   T *= 1 - sigma.  The pixel centre is the integer lattice point.
 //
-// B200 mapping (warp-centric).  The unit of work is one 8x8 quarter of a
-// 16x16 tile, owned by ONE warp (2 vertically adjacent pixels per lane,
-// sharing dx and the dx-only terms).  Warps are persistent and pull units
-// from a heaviest-tile-first queue, so the load balances at quarter-tile
-// granularity and no warp ever waits for a sibling (no __syncthreads).
+// B200 mapping (warp-centric).  Tracking launches (render, training): the
+// unit of work is one 8x8 quarter of a 16x16 tile, owned by ONE warp (2
+// vertically adjacent pixels per lane, sharing dx and the dx-only terms).
+// Image-only launches (sweeps): one warp per tile, 8 rows of one column per
+// lane, each 16x8 half walking its own culled entry list (compact_fwd_split).
+// Units are dispatched heaviest tile first, so the load balances at
+// sub-tile granularity and no warp ever waits for a sibling.  Batches are
+// blended speculatively without per-pair tests and re-run exactly only where
+// a pixel crosses the transmittance floor (see composite_unit).
 // A warp walks its tile's entry list 32 at a time: each lane gathers one
 // entry's 36 B splat record (mean re-based to the tile origin in float64,
 // so dx/dy keep ~1e-6 px precision), tests it against the warp's 8x8
@@ -22,7 +26,8 @@
 // pixel of the sub-block, which the reference skips too.
 //
 // Power is evaluated on the log2 scale, p2 = A2 dx^2 + B2 dx dy + C2 dy^2
-// (= power * log2 e) with one MUFU.EX2 per pair; the transmittance update
+// (= power * log2 e) with one MUFU.EX2 per pair (image-only: 5 per 8 rows via
+// the row recurrence, blend_splat_spec_rec); the transmittance update
 // T <- T - sigma T is a single fused multiply-add.
 #include <stdlib.h>
 

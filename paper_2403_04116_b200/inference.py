@@ -197,7 +197,7 @@ class SweepRenderer:
 
 
 def render_sweep(cloud: GaussianCloud, scanner: ScannerConfig, angles=None, n_streams: int = 3,
-                 batch: int = 8) -> torch.Tensor:
+                 batch: int = 12) -> torch.Tensor:
     """Render ``angles`` (default: the scanner's) into a [V, H, W] device
     stack (batches of ``batch`` views per compositing launch)."""
     if angles is None:

@@ -64,6 +64,11 @@ __device__ unsigned long long g_fwd_stats[4];  // (development aid) recurrence /
 #define XG_FWD_REC_UNROLL 4  // measured: 1 -0.8 %, 2, 4 +0.5 % (C3) / +1.4 % (C4)
 #endif
 constexpr int kRecUnroll = XG_FWD_REC_UNROLL;
+// split path, direct-EX2 batches (measured: 2 vs 4 splats +0.9 % at C3, no spill)
+#ifndef XG_FWD_SPLIT_UNROLL
+#define XG_FWD_SPLIT_UNROLL 2
+#endif
+constexpr int kSplitUnroll = XG_FWD_SPLIT_UNROLL;
 // kClamp can only bind when alpha >= 0.99 (dens <= 1 for p2 <= 0); below a
 // safety margin for the MUFU.EX2 error the clamp logic is compiled out.
 constexpr float kNoClampAlpha = 0.98999f;
@@ -492,10 +497,10 @@ __device__ __forceinline__ void blend_splat_spec_rec(const FRec& r, float fx, co
   }
 }
 
-template <int kP>
+template <int kP, int kU = kFwdUnroll>
 __device__ __forceinline__ void blend_batch_spec(const FRec* rec, int cnt, float fx, const float2 (&fy)[kP],
                                                  float2 (&T)[kP], float2 (&acc)[kP]) {
-#pragma unroll kFwdUnroll
+#pragma unroll kU
   for (int q = 0; q < cnt; ++q) blend_splat_spec<kP>(rec[q], fx, fy, T, acc);
 }
 
@@ -528,7 +533,8 @@ __device__ __forceinline__ void blend_splat_spec_track(const FRec& r, int krel, 
 template <bool kGeneral, bool kTrack, int kP>
 __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, const float2 (&fy)[kP],
                                             float2 (&T)[kP], float2 (&acc)[kP], int (&last)[2 * kP]) {
-#pragma unroll kFwdUnroll
+  constexpr int kU = (!kTrack && kP == 4) ? kSplitUnroll : kFwdUnroll;  // (split image-only kernels: fewer registers)
+#pragma unroll kU
   for (int q = 0; q < cnt; ++q) blend_splat<kGeneral, kTrack, kP>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last);
 }
 
@@ -677,7 +683,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 #pragma unroll kRecUnroll
               for (int q = 0; q < cnt; ++q) blend_splat_spec_rec(rh[q], u.fx, fy, T, acc);
             } else {
-              blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);
+              blend_batch_spec<kP, kSplitUnroll>(rh, cnt, u.fx, fy, T, acc);
             }
           } else {
             blend_batch_spec<kP>(rh, cnt, u.fx, fy, T, acc);

@@ -1,0 +1,99 @@
+"""GPU engine vs the REAL reference at BASELINE.json's full sizes
+(tests/golden/fullsize.npz, written by xsplat 0.1.0 through
+tests/golden/make_golden_fullsize.py) - no oracle in between:
+
+* C1 (50,653 G, 256^2) at phi = 0.7 and pi/4, C3 (493,039 G, 512^2) at
+  phi = 0, pi/4, 0.7, C4 (1,030,301 G, 1024^2) at 0.7: active set, float64
+  depths, tile ranges and the full (tile, depth, index) entry order
+  bit-identical to the reference's SplatList (frontend.py:104-194) - at
+  pi/4 that includes the reference's tie-breaking of the symmetric
+  lattice's equal-depth splats;
+* C1 images and the C3 pi/4 image within 1e-4 relative of the reference's
+  float64 image (north_star tolerance), C1 radii within 1e-7 relative;
+* C1 at phi = 0.7 with dL/dI ~ N(0,1)/HW (seed 0): kernel-level gradients
+  (backward_tiles) and RenderGradients normwise within 1e-4
+  (backward.py:21-124)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import fullsize_golden as fg
+from conftest import normwise_ok
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def xg():
+    import torch
+
+    import paper_2403_04116_b200 as xg
+
+    torch.cuda.set_device(0)
+    return xg
+
+
+_cloud_cache: dict = {}
+
+
+def _render(xg, case):
+    import torch
+
+    g = fg.G_OF[case.split("_")[0]]
+    if g not in _cloud_cache:
+        _cloud_cache.clear()
+        _cloud_cache[g] = xg.GaussianCloud(**fg.cloud_arrays(case), device="cuda")
+    cloud = _cloud_cache[g]
+    l_so, l_sd, w, h, pitch, phi = fg.camera(case)
+    sc = xg.ScannerConfig(l_so, l_sd, w, h, pitch)
+    proj, sp = xg.render(cloud, xg.extrinsic_from_angle(sc, phi), xg.intrinsic_from_config(sc), (h, w))
+    torch.cuda.synchronize()
+    return cloud, proj, sp
+
+
+@pytest.mark.parametrize("case", ["C1_0.7", "C1_pi4", "C3_0", "C3_pi4", "C3_0.7", "C4_0.7"])
+def test_binning_equals_reference_full_size(xg, case):
+    cloud, proj, sp = _render(xg, case)
+    act = sp.active_indices.cpu().numpy()
+    fg.check_binning(case, act, sp.entry_splat.cpu().numpy(), sp.tile_ranges.cpu().numpy(),
+                     sp.depths.cpu().numpy())
+    assert sp.n_entries == int(fg.load()[case + "/n_entries"])
+    fx = fg.load()
+    p = case + "/"
+    if p + "image" in fx:
+        img = proj.pixels.cpu().numpy().astype(np.float64)
+        gold = fx[p + "image"].astype(np.float64)
+        scale = np.abs(gold).max()
+        err = np.abs(img - gold)
+        assert np.all(err <= 1e-4 * np.abs(gold) + 1e-6 * scale), (case, float(err.max()))
+    if p + "radii" in fx:
+        assert np.abs(sp.radii.cpu().numpy() / fx[p + "radii"] - 1).max() < 1e-7, case
+        assert np.array_equal(sp.depths.cpu().numpy(), fx[p + "depths"]), case
+
+
+def test_c1_gradients_equal_reference(xg):
+    import torch
+
+    fx = fg.load()
+    p = "C1_0.7/"
+    cloud, proj, sp = _render(xg, "C1_0.7")
+    d = 256
+    dl = np.random.default_rng(0).normal(size=(d, d)) / (d * d)
+    n = cloud.n_points
+    kg = {k: torch.zeros(s, dtype=torch.float64, device="cuda")
+          for k, s in (("g_mean", (n, 2)), ("g_conic", (n, 3)), ("g_int", n), ("g_alpha", n))}
+    grads = xg.render_backward(cloud, sp, torch.as_tensor(dl), kernel_grads=kg)
+    torch.cuda.synchronize()
+    act = sp.active_indices.cpu().numpy()
+    floor = 1e-3 * max(np.abs(fx[p + "k_" + k]).max() for k in kg)
+    for k, v in kg.items():
+        ok, rel = normwise_ok(v.cpu().numpy()[act], fx[p + "k_" + k], floor)
+        assert ok, (k, rel)
+    fields = ("positions", "rotations", "log_scales", "raw_opacities", "features")
+    floor = 1e-3 * max(np.abs(fx[p + "grad_" + f]).max() for f in fields)
+    for f in fields + ("screen_norms",):
+        ok, rel = normwise_ok(getattr(grads, f).cpu().numpy(), fx[p + "grad_" + f], floor)
+        assert ok, (f, rel)
+    assert np.array_equal(grads.visible.cpu().numpy(), fx[p + "grad_visible"])

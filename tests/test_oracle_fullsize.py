@@ -1,0 +1,70 @@
+"""Pin the CPU oracle to the real reference at BASELINE.json's full sizes
+(tests/golden/fullsize.npz, make_golden_fullsize.py): C1 and C3 at phi = 0,
+pi/4 (the symmetric lattice view whose exact depth ties the order must break
+as the reference does) and 0.7, C4 at 0.7.  CPU only."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import fullsize_golden as fg
+from conftest import normwise_ok
+from oracle import oracle as orc
+
+BIN_CASES = ["C1_0.7", "C1_pi4", "C3_0", "C3_pi4", "C3_0.7", "C4_0.7"]
+_runs: dict = {}
+
+
+def _oracle(case):
+    if case not in _runs:
+        arrs = fg.cloud_arrays(case)
+        cam = orc.camera_from_view(*fg.camera(case))
+        pre = orc.preprocess(arrs, np.ones(16, np.float32), cam)
+        binned = orc.bin_entries(pre, cam)
+        _runs.clear()  # keep one full-size case resident
+        _runs[case] = (arrs, cam, pre, binned)
+    return _runs[case]
+
+
+@pytest.mark.parametrize("case", BIN_CASES)
+def test_oracle_binning_equals_reference(case):
+    arrs, cam, pre, binned = _oracle(case)
+    act = np.flatnonzero(pre["active"])
+    rows = fg.ref_form(binned["entry_splat"], act, pre["active"].size)
+    fg.check_binning(case, act, rows, binned["tile_ranges"], pre["depth"][act])
+
+
+@pytest.mark.parametrize("case", ["C1_0.7", "C1_pi4"])
+def test_oracle_c1_geometry_and_image(case):
+    fx = fg.load()
+    p = case + "/"
+    arrs, cam, pre, binned = _oracle(case)
+    act = np.flatnonzero(pre["active"])
+    assert np.array_equal(act, fx[p + "active_indices"])
+    assert np.array_equal(pre["depth"][act], fx[p + "depths"])
+    assert np.abs(pre["radius"][act] / fx[p + "radii"] - 1).max() < 1e-7
+    d = cam.width
+    img = orc.composite_fwd(pre, binned, d, d)["image"].astype(np.float64)
+    gold = fx[p + "image"]
+    scale = np.abs(gold).max()
+    assert np.all(np.abs(img - gold) <= 1e-4 * np.abs(gold) + 1e-6 * scale), np.abs(img - gold).max()
+
+
+def test_oracle_c1_gradients():
+    fx = fg.load()
+    p = "C1_0.7/"
+    arrs, cam, pre, binned = _oracle("C1_0.7")
+    d = cam.width
+    dl = np.random.default_rng(0).normal(size=(d, d)) / (d * d)
+    kg = orc.composite_bwd(pre, binned, d, d, dl)
+    act = np.flatnonzero(pre["active"])
+    floor = 1e-3 * max(np.abs(fx[p + k]).max() for k in ("k_g_mean", "k_g_conic", "k_g_int", "k_g_alpha"))
+    for k in ("g_mean", "g_conic", "g_int", "g_alpha"):
+        ok, rel = normwise_ok(kg[k][act], fx[p + "k_" + k], floor)
+        assert ok, (k, rel)
+    g = orc.preprocess_bwd(arrs, np.ones(16, np.float32), cam, pre, kg)
+    floor = 1e-3 * max(np.abs(fx[p + "grad_" + f]).max() for f in orc.PARAM_FIELDS)
+    for f in orc.PARAM_FIELDS:
+        ok, rel = normwise_ok(g[f], fx[p + "grad_" + f], floor)
+        assert ok, (f, rel)

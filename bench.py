@@ -539,10 +539,8 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
         if world == 1:
             tr = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg, targets_on_host=(mode == "e2e"))
         else:
-            dp = DataParallelTrainer(ds, GaussianCloud(**init, device="cuda"), cfg,
+            tr = DataParallelTrainer(ds, GaussianCloud(**init, device="cuda"), cfg,
                                      targets_on_host=(mode == "e2e"))
-            tr = dp.t
-            tr.step = dp.step  # the DP step drives the same Trainer state
         warm = max(args.warmup, 5)  # reach densify_from_iter = 500
         for _ in range(warm * per):
             tr.step()

@@ -92,7 +92,7 @@ __global__ void k_duplicate(const uint32_t* __restrict__ order, const uint32_t* 
 __global__ void k_tile_bounds(const uint32_t* __restrict__ keys, const uint32_t* counters, long long cap,
                               long long* __restrict__ ranges) {
   long long e = counters[XG_CTR_ENTRIES];
-  if (e > cap) e = cap;
+  if (e > cap) e = 0;  // overflow: the list is partial (k_duplicate skips warps past cap); re-binned
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < e;
        k += (long long)gridDim.x * blockDim.x) {
     const uint32_t t = keys[k];
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
   __shared__ long long s_val[1024];
   __shared__ long long s_next;
   long long e = counters[XG_CTR_ENTRIES];
-  if (e > cap) e = cap;
+  if (e > cap) e = 0;  // overflow: every tile empty until the re-bin
   if (threadIdx.x == 0) s_next = e;
   for (int hi = n_tiles; hi > 0; hi -= 1024) {
     const int t = hi - 1024 + (int)threadIdx.x;

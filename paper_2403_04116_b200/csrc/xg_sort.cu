@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kSortThreads)
   constexpr int BINS = 1 << BITS;
   __shared__ uint32_t h[kSortWarps][BINS];
   long long n = *n_dev;
-  if (n > cap) n = cap;
+  if (n > cap) n = 0;  // overflowed list (never fully written): discarded and re-binned
   const int warp = threadIdx.x >> 5;
   for (int b = threadIdx.x; b < kSortWarps * BINS; b += kSortThreads) (&h[0][0])[b] = 0;
   __syncthreads();
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kSortThreads)
   __shared__ uint32_t wh[kSortWarps][BINS];
   __shared__ uint32_t goff[BINS];
   long long n = *n_dev;
-  if (n > cap) n = cap;
+  if (n > cap) n = 0;  // overflowed list (never fully written): discarded and re-binned
   const long long base = (long long)blockIdx.x * kSortTile;
   if (base >= n) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

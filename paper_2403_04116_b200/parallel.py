@@ -11,10 +11,11 @@ B200 node, gloo in the CPU tests).
   a distinct training view, runs the reverse composite + chain rule, and the
   flat 27N gradient is summed over ranks.  ``GradientAllReducer`` splits the
   flat buffer into buckets, issues every bucket's all-reduce asynchronously
-  and runs the per-bucket epilogue (finite check + fused Adam on that
-  element range, ``xg_adam_range``) as soon as that bucket has landed, so
-  Adam on bucket i overlaps the reduction of bucket i+1; all ranks then
-  hold bit-identical parameters.  Density statistics stay rank-local (the
+  and runs the per-bucket epilogue as soon as that bucket has landed: the
+  finite check of the bucket, and the fused Adam (``xg_adam_range``) of
+  every field whose buckets have all been checked - so Adam on the early
+  fields overlaps the reduction of the later ones; all ranks then hold
+  bit-identical parameters.  Density statistics stay rank-local (the
   per-view screen norms are summed, not the norm of the summed gradient) and
   are all-reduced only at densify events.
 
@@ -30,6 +31,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as nat
+from .trainer import Trainer
 
 
 def world_info(group=None) -> tuple[int, int]:
@@ -128,61 +130,71 @@ def allreduce_stats(stats, group=None) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
 
-class DataParallelTrainer:
+def _field_ends(n: int, nf: int) -> list[int]:
+    """End offsets of the five fields in the flat [pos | rot | log_s | raw | feat] layout."""
+    ends, o = [], 0
+    for wdt in (3, 4, 3, 1, nf):
+        o += n * wdt
+        ends.append(o)
+    return ends
+
+
+class DataParallelTrainer(Trainer):
     """Data-parallel training: one view per rank per step, summed gradients,
-    bucket-pipelined fused Adam, identical replicas."""
+    bucket-pipelined fused Adam, identical replicas.
 
-    def __init__(self, dataset, cloud, cfg, group=None, bucket_bytes: int = 8 << 20, targets_on_host=False):
-        from .trainer import Trainer
+    The iteration is ``Trainer.step``'s - the same forward / fused loss
+    (L1, or L1 + SSIM when ``gamma > 0``) / reverse pass, opacity reset,
+    logging, evaluation and checkpoints (rank 0 writes ``out_dir``) - with
+    two phases replaced: the view schedule (``world`` views of the shared
+    permutation per step, this rank's is element ``rank``) and the gradient
+    application (all-reduce + Adam), plus the density statistics summed over
+    ranks before each density-control event.
 
-        self.rank, self.world = world_info(group)
+    Divergence semantics follow the reference's ``adam_step``
+    (trainer.py:158-170): fields are checked in order, fields before the
+    first non-finite one are updated, that field and every later one are
+    not.  Each bucket's finite check runs as soon as it has landed; a
+    field's Adam is queued once every bucket of that field (and of all
+    earlier fields) has been checked, so a non-finite value in a later
+    bucket of a field can never follow a partial update of it."""
+
+    def __init__(self, dataset, cloud, cfg, group=None, bucket_bytes: int = 8 << 20, targets_on_host=False,
+                 out_dir=None, verbose: bool = False):
+        rank, world = world_info(group)
+        super().__init__(dataset, cloud, cfg, out_dir=out_dir if rank == 0 else None,
+                         verbose=verbose and rank == 0, targets_on_host=targets_on_host)
+        self.rank, self.world = rank, world
         self.group = group
-        self.t = Trainer(dataset, cloud, cfg, targets_on_host=targets_on_host)
         self.bucket_bytes = bucket_bytes
         self._reducer = None
 
     @property
-    def cloud(self):
-        return self.t.cloud
+    def t(self):  # (round-1 API: the wrapped Trainer is now the object itself)
+        return self
 
     def _reducer_for(self, numel: int) -> GradientAllReducer:
         if self._reducer is None or self._reducer.numel != numel:
             self._reducer = GradientAllReducer(numel, self.bucket_bytes, self.group)
         return self._reducer
 
-    def step(self) -> None:
-        from .trainer import DensifyStats, densify_and_prune, position_learning_rate, _lr_array
+    def _next_view(self) -> int:
+        return dp_views(self.order, self.dataset.train_indices, self.rng, self.world)[self.rank]
 
-        t = self.t
-        cfg = t.cfg
-        t.it += 1
-        it = t.it
-        views = dp_views(t.order, t.dataset.train_indices, t.rng, self.world)
-        view = views[self.rank]
-        eng, cloud = t.eng, t.cloud
-        fr = eng.frame
-        fr.preprocess(cloud, t.cams[view])
-        fr.bin_async()  # the forward is queued before the counter read (Trainer.step)
-        tgt = t.targets[view]
-        if t.targets_on_host:
-            t.tgt_bufs[0].copy_(tgt, non_blocking=True)  # (stream-ordered on the compute stream)
-            tgt = t.tgt_bufs[0]
-        eng.l1.zero_()
-        fr.composite(target=tgt, l1_sum=eng.l1, train=True)
-        if fr.finish_bin():
-            eng.l1.zero_()
-            fr.composite(target=tgt, l1_sum=eng.l1, train=True)
-        c = fr.last_counters
-        nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))
-        nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
-        fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
-                    l1_scale=1.0 / (t.h * t.w), stats=t.stats)
-        lr = _lr_array({"positions": position_learning_rate(cfg, it - 1), "rotations": cfg.lr_rotation,
-                        "log_scales": cfg.lr_scaling, "raw_opacities": cfg.lr_opacity,
-                        "features": cfg.lr_feature})
-        t.state.step += 1
-        bc1 = 1.0 - cfg.beta1**t.state.step
-        bc2 = 1.0 - cfg.beta2**t.state.step
+    def _upcoming_view(self):
+        return self.order[-1 - self.rank] if len(self.order) > self.rank else None
+
+    def _reduce_stats(self) -> None:
+        allreduce_stats(self.stats, self.group)
+
+    def _apply_gradients(self) -> None:
+        from .trainer import _lr_array
+
+        cfg, cloud, fr = self.cfg, self.cloud, self.eng.frame
+        lr = _lr_array(self._lr_table())
+        self.state.step += 1
+        bc1 = 1.0 - cfg.beta1**self.state.step
+        bc2 = 1.0 - cfg.beta2**self.state.step
         n, nf = cloud.n_points, cloud.n_features
         # flags of the SUMMED gradient decide divergence, identically on all
         # ranks: the finite check writes its word at counters[STATUS] of the
@@ -190,23 +202,25 @@ class DataParallelTrainer:
         sticky = fr.counters.data_ptr() + 4 * nat.XG_CTR_STICKY
         flag_base = sticky - 4 * nat.XG_CTR_STATUS
         lib = nat.lib()
-        gflat = eng.grads.flat
+        gflat = self.eng.grads.flat
+        ends = _field_ends(n, nf)
+        done = [0]
+
+        def adam(lo, hi):
+            nat.check(lib.xg_adam_range(cloud.flat.data_ptr(), gflat.data_ptr(), self.state.m_flat.data_ptr(),
+                                        self.state.v_flat.data_ptr(), n, nf, lr, cfg.beta1, cfg.beta2, cfg.eps,
+                                        bc1, bc2, sticky, lo, hi, nat.stream()), "xg_adam_range")
 
         def epilogue(lo, hi):
             nat.check(lib.xg_check_finite_range(gflat.data_ptr(), n, nf, lo, hi, flag_base, nat.stream()),
                       "xg_check_finite_range")
-            nat.check(lib.xg_adam_range(cloud.flat.data_ptr(), gflat.data_ptr(), t.state.m_flat.data_ptr(),
-                                        t.state.v_flat.data_ptr(), n, nf, lr, cfg.beta1, cfg.beta2, cfg.eps,
-                                        bc1, bc2, sticky, lo, hi, nat.stream()), "xg_adam_range")
+            ready = max([e for e in ends if e <= hi], default=0)  # fields checked in full
+            if ready > done[0]:
+                adam(done[0], ready)
+                done[0] = ready
 
         self._reducer_for(gflat.numel())(gflat, epilogue)
+        if done[0] < gflat.numel():  # (unreachable: the last bucket ends at the last field's end)
+            adam(done[0], gflat.numel())
         nat.check(lib.xg_adam_renorm(cloud.flat.data_ptr(), n, nf, sticky, nat.stream()), "xg_adam_renorm")
         cloud.mark_mutated()
-        if cfg.densify_from_iter < it <= cfg.densify_until_iter and it % cfg.densify_interval == 0:
-            nat.raise_for_status(int(fr.counters[nat.XG_CTR_STICKY].item()) & 0xFFFFFFFF)
-            allreduce_stats(t.stats, self.group)
-            t.cloud, t.state, _ = densify_and_prune(cloud, t.state, t.stats, cfg, t.size_threshold, t.rng)
-            t.stats = DensifyStats.zeros(t.cloud.n_points, t.dev)
-            eng.resize(t.cloud)
-            t.densify_events += 1
-

@@ -393,21 +393,36 @@ class Trainer:
             self.tgt_ready[slot].record(self.copy_stream)
         self.tgt_view[slot] = view
 
+    # --- one iteration, in phases (DataParallelTrainer overrides the view
+    # --- choice and the gradient application) ---------------------------------
     def step(self) -> None:
-        cfg, eng = self.cfg, self.eng
         self.it += 1
-        it = self.it
-        h, w = self.h, self.w
+        view = self._next_view()
+        slot = self.tgt_slot
+        tgt = self._render_and_backward(view, slot)
+        self._apply_gradients()
+        self._tail(tgt, slot)
+
+    def _next_view(self) -> int:
         if not self.order:
             self.order = [int(i) for i in self.rng.permutation(self.dataset.train_indices)]
-        view = self.order.pop()
+        return self.order.pop()
+
+    def _upcoming_view(self):
+        """The view the next step will train on, if known (target prefetch)."""
+        return self.order[-1] if self.order else None
+
+    def _render_and_backward(self, view: int, slot: int) -> torch.Tensor:
+        """Forward with the fused L1 sum, the loss's pixel gradient and the
+        reverse pass into ``eng.grads`` (+ DensifyStats); returns the target."""
+        cfg, eng = self.cfg, self.eng
+        h, w = self.h, self.w
         fr = eng.frame
         fr.preprocess(self.cloud, self.cams[view])
         # the forward is queued before the host reads the binning counters
         # (it skips itself on the device after an entry overflow, then runs
         # again on the re-binned lists), so the GPU never waits on the sync
         fr.bin_async()
-        slot = self.tgt_slot
         if self.targets_on_host:
             if self.tgt_view[slot] != view:  # not prefetched by the previous step
                 self._copy_target(slot, view)
@@ -425,7 +440,7 @@ class Trainer:
         nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
         if self.targets_on_host:
             self.loss_host.copy_(eng.l1, non_blocking=True)  # the step's scalar result, to the host
-        value = None
+        self.s_dev = None
         if cfg.gamma == 0.0:
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
                         l1_scale=1.0 / (h * w), stats=self.stats)
@@ -434,25 +449,44 @@ class Trainer:
             # (trainer.py:117-123) straight into the backward's input
             if eng.ssim is None:
                 eng.ssim = SsimEngine(h, w, self.dev)
-            s_dev = eng.ssim.run(fr.image, tgt, 1.0, dl=eng.dl, dl_ssim_scale=-cfg.gamma,
-                                 dl_l1_scale=(1.0 - cfg.gamma) / (h * w))
+            self.s_dev = eng.ssim.run(fr.image, tgt, 1.0, dl=eng.dl, dl_ssim_scale=-cfg.gamma,
+                                      dl_l1_scale=(1.0 - cfg.gamma) / (h * w))
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis,
                         dl_dimage=eng.dl, stats=self.stats)
+        return tgt
+
+    def _lr_table(self) -> dict:
+        cfg = self.cfg
+        return {"positions": position_learning_rate(cfg, self.it - 1), "rotations": cfg.lr_rotation,
+                "log_scales": cfg.lr_scaling, "raw_opacities": cfg.lr_opacity, "features": cfg.lr_feature}
+
+    def _apply_gradients(self) -> None:
+        fr = self.eng.frame
         # carry this step's non-finite flags into the sticky word Adam reads
         fr.counters[nat.XG_CTR_STICKY : nat.XG_CTR_STICKY + 1].bitwise_or_(
             fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1] & self.grad_mask)
-        lr_table = {"positions": position_learning_rate(cfg, it - 1), "rotations": cfg.lr_rotation,
-                    "log_scales": cfg.lr_scaling, "raw_opacities": cfg.lr_opacity, "features": cfg.lr_feature}
         self.state.step += 1
-        _adam_launch(self.cloud, eng.grads.flat, self.state, lr_table, cfg,
+        _adam_launch(self.cloud, self.eng.grads.flat, self.state, self._lr_table(), self.cfg,
                      fr.counters.data_ptr() + 4 * nat.XG_CTR_STICKY)
 
+    def _reduce_stats(self) -> None:
+        """Density statistics of this process are the whole step's (DP: summed)."""
+
+    def _tail(self, tgt: torch.Tensor, slot: int) -> None:
+        """Density control, opacity reset, logging / evaluation, checkpoints
+        (trainer.py:389-437) and the next target's prefetch."""
+        cfg, eng, it = self.cfg, self.eng, self.it
+        h, w = self.h, self.w
+        fr = eng.frame
         densify_now = cfg.densify_from_iter < it <= cfg.densify_until_iter and it % cfg.densify_interval == 0
+        reset_now = bool(cfg.opacity_reset_interval) and it % cfg.opacity_reset_interval == 0
         log_now = it % cfg.log_interval == 0 or it == cfg.iterations
         ckpt_now = self.out_path is not None and it in cfg.checkpoint_iterations
-        if densify_now or log_now or ckpt_now or it == cfg.iterations:
+        if densify_now or reset_now or log_now or ckpt_now or it == cfg.iterations:
+            # the reference raises inside adam_step, before any of these
             nat.raise_for_status(int(fr.counters[nat.XG_CTR_STICKY].item()) & 0xFFFFFFFF)
         if densify_now:
+            self._reduce_stats()
             self.cloud, self.state, rep = densify_and_prune(self.cloud, self.state, self.stats, cfg,
                                                             self.size_threshold, self.rng)
             self.stats = DensifyStats.zeros(self.cloud.n_points, self.dev)
@@ -460,15 +494,14 @@ class Trainer:
             self.densify_events += 1
             if self.verbose:
                 print(f"[{it}] density control: {rep}")
-        if cfg.opacity_reset_interval and it % cfg.opacity_reset_interval == 0:
+        if reset_now:
             self.cloud.raw_opacities.clamp_(max=logit(0.01))
             self.state.exp_avg["raw_opacities"].zero_()
             self.state.exp_avg_sq["raw_opacities"].zero_()
         if log_now:
-            if value is None:
-                value = float(eng.l1.item()) / (h * w)
-                if cfg.gamma != 0.0:
-                    value = (1.0 - cfg.gamma) * value + cfg.gamma * (1.0 - float(s_dev.item()))
+            value = float(eng.l1.item()) / (h * w)
+            if cfg.gamma != 0.0:
+                value = (1.0 - cfg.gamma) * value + cfg.gamma * (1.0 - float(self.s_dev.item()))
             row = {"iteration": it, "loss": value, "train_psnr": psnr(fr.image, tgt), "test_psnr": None,
                    "test_ssim": None, "n_points": self.cloud.n_points}
             if it % cfg.eval_interval == 0 or it == cfg.iterations:
@@ -487,8 +520,9 @@ class Trainer:
             # this step's target buffer is free once its kernels ran; the next
             # view's target goes into the other one now
             self.tgt_free[slot].record()
-            if self.order:
-                self._copy_target(1 - slot, self.order[-1])
+            nxt = self._upcoming_view()
+            if nxt is not None:
+                self._copy_target(1 - slot, nxt)
             self.tgt_slot = 1 - slot
 
     def close(self) -> None:

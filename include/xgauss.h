@@ -241,6 +241,21 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
                            const int32_t* n_contrib, const float* dl_dimage, const float* image,
                            const float* target, float l1_scale, float* grad_acc, void* stream);
 
+/* Reproducible K4a (the reference's single-threaded backward is bitwise
+ * reproducible, pkg/tests/test_trainer.py:336-353): the same reverse replay,
+ * but each (entry, chunk) warp STORES its per-entry 8-value sum into
+ * entry_grad[entry_capacity][8] (zeroed here) instead of adding it to the
+ * splat; xg_reduce_entry_grads then writes grad_acc[N][8] by summing each
+ * splat's entries in row-major order of its tile rectangle.  Needs the
+ * checkpointed replay (a tracking forward with replay_ckpt/replay_items/
+ * unit_cost, and image).  Same numbers as xg_composite_bwd up to the
+ * summation order, identical run to run. */
+xg_status xg_composite_bwd_entries(const xg_camera* cam, const xg_splats* sp, const float* t_final,
+                                   const int32_t* n_contrib, const float* dl_dimage, const float* image,
+                                   const float* target, float l1_scale, float* entry_grad, void* stream);
+xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const float* entry_grad,
+                                float* grad_acc, void* stream);
+
 /* K4b: chain rule to every cloud field (float64 arithmetic).  Writes
  * grads (flat, same layout as params; zero rows for culled Gaussians),
  * screen_norms[N], visible[N]; flags non-finite fields in the status word.

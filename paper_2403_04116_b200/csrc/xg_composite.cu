@@ -1001,6 +1001,7 @@ struct BwdArgs {
   const float2* ckpt;         // chunked replay: the forward's checkpoints,
   const uint2* items;         //   the chunk list (tile, sub << 24 | chunk)
   const uint32_t* n_items;    //   and its length
+  float* entry_grad;          // reproducible mode: [E][8] per-entry sums (plain stores), else null
 };
 
 // Backward records (shared memory), signs folded as in the forward:
@@ -1236,7 +1237,7 @@ template <int kMode, int kP>
 __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, const uint32_t* gid, int cnt, float fx,
                                               const float2 (&fy)[kP], const int (&last)[2 * kP],
                                               const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP],
-                                              float* grad_acc) {
+                                              float* grad_acc, float* entry_grad, long long start) {
   const int lane = threadIdx.x & 31;
   // splats two at a time, back to front (A = q, then B = q - 1), their
   // records reduced together
@@ -1258,8 +1259,16 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
     const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
     const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
     if ((lane & 7) == 0 && (lane < 16 || hasB)) {
-      const uint32_t id = lane < 16 ? gid[q] : gid[q - 1];
-      red_add_v4(grad_acc + 8 * (long long)id + ((lane & 8) ? 4 : 0), tot, t1, t2, t3);
+      if (entry_grad) {
+        // reproducible mode: this warp is the only writer of the entry's
+        // (whole-tile sub-block, one chunk) sum; xg_reduce_entry_grads adds
+        // a splat's entries in a fixed order
+        const long long e = start + (lane < 16 ? kk[q] : kk[q - 1]);
+        *reinterpret_cast<float4*>(entry_grad + 8 * e + ((lane & 8) ? 4 : 0)) = make_float4(tot, t1, t2, t3);
+      } else {
+        const uint32_t id = lane < 16 ? gid[q] : gid[q - 1];
+        red_add_v4(grad_acc + 8 * (long long)id + ((lane & 8) ? 4 : 0), tot, t1, t2, t3);
+      }
     }
   }
 }
@@ -1322,11 +1331,11 @@ __device__ __forceinline__ void replay_range(const BwdArgs& a, const Unit& u, lo
     }
 #endif
     if (general)
-      unblend_batch<1, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
+      unblend_batch<1, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc, a.entry_grad, start);
     else if (exact)
-      unblend_batch<0, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc);
+      unblend_batch<0, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc, a.entry_grad, start);
     else
-      unblend_batch<2, kP>(rec, kk, gid, cnt, u.fx, fye, last, g, T, nS, a.grad_acc);
+      unblend_batch<2, kP>(rec, kk, gid, cnt, u.fx, fye, last, g, T, nS, a.grad_acc, a.entry_grad, start);
     __syncwarp();
   }
 }
@@ -1656,6 +1665,42 @@ using namespace xg;
 
 extern "C" {
 
+// Reproducible mode: grad_acc[g] = the sum of splat g's per-entry records,
+// added in row-major order of its tile rectangle.  The entry of g in tile t
+// is found by binary search of the tile's list, which is sorted by
+// (float64 depth bits, cloud index) - the binning's own key.
+__global__ void k_reduce_entry_grads(const float* __restrict__ entry_grad, const uint32_t* __restrict__ entry,
+                                     const long long* __restrict__ ranges, const unsigned long long* __restrict__ dkey,
+                                     const ushort4* __restrict__ rect, const uint32_t* __restrict__ n_tiles,
+                                     long long n, int ntx, const uint32_t* n_entries, long long cap,
+                                     float* __restrict__ grad_acc) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+  if (n_tiles[g] && !(n_entries && (long long)*n_entries > cap)) {
+    const ushort4 r = rect[g];
+    const unsigned long long kd = dkey[g];
+    for (int ty = r.y; ty <= r.w; ++ty)
+      for (int tx = r.x; tx <= r.z; ++tx) {
+        const int t = ty * ntx + tx;
+        long long lo = ranges[2 * t], hi = ranges[2 * t + 1];
+        while (lo < hi) {  // first position whose key is >= (kd, g)
+          const long long mid = (lo + hi) >> 1;
+          const uint32_t e = entry[mid];
+          const unsigned long long ke = dkey[e];
+          if (ke < kd || (ke == kd && e < (uint32_t)g)) lo = mid + 1;
+          else hi = mid;
+        }
+        const float4 a = *reinterpret_cast<const float4*>(entry_grad + 8 * lo);
+        const float4 b = *reinterpret_cast<const float4*>(entry_grad + 8 * lo + 4);
+        s0.x += a.x; s0.y += a.y; s0.z += a.z; s0.w += a.w;
+        s1.x += b.x; s1.y += b.y; s1.z += b.z; s1.w += b.w;
+      }
+  }
+  *reinterpret_cast<float4*>(grad_acc + 8 * g) = s0;
+  *reinterpret_cast<float4*>(grad_acc + 8 * g + 4) = s1;
+}
+
 static xg_status composite_fwd_impl(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
                                     int32_t* n_contrib, const float* target, double* l1_sum, void* stream,
                                     bool lite) {
@@ -1779,10 +1824,11 @@ xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, fl
   return check_launch("k_composite_fwd_batch");
 }
 
-xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
-                           const int32_t* n_contrib, const float* dl_dimage, const float* image,
-                           const float* target, float l1_scale, float* grad_acc, void* stream) {
-  if (!cam || !sp || !t_final || !n_contrib || !grad_acc || (!dl_dimage && (!image || !target))) {
+static xg_status composite_bwd_impl(const xg_camera* cam, const xg_splats* sp, const float* t_final,
+                                    const int32_t* n_contrib, const float* dl_dimage, const float* image,
+                                    const float* target, float l1_scale, float* grad_acc, float* entry_grad,
+                                    void* stream) {
+  if (!cam || !sp || !t_final || !n_contrib || !(grad_acc || entry_grad) || (!dl_dimage && (!image || !target))) {
     set_error_msg("xg_composite_bwd: invalid argument");
     return XG_ERR_INVALID;
   }
@@ -1811,10 +1857,16 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
               (const long long*)sp->tile_ranges, nullptr, work, n_tiles, false, t_final, n_contrib, dl_dimage,
               image, target, l1_scale, grad_acc,
               sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
-              tiles_x(*cam), cam->width, cam->height, (const float2*)sp->replay_ckpt, items, n_items};
+              tiles_x(*cam), cam->width, cam->height, (const float2*)sp->replay_ckpt, items, n_items,
+              entry_grad};
     k_composite_bwd_ck<<<persistent_grid(k_composite_bwd_ck, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0,
                          (cudaStream_t)stream>>>(a);
     return check_launch("k_composite_bwd_ck");
+  }
+  if (entry_grad) {
+    set_error_msg("xg_composite_bwd_entries: needs the checkpointed replay (a tracking forward with "
+                  "replay_ckpt, replay_items, unit_cost, and the image)");
+    return XG_ERR_INVALID;
   }
   // schedule the reverse replay by the per-unit cost the forward recorded
   const bool by_unit = sp->unit_cost && sp->unit_order;
@@ -1835,6 +1887,45 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   }
   k_composite_bwd<<<persistent_grid(k_composite_bwd, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0, (cudaStream_t)stream>>>(a);
   return check_launch("k_composite_bwd");
+}
+
+xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
+                           const int32_t* n_contrib, const float* dl_dimage, const float* image,
+                           const float* target, float l1_scale, float* grad_acc, void* stream) {
+  return composite_bwd_impl(cam, sp, t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc, nullptr,
+                            stream);
+}
+
+xg_status xg_composite_bwd_entries(const xg_camera* cam, const xg_splats* sp, const float* t_final,
+                                   const int32_t* n_contrib, const float* dl_dimage, const float* image,
+                                   const float* target, float l1_scale, float* entry_grad, void* stream) {
+  if (kBwdSubs != 1) {
+    set_error_msg("xg_composite_bwd_entries: built with XG_BWD_PAIRS != 4 (several writers per entry)");
+    return XG_ERR_INVALID;
+  }
+  if (!entry_grad || !sp || sp->entry_capacity < 1) {
+    set_error_msg("xg_composite_bwd_entries: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  // entries no reverse step reaches (culled, past every pixel's last) stay 0
+  cudaMemsetAsync(entry_grad, 0, sizeof(float) * 8 * (size_t)sp->entry_capacity, (cudaStream_t)stream);
+  return composite_bwd_impl(cam, sp, t_final, n_contrib, dl_dimage, image, target, l1_scale, nullptr, entry_grad,
+                            stream);
+}
+
+xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const float* entry_grad,
+                                float* grad_acc, void* stream) {
+  if (!cam || !sp || !entry_grad || !grad_acc || !sp->entry_splat || !sp->tile_ranges || !sp->depth_key ||
+      !sp->rect || !sp->n_tiles || sp->n < 1) {
+    set_error_msg("xg_reduce_entry_grads: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  k_reduce_entry_grads<<<div_up(sp->n, 256), 256, 0, (cudaStream_t)stream>>>(
+      entry_grad, sp->entry_splat, (const long long*)sp->tile_ranges, (const unsigned long long*)sp->depth_key,
+      (const ushort4*)sp->rect, sp->n_tiles, sp->n, tiles_x(*cam),
+      sp->entry_capacity > 0 && sp->counters ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
+      grad_acc);
+  return check_launch("k_reduce_entry_grads");
 }
 
 int64_t xg_replay_slots(int64_t entry_capacity, int32_t n_tiles_total) {

@@ -71,6 +71,7 @@ class Frame:
         self.workspace = None
         self.replay_ckpt = None  # training frames only: allocated by the first tracking composite
         self.replay_items = None
+        self.entry_grad = None  # reproducible backward only: [entry_capacity][8] per-entry records
         self.set_capacity(entry_capacity if entry_capacity else max(16 * n, 1024))
         self.cam = None
         self.has_forward = False
@@ -157,7 +158,8 @@ class Frame:
         )
 
     def composite(self, target: torch.Tensor | None = None, l1_sum: torch.Tensor | None = None,
-                  image_out: torch.Tensor | None = None, track: bool = True, train: bool = False) -> None:
+                  image_out: torch.Tensor | None = None, track: bool = True, train: bool = False,
+                  events: list | None = None) -> None:
         """K3.  ``image_out`` (float32 [H, W], contiguous) receives the image
         instead of the frame's own buffer (e.g. a slot of a sweep stack).
         ``track=False`` (inference) skips the per-pixel final transmittance
@@ -170,6 +172,10 @@ class Frame:
         sp = self.splats_struct()
         img = self.image if image_out is None else image_out
         fn = "xg_composite_fwd_train" if (track and train) else "xg_composite_fwd"
+        ev = None
+        if events is not None:  # (measurement: CUDA events around the launch)
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         nat.check(
             getattr(nat.lib(), fn)(
                 ctypes.byref(self.cam), ctypes.byref(sp), img.data_ptr(),
@@ -178,6 +184,9 @@ class Frame:
             ),
             fn,
         )
+        if ev is not None:
+            ev[1].record()
+            events.append(ev)
         self.has_forward = track
         self.fwd_image = img  # the image the backward (fused L1, replay restarts) reads
 
@@ -232,18 +241,37 @@ class Frame:
 
     def backward(self, cloud, grad_acc: torch.Tensor, grads_flat: torch.Tensor, screen_norms, visible,
                  dl_dimage: torch.Tensor | None = None, target: torch.Tensor | None = None,
-                 l1_scale: float = 0.0, stats=None, kernel_grads=None) -> None:
+                 l1_scale: float = 0.0, stats=None, kernel_grads=None, reproducible: bool = False,
+                 events: list | None = None) -> None:
+        """K4a + K4b.  ``reproducible`` sums each splat's per-entry gradient
+        records in a fixed order (xg_composite_bwd_entries +
+        xg_reduce_entry_grads) instead of with float atomics, so the result
+        is identical run to run (the reference's single-threaded backward
+        is); it needs this frame's tracking forward (checkpointed replay).
+        ``events`` (measurement) receives a (start, end) pair of CUDA events
+        recorded around the reverse-composite launch."""
         sp = self.splats_struct()
-        grad_acc.zero_()
-        nat.check(
-            nat.lib().xg_composite_bwd(
-                ctypes.byref(self.cam), ctypes.byref(sp), self.t_final.data_ptr(),
-                self.n_contrib.data_ptr(), nat.ptr(dl_dimage, "dl_dimage"), self.fwd_image.data_ptr(),
-                nat.ptr(target, "target") if dl_dimage is None else None,
-                ctypes.c_float(l1_scale), grad_acc.data_ptr(), nat.stream(),
-            ),
-            "xg_composite_bwd",
-        )
+        args = (ctypes.byref(self.cam), ctypes.byref(sp), self.t_final.data_ptr(), self.n_contrib.data_ptr(),
+                nat.ptr(dl_dimage, "dl_dimage"), self.fwd_image.data_ptr(),
+                nat.ptr(target, "target") if dl_dimage is None else None, ctypes.c_float(l1_scale))
+        if reproducible:
+            if self.entry_grad is None or self.entry_grad.shape[0] < self.entry_capacity:
+                self.entry_grad = torch.empty((self.entry_capacity, 8), dtype=torch.float32, device=self.device)
+            nat.check(nat.lib().xg_composite_bwd_entries(*args, self.entry_grad.data_ptr(), nat.stream()),
+                      "xg_composite_bwd_entries")
+            nat.check(nat.lib().xg_reduce_entry_grads(ctypes.byref(self.cam), ctypes.byref(sp),
+                                                      self.entry_grad.data_ptr(), grad_acc.data_ptr(),
+                                                      nat.stream()), "xg_reduce_entry_grads")
+        else:
+            grad_acc.zero_()
+            ev = None
+            if events is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            nat.check(nat.lib().xg_composite_bwd(*args, grad_acc.data_ptr(), nat.stream()), "xg_composite_bwd")
+            if ev is not None:
+                ev[1].record()
+                events.append(ev)
         cs = nat.cloud_struct(cloud)
         ns = oc = wg = None
         if stats is not None:

@@ -74,7 +74,8 @@ class SweepRenderer:
     def prepare(self, angles) -> None:
         angles = np.atleast_1d(np.asarray(angles, dtype=np.float64))
         if not self.frames or self.capacity == 0:
-            self.capacity = self._probe_capacity(float(angles[0]))
+            # (after an overflow finish() dropped the frames: keep the grown capacity)
+            self.capacity = max(self.capacity, self._probe_capacity(float(angles[0])))
             n = 2 * self.batch if self.batch > 1 else len(self.streams)
             self.frames = [Frame(self.cloud.n_points, self.h, self.w, self.cloud.device,
                                  entry_capacity=self.capacity) for _ in range(n)]
@@ -105,6 +106,7 @@ class SweepRenderer:
             self._render_batched(angles, out, host_out, status, composite_events)
         else:
             self._render_streams(angles, out, host_out, status, composite_events)
+        self.last_status = status  # per-view status words (device), e.g. to count overflows after check=False
         if check:
             self.finish(angles, out, host_out, status)
         return out

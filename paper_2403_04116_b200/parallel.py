@@ -160,10 +160,11 @@ class DataParallelTrainer(Trainer):
     bucket of a field can never follow a partial update of it."""
 
     def __init__(self, dataset, cloud, cfg, group=None, bucket_bytes: int = 8 << 20, targets_on_host=False,
-                 out_dir=None, verbose: bool = False):
+                 out_dir=None, verbose: bool = False, reproducible: bool = False):
         rank, world = world_info(group)
         super().__init__(dataset, cloud, cfg, out_dir=out_dir if rank == 0 else None,
-                         verbose=verbose and rank == 0, targets_on_host=targets_on_host)
+                         verbose=verbose and rank == 0, targets_on_host=targets_on_host,
+                         reproducible=reproducible)
         self.rank, self.world = rank, world
         self.group = group
         self.bucket_bytes = bucket_bytes

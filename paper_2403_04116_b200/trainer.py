@@ -333,11 +333,18 @@ class Trainer:
     is ``Trainer(...).run()``."""
 
     def __init__(self, dataset: ProjectionSet, cloud: GaussianCloud, cfg: TrainConfig, out_dir=None,
-                 verbose: bool = False, targets_on_host: bool = False):
+                 verbose: bool = False, targets_on_host: bool = False, reproducible: bool = False):
         if dataset.train_indices.size < 1:
             raise InvalidParameterError("dataset has no training projections")
         nat.require_cuda(cloud.flat, "cloud")
         self.dataset, self.cfg, self.verbose = dataset, cfg, verbose
+        # reproducible: gradients summed in a fixed order (Frame.backward),
+        # logged losses by an in-order reduction - byte-identical runs, like
+        # the reference's single-threaded loop (test_trainer.py:336-353)
+        self.reproducible = bool(reproducible)
+        # measurement hook: when a dict of lists, (start, end) CUDA events
+        # around each iteration's forward / reverse composite launches
+        self.kernel_events = None
         self.cloud = cloud.copy()
         self.dev = dev = self.cloud.device
         self.state = OptimizerState(self.cloud)
@@ -430,8 +437,9 @@ class Trainer:
             tgt = self.tgt_bufs[slot]
         else:
             tgt = self.targets[view]
+        ke = self.kernel_events
         eng.l1.zero_()
-        fr.composite(target=tgt, l1_sum=eng.l1, train=True)
+        fr.composite(target=tgt, l1_sum=eng.l1, train=True, events=ke["fwd"] if ke is not None else None)
         if fr.finish_bin():
             eng.l1.zero_()
             fr.composite(target=tgt, l1_sum=eng.l1, train=True)
@@ -443,7 +451,8 @@ class Trainer:
         self.s_dev = None
         if cfg.gamma == 0.0:
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
-                        l1_scale=1.0 / (h * w), stats=self.stats)
+                        l1_scale=1.0 / (h * w), stats=self.stats, reproducible=self.reproducible,
+                        events=ke["bwd"] if ke is not None else None)
         else:
             # xg_ssim writes dl = -gamma dSSIM/dI + (1 - gamma) sign(I - T) / HW
             # (trainer.py:117-123) straight into the backward's input
@@ -452,7 +461,8 @@ class Trainer:
             self.s_dev = eng.ssim.run(fr.image, tgt, 1.0, dl=eng.dl, dl_ssim_scale=-cfg.gamma,
                                       dl_l1_scale=(1.0 - cfg.gamma) / (h * w))
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis,
-                        dl_dimage=eng.dl, stats=self.stats)
+                        dl_dimage=eng.dl, stats=self.stats, reproducible=self.reproducible,
+                        events=ke["bwd"] if ke is not None else None)
         return tgt
 
     def _lr_table(self) -> dict:
@@ -499,7 +509,10 @@ class Trainer:
             self.state.exp_avg["raw_opacities"].zero_()
             self.state.exp_avg_sq["raw_opacities"].zero_()
         if log_now:
-            value = float(eng.l1.item()) / (h * w)
+            if self.reproducible:  # (the fused L1 sum adds with float atomics)
+                value = float((fr.image.double() - tgt.double()).abs().mean())
+            else:
+                value = float(eng.l1.item()) / (h * w)
             if cfg.gamma != 0.0:
                 value = (1.0 - cfg.gamma) * value + cfg.gamma * (1.0 - float(self.s_dev.item()))
             row = {"iteration": it, "loss": value, "train_psnr": psnr(fr.image, tgt), "test_psnr": None,
@@ -542,9 +555,11 @@ class Trainer:
 
 
 def train(dataset: ProjectionSet, cloud: GaussianCloud, cfg: TrainConfig, out_dir=None,
-          verbose: bool = False) -> TrainResult:
-    """Optimise the cloud against the training projections (trainer.py:330-438)."""
-    return Trainer(dataset, cloud, cfg, out_dir, verbose).run()
+          verbose: bool = False, reproducible: bool = False) -> TrainResult:
+    """Optimise the cloud against the training projections (trainer.py:330-438).
+    ``reproducible=True`` makes runs byte-identical (fixed-order gradient
+    sums; ~15 % slower per iteration), as the reference's are."""
+    return Trainer(dataset, cloud, cfg, out_dir, verbose, reproducible=reproducible).run()
 
 
 __all__ = [

@@ -1,0 +1,149 @@
+"""The reference's end-to-end acceptance gate on the GPU engine
+(pkg/tests/test_acceptance.py:187-267), same pipeline and bars:
+
+* data: ``xsplat gen-data`` defaults (cli.py:64-78, config.py:24-40,107-114):
+  the default phantom voxelised on the 64^3 grid of the 100 mm cube,
+  cone-beam projected at 100 angles onto a 64^2 detector (pitch 3 mm),
+  normalised, 3 % noise (seed 0), alternating train / test split;
+* model: ``xsplat train`` defaults (cli.py:81-114): ACUI cuboid init (grid
+  64, interval 8), N_f = 16, 5,000 iterations, TrainConfig defaults;
+* bars: held-out PSNR >= 30 dB and SSIM >= 0.90 on the clean test views
+  (the reference's wall-time bar is 30 min; here it is seconds);
+  convergence: held-out PSNR +3 dB from iteration 200 to 2,000;
+  ablations: N_f = 16 beats N_f = 1 by >= 1 dB and the cuboid init is not
+  worse than the random init (same data, 5,000 iterations each).
+The determinism check of the reference (byte-identical checkpoints across
+runs, test_acceptance.py:252-267) runs with ``reproducible=True`` (fixed-
+order gradient sums); the default mode's backward sums with float atomics,
+so its re-runs are only bounded in final quality."""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ITERATIONS = 5000
+
+
+def _data():
+    import paper_2403_04116_b200 as xg
+    from paper_2403_04116_b200.dataset import add_noise, make_projection_set
+    from paper_2403_04116_b200.phantom import default_phantom_primitives, make_phantom
+
+    sc = xg.ScannerConfig(1000.0, 1500.0, 64, 64, 3.0, xg.equal_interval_angles(100))
+    extent = np.full(3, 100.0)
+    ph = make_phantom(default_phantom_primitives(tuple(extent)), (64, 64, 64), extent / 64)
+    return add_noise(make_projection_set(ph, sc), 0.03, 0)
+
+
+def _train(ds, out, n_features=16, init="cuboid", iterations=ITERATIONS, reproducible=False):
+    from paper_2403_04116_b200 import acui
+    from paper_2403_04116_b200.trainer import TrainConfig, evaluate, train
+
+    cloud = acui.init_alternative(init, acui.CuboidSpec((100.0,) * 3, (64,) * 3), n_features, 0,
+                                  basis_weights=np.ones(n_features), device="cuda")
+    res = train(ds, cloud, TrainConfig(iterations=iterations), out_dir=out, reproducible=reproducible)
+    from paper_2403_04116_b200.cloudio import load_cloud
+
+    final = load_cloud(out / "cloud_final.ply", device="cuda")
+    return res, evaluate(final, ds, ds.test_indices)
+
+
+@pytest.fixture(scope="module")
+def e2e(tmp_path_factory):
+    import torch
+
+    torch.cuda.set_device(0)
+    root = tmp_path_factory.mktemp("e2e")
+    t0 = time.perf_counter()
+    ds = _data()
+    res, report = _train(ds, root / "out")
+    return {"ds": ds, "res": res, "report": report, "elapsed": time.perf_counter() - t0, "root": root}
+
+
+def _read_metrics(path):
+    rows = []
+    with open(path) as fh:
+        header = fh.readline().strip().split("\t")
+        for line in fh:
+            cells = line.strip().split("\t")
+            rows.append({k: (None if v == "-" else float(v)) for k, v in zip(header, cells)})
+    return rows
+
+
+def _held_out_at(rows, it):
+    for r in rows:
+        if r["iteration"] == it:
+            assert r["test_psnr"] is not None, f"no eval at iteration {it}"
+            return r["test_psnr"]
+    raise AssertionError(f"iteration {it} not in metrics log")
+
+
+def test_held_out_quality_and_wall_time(e2e):
+    r = e2e["report"]
+    print(f"\nend to end: test PSNR {r.psnr:.2f} dB, SSIM {r.ssim:.4f}, wall {e2e['elapsed']:.1f} s, "
+          f"N {e2e['res'].cloud.n_points}")
+    assert r.psnr >= 30.0
+    assert r.ssim >= 0.90
+    assert e2e["elapsed"] <= 30 * 60
+
+
+def test_convergence_trend(e2e):
+    rows = _read_metrics(e2e["root"] / "out" / "metrics.tsv")
+    early, late = _held_out_at(rows, 200), _held_out_at(rows, 2000)
+    print(f"\nconvergence: test PSNR {early:.2f} dB @200 -> {late:.2f} dB @2000")
+    assert late >= early + 3.0
+
+
+def test_ablation_directions(e2e, tmp_path):
+    """The three runs in reproducible mode (fixed outcomes), next to the
+    reference's own numbers for the same runs (tests/golden/acceptance_ref.json,
+    make_golden_acceptance.py: 41.82 / 40.68 / 41.69 dB)."""
+    import json
+    from pathlib import Path
+
+    ref = {(r["nf"], r["init"]): r["psnr"] for r in
+           json.loads((Path(__file__).resolve().parent / "golden" / "acceptance_ref.json").read_text())}
+    _, base = _train(e2e["ds"], tmp_path / "nf16", reproducible=True)
+    _, nf1 = _train(e2e["ds"], tmp_path / "nf1", n_features=1, reproducible=True)
+    _, rnd = _train(e2e["ds"], tmp_path / "random", init="random", reproducible=True)
+    print(f"\nablations: nf16_cuboid {base.psnr:.2f} dB (reference {ref[(16, 'cuboid')]:.2f}), "
+          f"nf1 {nf1.psnr:.2f} dB (reference {ref[(1, 'cuboid')]:.2f}), "
+          f"random_init {rnd.psnr:.2f} dB (reference {ref[(16, 'random')]:.2f})")
+    assert base.psnr >= nf1.psnr + 1.0
+    assert base.psnr >= rnd.psnr
+    for got, key in ((base, (16, "cuboid")), (nf1, (1, "cuboid")), (rnd, (16, "random"))):
+        assert abs(got.psnr - ref[key]) < 1.0, (key, got.psnr, ref[key])
+
+
+def test_rerun_spread(e2e, tmp_path):
+    """Default (fast) mode: the backward sums with float atomics, so re-runs
+    of the same training differ by summation order, amplified over 5,000
+    Adam steps and 24 density-control events (measured: 41.62 .. 42.22 dB);
+    every run clears the quality bar."""
+    _, a = _train(e2e["ds"], tmp_path / "r1")
+    _, b = _train(e2e["ds"], tmp_path / "r2")
+    ps = [e2e["report"].psnr, a.psnr, b.psnr]
+    print(f"\nre-runs: test PSNR {ps}")
+    assert max(ps) - min(ps) < 1.5
+    assert min(ps) >= 30.0
+
+
+def test_checkpoints_and_logs_byte_identical(e2e, tmp_path):
+    """test_acceptance.py:252-267 with train(..., reproducible=True): 600
+    iterations (crossing the density-control window), twice; the final
+    cloud and the metrics log must be byte-identical."""
+    from paper_2403_04116_b200 import acui
+    from paper_2403_04116_b200.trainer import TrainConfig, train
+
+    for name in ("r1", "r2"):
+        cloud = acui.init_alternative("cuboid", acui.CuboidSpec((100.0,) * 3, (64,) * 3), 16, 0, device="cuda")
+        train(e2e["ds"], cloud, TrainConfig(iterations=600), out_dir=tmp_path / name, reproducible=True)
+    for fname in ("cloud_final.ply", "metrics.tsv"):
+        a = (tmp_path / "r1" / fname).read_bytes()
+        b = (tmp_path / "r2" / fname).read_bytes()
+        assert a == b, f"{fname} differs between identical runs"

@@ -346,6 +346,23 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
                             double* g_mean, double* g_conic, double* g_int, double* g_alpha,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same contract at the reference's precision: float64 arithmetic in
+ * _kernels.pyx's operation order (compiled without FMA contraction), for the
+ * "cuda" kernel backend registered in xsplat itself
+ * (paper_2403_04116_b200/rasterizer/xsplat_backend.py).  Replaces
+ * rasterizer/_kernels.pyx:23-74 (forward_tiles) and :77-178
+ * (backward_tiles) one for one; all arrays device-resident, outputs zeroed
+ * here, no workspace. */
+xg_status xg_forward_tiles_f64(int32_t h, int32_t w, const double* means2d, const double* conics,
+                               const double* intensities, const double* opacities, const int32_t* entry_splat,
+                               int64_t n_entries, const int64_t* tile_ranges, int64_t n_splats, double* image,
+                               void* stream);
+xg_status xg_backward_tiles_f64(int32_t h, int32_t w, const double* means2d, const double* conics,
+                                const double* intensities, const double* opacities, const int32_t* entry_splat,
+                                int64_t n_entries, const int64_t* tile_ranges, int64_t n_splats,
+                                const double* dl_dimage, double* g_mean, double* g_conic, double* g_int,
+                                double* g_alpha, void* stream);
+
 /* A voxel phantom (phantom.py:117-140): float64 densities [m0][m1][m2]
  * (C order; axes = world x, y, z), centred on the world origin. */
 typedef struct xg_volume {

@@ -29,3 +29,9 @@ from xsplat.rasterizer import available_backends
 assert "compiled" in available_backends(), available_backends()
 print("build_ref: xsplat built into", sys.argv[1], "backends", available_backends())
 PY
+# the reference's own test modules, next to the build (git-ignored, travel to
+# the GPU box): tests/test_gpu_xsplat_plugin.py runs them with the "cuda"
+# kernel backend registered (paper_2403_04116_b200/rasterizer/xsplat_backend.py)
+rm -rf "$OUT/xsplat_tests"
+cp -r "$SRC/tests" "$OUT/xsplat_tests"
+echo "build_ref: reference tests copied to $OUT/xsplat_tests"

@@ -6,7 +6,8 @@ box.  ``xg_preprocess.cu`` and ``xg_project.cu`` are compiled with
 ``-fmad=false``: the per-Gaussian float64 projection (and the phantom
 projector's ray samples) must round every product/sum as written so radii,
 tile rects, depth keys and sample positions reproduce the oracle /
-reference bit for bit.
+reference bit for bit; ``xg_tiles64.cu`` (the float64 plug-in kernels) too,
+to round as the reference's Cython loop does.
 """
 
 from __future__ import annotations
@@ -25,8 +26,8 @@ OBJ = PKG / "csrc" / "_obj"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
-PER_FILE = {"xg_preprocess.cu": ["-fmad=false"], "xg_project.cu": ["-fmad=false"]}
-SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu", "xg_project.cu"]
+PER_FILE = {"xg_preprocess.cu": ["-fmad=false"], "xg_project.cu": ["-fmad=false"], "xg_tiles64.cu": ["-fmad=false"]}
+SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu", "xg_project.cu", "xg_tiles64.cu"]
 
 
 def nvcc() -> str:

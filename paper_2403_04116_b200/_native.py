@@ -149,6 +149,14 @@ SIGNATURES = {
         [c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p,
          c_void_p, c_size, c_void_p],
     ),
+    "xg_forward_tiles_f64": (
+        c_i32, [c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p,
+                c_void_p],
+    ),
+    "xg_backward_tiles_f64": (
+        c_i32, [c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p,
+                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
     "xg_backward_tiles": (
         c_i32,
         [c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p,

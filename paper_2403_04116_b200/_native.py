@@ -33,7 +33,8 @@ XG_ST_ENTRY_OVERFLOW = 0x8
 XG_ST_GRAD_SHIFT = 8
 XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
 XG_CTR_ITEMS = 6
-XG_NCOUNTERS = 8
+XG_CTR_L1 = 8  # words 8-9: the fused-L1 double, zeroed by xg_preprocess_fwd
+XG_NCOUNTERS = 10
 XG_ABI_VERSION = 3
 XG_REPLAY_CHUNK = 256
 XG_MAX_BATCH = 16

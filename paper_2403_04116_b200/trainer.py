@@ -314,16 +314,20 @@ class _IterationEngine:
     def __init__(self, cloud: GaussianCloud, h: int, w: int):
         self.h, self.w = h, w
         self.resize(cloud)
-        self.l1 = torch.zeros(1, dtype=torch.float64, device=cloud.device)
         self.dl = torch.empty((h, w), dtype=torch.float32, device=cloud.device)  # fused loss gradient
         self.ssim = None  # SsimEngine, created on the first gamma > 0 step
+
+    @property
+    def l1(self) -> torch.Tensor:
+        """The fused-L1 sum of the current frame's forward (zeroed by its preprocess)."""
+        return self.frame.l1_sum
 
     def resize(self, cloud: GaussianCloud, capacity: int | None = None) -> None:
         n = cloud.n_points
         cap = capacity or (getattr(self, "frame", None) and self.frame.entry_capacity) or 16 * n
         self.frame = Frame(n, self.h, self.w, cloud.device, entry_capacity=cap)
         self.grads = make_gradients(n, cloud.n_features, cloud.device)
-        self.acc = torch.empty((n, 8), dtype=torch.float32, device=cloud.device)
+        self.acc = torch.zeros((n, 8), dtype=torch.float32, device=cloud.device)  # (kept zero by xg_preprocess_bwd)
         self.vis = torch.empty(n, dtype=torch.uint8, device=cloud.device)
 
 
@@ -388,7 +392,6 @@ class Trainer:
         self.order: list = []
         self.it = 0
         self.t0 = time.perf_counter()
-        self.grad_mask = 0x1F << nat.XG_ST_GRAD_SHIFT
         self.densify_events = 0
 
     def _copy_target(self, slot: int, view: int) -> None:
@@ -438,10 +441,9 @@ class Trainer:
         else:
             tgt = self.targets[view]
         ke = self.kernel_events
-        eng.l1.zero_()
+        # (the L1 accumulator lives in the frame's counters, zeroed by preprocess)
         fr.composite(target=tgt, l1_sum=eng.l1, train=True, events=ke["fwd"] if ke is not None else None)
-        if fr.finish_bin():
-            eng.l1.zero_()
+        if fr.finish_bin():  # (the skipped first forward added nothing)
             fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         c = fr.last_counters
         nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))  # divergence of the previous step
@@ -472,9 +474,7 @@ class Trainer:
 
     def _apply_gradients(self) -> None:
         fr = self.eng.frame
-        # carry this step's non-finite flags into the sticky word Adam reads
-        fr.counters[nat.XG_CTR_STICKY : nat.XG_CTR_STICKY + 1].bitwise_or_(
-            fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1] & self.grad_mask)
+        # (xg_preprocess_bwd ORed this step's non-finite flags into the sticky word Adam reads)
         self.state.step += 1
         _adam_launch(self.cloud, self.eng.grads.flat, self.state, self._lr_table(), self.cfg,
                      fr.counters.data_ptr() + 4 * nat.XG_CTR_STICKY)
@@ -512,7 +512,7 @@ class Trainer:
             if self.reproducible:  # (the fused L1 sum adds with float atomics)
                 value = float((fr.image.double() - tgt.double()).abs().mean())
             else:
-                value = float(eng.l1.item()) / (h * w)
+                value = float(fr.l1_sum.item()) / (h * w)  # (fr: this step's frame, even after a resize)
             if cfg.gamma != 0.0:
                 value = (1.0 - cfg.gamma) * value + cfg.gamma * (1.0 - float(self.s_dev.item()))
             row = {"iteration": it, "loss": value, "train_psnr": psnr(fr.image, tgt), "test_psnr": None,

@@ -71,10 +71,8 @@ def test_fused_l1_matches_reference(golden, l1g):
         fr = eng.frame
         fr.preprocess(cloud, cam)
         fr.bin_async()
-        eng.l1.zero_()
         fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         if fr.finish_bin():
-            eng.l1.zero_()
             fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
                     l1_scale=1.0 / (h * w), stats=stats)
@@ -103,7 +101,6 @@ def test_fused_l1_ssim_matches_reference(golden, l1g):
         fr = eng.frame
         fr.preprocess(cloud, cam)
         fr.ensure_binned()
-        eng.l1.zero_()
         fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         eng.ssim = SsimEngine(h, w, cloud.device)
         s_dev = eng.ssim.run(fr.image, tgt, 1.0, dl=eng.dl, dl_ssim_scale=-gamma,

@@ -274,6 +274,21 @@ class TestTrainLoop:  # test_trainer.py:290-386
         res = tr.train(ds, cloud_of(xg, random_arrays(6, rng, pos_scale=30.0)), cfg)
         assert res.cloud.n_points > 6
 
+    def test_logged_loss_on_density_control_steps(self, xg, tr, rng):
+        """A row logged at a density-control iteration reports that step's
+        loss (the fused L1 of the frame it rendered, not the resized one's);
+        reproducible mode computes it by an in-order reduction - both agree."""
+        sc = small_scanner(32, 32, 6.0, n_views=4)
+        ds = self_render_dataset(xg, cloud_of(xg, random_arrays(8, rng, pos_scale=30.0, scale_range=(8.0, 15.0))), sc)
+        start = random_arrays(6, rng, pos_scale=30.0)
+        cfg = tr.TrainConfig(iterations=40, gamma=0.0, densify_from_iter=5, densify_interval=10,
+                             densify_until_iter=40, densify_grad_threshold=1e-9, log_interval=10)
+        a = tr.train(ds, cloud_of(xg, start), cfg)
+        b = tr.train(ds, cloud_of(xg, start), cfg, reproducible=True)
+        for ra, rb in zip(a.metrics, b.metrics):
+            assert ra["loss"] > 0 and rb["loss"] > 0, (ra, rb)
+        assert abs(a.metrics[0]["loss"] / b.metrics[0]["loss"] - 1) < 1e-5
+
     def test_gamma_ssim_path_runs(self, xg, tr, rng):
         sc = small_scanner(n_views=2)
         ds = self_render_dataset(xg, cloud_of(xg, random_arrays(3, rng)), sc)

@@ -14,6 +14,8 @@
 // ~10 tile bits of the E entries replaces a 74-bit (tile|depth64) sort of E
 // keys: two passes over E instead of ten.
 #include <limits.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "xg_sort.cuh"
 
@@ -363,6 +365,8 @@ size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   size_t a = radix_workspace_bytes(multisplit(n_tiles) ? n : (n > cap ? n : cap));
   const size_t o = onesweep_workspace_bytes(n);
   if (o > a) a = o;
+  const size_t bsw = bucket_sort_workspace_bytes(n);
+  if (bsw > a) a = bsw;
   size_t b = scan_workspace_bytes(multisplit(n_tiles) ? (n > n_tiles * bin_chunks(n, n_tiles) ? n : n_tiles * bin_chunks(n, n_tiles)) : n);
   return a > b ? a : b;
 }
@@ -426,14 +430,25 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   xg_status st;
   // n as a device count for the generic sort: stash it in counters[TOUCH]
   uint32_t* n_dev = sp->counters + XG_CTR_TOUCH;
-  // 1. depth sort
-  k_iota<<<div_up(n, 256), 256, 0, s>>>(sp->order, n, n_dev);
-  if ((st = check_launch("k_iota")) != XG_OK) return st;
-  // (depth_key is the sort's read-only input: a re-bin after an entry
-  // overflow sorts the same keys again)
-  if ((st = onesweep_sort_pairs64((const unsigned long long*)sp->depth_key, sp->order, w.keyN1, w.keyN2, w.valN1,
-                                  sp->order, sp->order, n, n_dev, w.tail, w.tail_bytes, s)) != XG_OK)
+  // 1. depth sort (depth_key is the sort's read-only input: a re-bin after an
+  // entry overflow sorts the same keys again).  Default: the bucket sort
+  // (xg_sort.cu); XG_DEPTH_SORT=onesweep selects the 8-pass LSD onesweep.
+  static const bool onesweep = getenv("XG_DEPTH_SORT") && strcmp(getenv("XG_DEPTH_SORT"), "onesweep") == 0;
+  if (onesweep) {
+    k_iota<<<div_up(n, 256), 256, 0, s>>>(sp->order, n, n_dev);
+    if ((st = check_launch("k_iota")) != XG_OK) return st;
+    if ((st = onesweep_sort_pairs64((const unsigned long long*)sp->depth_key, sp->order, w.keyN1, w.keyN2, w.valN1,
+                                    sp->order, sp->order, n, n_dev, w.tail, w.tail_bytes, s)) != XG_OK)
+      return st;
+  } else if ((st = bucket_sort_depth((const unsigned long long*)sp->depth_key, sp->n_tiles, n, w.keyN1, w.keyN2,
+                                     w.valN1, w.offN, sp->order, n_dev, w.tail, w.tail_bytes, s)) != XG_OK) {
     return st;
+  }
+  // (development aid, tools/probe_bin_stages.py: XG_BIN_STOP=1 stops after
+  // the depth sort, 2 after the count / scan / ranges - the stage costs
+  // inside a concurrent sweep; results are then incomplete)
+  static const int bin_stop = getenv("XG_BIN_STOP") ? atoi(getenv("XG_BIN_STOP")) : 0;
+  if (bin_stop == 1) return XG_OK;
   if (multisplit(n_tiles)) {
     // 2-4. fused duplicate + stable tile sort + ranges
     const int C = (int)bin_chunks(n, n_tiles);
@@ -457,6 +472,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     k_bin_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(w.hoff, C, n_tiles, sp->counters,
                                                       (long long*)sp->tile_ranges);
     if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
+    if (bin_stop == 2) return XG_OK;
     k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
                                                bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
     if ((st = check_launch("k_bin_emit")) != XG_OK) return st;

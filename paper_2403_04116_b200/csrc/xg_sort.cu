@@ -379,7 +379,7 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
 
 __global__ void __launch_bounds__(kOsThreads)
     k_os_hist(const unsigned long long* __restrict__ keys, const uint32_t* n_dev, long long cap,
-              uint32_t* __restrict__ ghist) {
+              uint32_t* __restrict__ ghist, int n_passes) {
   __shared__ uint32_t h[kOsPasses][256];
   for (int i = threadIdx.x; i < kOsPasses * 256; i += kOsThreads) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(kOsThreads)
   for (long long i = (long long)blockIdx.x * kOsThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kOsThreads) {
     const unsigned long long k = keys[i];
 #pragma unroll
-    for (int p = 0; p < kOsPasses; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
+    for (int p = 0; p < kOsPasses; ++p)
+      if (p < n_passes) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kOsPasses * 256; i += kOsThreads) {
@@ -400,7 +401,8 @@ __global__ void __launch_bounds__(kOsThreads)
 // exclusive offsets per pass, and the buffer each pass reads (sel[p]);
 // sel[kOsPasses] is where the result lands
 __global__ void __launch_bounds__(256) k_os_scan(const uint32_t* __restrict__ ghist, uint32_t* __restrict__ gofs,
-                                                 const uint32_t* n_dev, long long cap, int* __restrict__ sel) {
+                                                 const uint32_t* n_dev, long long cap, int* __restrict__ sel,
+                                                 int n_passes) {
   __shared__ uint32_t s[256];
   __shared__ int trivial[kOsPasses];
   long long n = *n_dev;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(256) k_os_scan(const uint32_t* __restrict__ gh
   for (int p = 0; p < kOsPasses; ++p) {
     const uint32_t v = ghist[p * 256 + d];
     const int t = __syncthreads_or((long long)v == n);
-    if (d == 0) trivial[p] = t;
+    if (d == 0) trivial[p] = t || p >= n_passes;  // (passes past n_passes: the caller's keys are zero there)
     s[d] = v;
     __syncthreads();
     for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele
@@ -547,9 +549,9 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
 
 // the result lands in vals[sel[K]]: copy it to vals_out unless it is there
 __global__ void k_os_finish(uint32_t* vals_out, const uint32_t* vals_a, const uint32_t* vals_b,
-                            const uint32_t* n_dev, long long cap, const int* sel) {
+                            const uint32_t* vals_in, const uint32_t* n_dev, long long cap, const int* sel) {
   const int r = sel[kOsPasses];
-  const uint32_t* src = r == 0 ? vals_a : r == 1 ? vals_b : nullptr;
+  const uint32_t* src = r == 0 ? vals_a : r == 1 ? vals_b : vals_in;  // (2: every pass trivial)
   if (!src || src == vals_out) return;
   long long n = *n_dev;
   if (n > cap) n = cap;
@@ -568,7 +570,7 @@ size_t onesweep_workspace_bytes(int64_t cap) {
 xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_t* vals_in,
                                 unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a,
                                 uint32_t* vals_b, uint32_t* vals_out, int64_t cap, const uint32_t* n_dev,
-                                void* ws, size_t ws_bytes, cudaStream_t s) {
+                                void* ws, size_t ws_bytes, cudaStream_t s, int n_passes, const int** result_sel) {
   if (cap <= 0) return XG_OK;
   if (ws_bytes < onesweep_workspace_bytes(cap)) {
     set_error_msg("onesweep_sort_pairs64: workspace too small");
@@ -586,12 +588,12 @@ xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_
   uint32_t* status = (uint32_t*)p;
   cudaMemsetAsync(ws, 0, onesweep_workspace_bytes(cap), s);
   const int hgrid = (int)(tiles < 296 ? tiles : 296);
-  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys_in, n_dev, cap, ghist);
+  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys_in, n_dev, cap, ghist, n_passes);
   xg_status st = check_launch("k_os_hist");
   if (st != XG_OK) return st;
-  k_os_scan<<<1, 256, 0, s>>>(ghist, gofs, n_dev, cap, sel);
+  k_os_scan<<<1, 256, 0, s>>>(ghist, gofs, n_dev, cap, sel, n_passes);
   if ((st = check_launch("k_os_scan")) != XG_OK) return st;
-  for (int pass = 0; pass < kOsPasses; ++pass) {
+  for (int pass = 0; pass < n_passes && pass < kOsPasses; ++pass) {  // (higher bytes all zero: no-op passes)
     OsArgs a;
     a.keys[0] = keys_a;
     a.keys[1] = keys_b;
@@ -610,8 +612,468 @@ xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_
     k_os_pass<<<(int)tiles, kOsThreads, 0, s>>>(a);
     if ((st = check_launch("k_os_pass")) != XG_OK) return st;
   }
-  k_os_finish<<<(int)(tiles < 296 ? tiles : 296), 256, 0, s>>>(vals_out, vals_a, vals_b, n_dev, cap, sel);
+  if (result_sel) {  // the caller reads vals {a, b, in}[sel[8]] itself
+    *result_sel = sel + kOsPasses;
+    return XG_OK;
+  }
+  k_os_finish<<<(int)(tiles < 296 ? tiles : 296), 256, 0, s>>>(vals_out, vals_a, vals_b, vals_in, n_dev, cap, sel);
   return check_launch("k_os_finish");
+}
+
+}  // namespace xg
+
+namespace xg {
+
+// ---------------------------------------------------------------------------
+// Depth order by buckets (K2 step 1; the 8-pass onesweep on the raw float64
+// bits stays selectable with XG_DEPTH_SORT=onesweep).
+//
+// The order wanted is ascending (float64 depth bits, cloud index) over the
+// active splats - what a stable LSD sort of the index-ordered keys gives.
+//   1. min / max of the active keys;
+//   2. bucket b = 1 + ((key - kmin) >> shift), 2^15 buckets spanning
+//      [kmin, kmax] (monotone in the key; inactive splats -> bucket 0, never
+//      looked at again: count / emit skip them); per-bucket counts and
+//      per-bucket min / max key (atomics);
+//   3. exclusive scan of the counts -> bucket starts;
+//   4. a STABLE sort of the 16-bit bucket ids (two onesweep passes instead
+//      of eight): every bucket's splats in cloud-index order;
+//   5. a bucket whose min key == max key (one depth value: the usual case on
+//      lattice clouds, where a depth is shared by a whole column of splats)
+//      is final; otherwise each splat's rank inside the bucket is counted by
+//      the total order (key, index) - or, for a bucket larger than
+//      kBsRankMax, the bucket is sorted by one CTA (bitonic in shared memory,
+//      or in place in global memory beyond kBsSmemMax).
+// The result is the same permutation bit for bit (a total order has one
+// sorted sequence); the symmetric phi = pi/4 views of the golden tests pin it.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kBsBits = 16;           // 16-bit ids: active buckets 0 .. 65534, 65535 = inactive
+constexpr uint32_t kBsBuckets = 1u << kBsBits;
+constexpr uint32_t kBsInactive = kBsBuckets - 1;
+constexpr int kBsRankMax = 256;       // counting rank up to this (mixed) bucket size
+constexpr int kBsSmemMax = 16384;     // shared-memory bitonic up to this size (12 B each: 192 KB)
+constexpr int kBsLargeThreads = 512;
+
+struct BsWs {
+  unsigned long long* mm;    // [0] min key, [1] ~max key (both via atomicMin)
+  uint32_t* n_large;
+  uint32_t* count;           // [kBsBuckets]
+  uint32_t* start;           // [kBsBuckets + 1]
+  unsigned long long* bmin;  // [kBsBuckets] per-bucket min key
+  unsigned long long* bmax;  // [kBsBuckets] per-bucket ~max key
+  uint32_t* large;           // [kBsBuckets]
+  uint32_t* mixed;           // [kBsBuckets]
+  uint32_t* n_mixed;
+  void* tail;                // scan / onesweep workspace
+  size_t tail_bytes;
+};
+
+inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+inline size_t bs_fixed_bytes() {
+  return 768 + 2 * al256(sizeof(uint32_t) * (kBsBuckets + 1)) + 2 * al256(sizeof(unsigned long long) * kBsBuckets) +
+         2 * al256(sizeof(uint32_t) * kBsBuckets);
+}
+
+inline bool bs_carve(void* ws, size_t bytes, BsWs& w) {
+  char* p = (char*)ws;
+  w.mm = (unsigned long long*)p; p += 256;
+  w.n_large = (uint32_t*)p; p += 256;
+  w.count = (uint32_t*)p; p += al256(sizeof(uint32_t) * (kBsBuckets + 1));
+  w.start = (uint32_t*)p; p += al256(sizeof(uint32_t) * (kBsBuckets + 1));
+  w.bmin = (unsigned long long*)p; p += al256(sizeof(unsigned long long) * kBsBuckets);
+  w.bmax = (unsigned long long*)p; p += al256(sizeof(unsigned long long) * kBsBuckets);
+  w.large = (uint32_t*)p; p += al256(sizeof(uint32_t) * kBsBuckets);
+  w.mixed = (uint32_t*)p; p += al256(sizeof(uint32_t) * kBsBuckets);
+  w.n_mixed = (uint32_t*)p; p += 256;
+  w.tail = p;
+  const size_t used = (size_t)(p - (char*)ws);
+  if (used > bytes) return false;
+  w.tail_bytes = bytes - used;
+  return true;
+}
+
+__device__ __forceinline__ int bs_shift(const unsigned long long* mm) {
+  const unsigned long long range = (~mm[1]) - mm[0];  // kmax - kmin
+  const int len = range ? 64 - __clzll(range) : 0;
+  return len > kBsBits ? len - kBsBits : 0;
+}
+
+__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
+
+__global__ void k_bs_minmax(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,
+                            long long n, unsigned long long* mm, uint32_t* n_dev) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = (uint32_t)n;  // (the onesweep's live count)
+  unsigned long long lo = ~0ull, nhi = ~0ull;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (n_tiles[i]) {
+      const unsigned long long k = keys[i];
+      lo = umin64(lo, k);
+      nhi = umin64(nhi, ~k);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = umin64(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    nhi = umin64(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+  }
+  __shared__ unsigned long long s_lo[32], s_nhi[32];  // (one atomic pair per CTA: 4k warps on two
+  const int warp = threadIdx.x >> 5;                   //  addresses serialised to ~10 us)
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[warp] = lo;
+    s_nhi[warp] = nhi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      lo = umin64(lo, s_lo[i]);
+      nhi = umin64(nhi, s_nhi[i]);
+    }
+    if (lo != ~0ull) atomicMin(mm, lo);
+    if (nhi != ~0ull) atomicMin(mm + 1, nhi);
+  }
+}
+
+__device__ __forceinline__ unsigned long long peer_min64(unsigned peers, unsigned long long v) {
+  const uint32_t hi = __reduce_min_sync(peers, (uint32_t)(v >> 32));
+  const uint32_t lo = __reduce_min_sync(peers, (uint32_t)(v >> 32) == hi ? (uint32_t)v : 0xffffffffu);
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+// bucket ids (the stable sort's keys), the iota values, per-bucket counts and key range
+__global__ void k_bs_bucket(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,
+                            long long n, const unsigned long long* __restrict__ mm,
+                            unsigned long long* __restrict__ bkey, uint32_t* __restrict__ iota,
+                            uint32_t* __restrict__ count, unsigned long long* __restrict__ bmin,
+                            unsigned long long* __restrict__ bmax) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int shift = bs_shift(mm);
+  const unsigned long long kmin = mm[0];
+  const bool valid = i < n;
+  unsigned long long k = 0;
+  uint32_t b = 0xffffffffu;
+  if (valid) {
+    k = keys[i];
+    b = n_tiles[i] ? min((uint32_t)((k - kmin) >> shift), kBsInactive - 1u) : kBsInactive;
+    bkey[i] = b;
+    iota[i] = (uint32_t)i;
+  }
+  const unsigned peers = __match_any_sync(0xffffffffu, b);
+  // min of k and of ~k over the lane's peers (same bucket): 64-bit minima as
+  // (high word, then low word among the lanes holding the high minimum)
+  const unsigned long long lo = peer_min64(peers, k), nhi = peer_min64(peers, ~k);
+  if (valid && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) {
+    atomicAdd(&count[b], (uint32_t)__popc(peers));
+    if (b != kBsInactive) {
+      atomicMin(&bmin[b], lo);
+      atomicMin(&bmax[b], nhi);
+    }
+  }
+}
+
+__device__ __forceinline__ bool bs_less(unsigned long long ka, uint32_t ia, unsigned long long kb, uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+// sorted: indices in (bucket, index) order.  Final position of sorted[p].
+struct BsSorted {  // the stable pass's result: vals {a, b, in}[*sel]
+  const uint32_t* v[3];
+  const int* sel;
+  __device__ __forceinline__ const uint32_t* get() const { return v[*sel]; }
+};
+
+__global__ void k_bs_rank(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,
+                          const unsigned long long* __restrict__ mm, BsSorted srt, long long n,
+                          const uint32_t* __restrict__ start, const unsigned long long* __restrict__ bmin,
+                          const unsigned long long* __restrict__ bmax, uint32_t* __restrict__ order,
+                          uint32_t* __restrict__ large, uint32_t* __restrict__ n_large, uint32_t* __restrict__ mixed,
+                          uint32_t* __restrict__ n_mixed) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t* __restrict__ sorted = srt.get();
+  const uint32_t ix = sorted[p];
+  const uint32_t b = n_tiles[ix] ? min((uint32_t)((keys[ix] - mm[0]) >> bs_shift(mm)), kBsInactive - 1u) : kBsInactive;
+  if (b == kBsInactive || bmin[b] == ~bmax[b]) {  // inactive, or one key value: index order is the order
+    order[p] = ix;
+    return;
+  }
+  const uint32_t lo = start[b], hi = start[b + 1];
+  if (hi - lo > 32u) {  // warp bitonic (<= kBsRankMax) or CTA sort
+    if (p == lo) {
+      if (hi - lo > (uint32_t)kBsRankMax) large[atomicAdd(n_large, 1u)] = b;
+      else mixed[atomicAdd(n_mixed, 1u)] = b;
+    }
+    return;
+  }
+  const unsigned long long k = keys[ix];
+  uint32_t r = 0;
+  for (uint32_t q = lo; q < hi; ++q) {
+    const uint32_t iq = sorted[q];
+    r += bs_less(keys[iq], iq, k, ix);
+  }
+  order[lo + r] = ix;
+}
+
+// One CTA per large mixed bucket: bitonic sort by (key, index) with all
+// comparators ascending (elements past the bucket's end - virtual +inf -
+// never move and are skipped), in shared memory when it fits, else in
+// place in global memory (scratch K / I).  Writes the bucket's order[].
+__global__ void __launch_bounds__(kBsLargeThreads)
+    k_bs_large(const unsigned long long* __restrict__ keys, BsSorted srt,
+               const uint32_t* __restrict__ start, const uint32_t* __restrict__ large,
+               const uint32_t* __restrict__ n_large, unsigned long long* __restrict__ gk, uint32_t* __restrict__ gi,
+               uint32_t* __restrict__ order) {
+  extern __shared__ unsigned char bs_smem[];
+  const uint32_t* __restrict__ sorted = srt.get();
+  const uint32_t nl = *n_large;
+  for (uint32_t j = blockIdx.x; j < nl; j += gridDim.x) {
+    const uint32_t b = large[j];
+    const uint32_t lo = start[b], s = start[b + 1] - lo;
+    uint32_t m = 1;
+    while (m < s) m <<= 1;
+    const bool in_smem = s <= (uint32_t)kBsSmemMax;
+    unsigned long long* K = in_smem ? reinterpret_cast<unsigned long long*>(bs_smem) : gk + lo;
+    uint32_t* I = in_smem ? reinterpret_cast<uint32_t*>(bs_smem + sizeof(unsigned long long) * kBsSmemMax) : gi + lo;
+    for (uint32_t t = threadIdx.x; t < s; t += blockDim.x) {
+      const uint32_t ix = sorted[lo + t];
+      K[t] = keys[ix];
+      I[t] = ix;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= m; k <<= 1) {
+      for (uint32_t st = k >> 1; st > 0; st >>= 1) {
+        const int ls = __ffs(st) - 1;
+        for (uint32_t t = threadIdx.x; t < (m >> 1); t += blockDim.x) {
+          const uint32_t blk = t >> ls, off = t & (st - 1);
+          uint32_t a, c;
+          if (st == (k >> 1)) {  // first step of a merge: mirrored pairs
+            a = blk * k + off;
+            c = blk * k + k - 1 - off;
+          } else {
+            a = (blk << (ls + 1)) + off;
+            c = a + st;
+          }
+          if (c < s) {
+            const unsigned long long ka = K[a], kc = K[c];
+            const uint32_t ia = I[a], ic = I[c];
+            if (bs_less(kc, ic, ka, ia)) {
+              K[a] = kc;
+              K[c] = ka;
+              I[a] = ic;
+              I[c] = ia;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t t = threadIdx.x; t < s; t += blockDim.x) order[lo + t] = I[t];
+    __syncthreads();
+  }
+}
+
+// One warp per mixed bucket of 33 .. kBsRankMax splats: bitonic sort by
+// (key, index) of kS * 32 register slots (element e = slot * 32 + lane;
+// padding = +inf), cross-lane steps by shuffles, in-lane steps by swaps.
+template <int kS>
+__device__ __forceinline__ void bs_warp_sort(unsigned long long (&k)[kS], uint32_t (&ix)[kS]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32 * kS; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int sl = 0; sl < kS; ++sl) {
+        const int e = sl * 32 + lane;
+        const bool up = (e & size) == 0;  // ascending block
+        if (j >= 32) {
+          const int js = j >> 5;
+          if ((sl & js) == 0) {  // pair (sl, sl ^ js) inside the lane, lower slot decides
+            const int so = sl ^ js;
+            const bool sw = up ? bs_less(k[so], ix[so], k[sl], ix[sl]) : bs_less(k[sl], ix[sl], k[so], ix[so]);
+            if (sw) {
+              const unsigned long long tk = k[sl];
+              const uint32_t ti = ix[sl];
+              k[sl] = k[so];
+              ix[sl] = ix[so];
+              k[so] = tk;
+              ix[so] = ti;
+            }
+          }
+        } else {
+          const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k[sl], j);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, ix[sl], j);
+          const bool lower = (lane & j) == 0;
+          const bool other_less = bs_less(ok, oi, k[sl], ix[sl]);
+          // keep the min in the lower position of an ascending pair (max of a descending one)
+          const bool take = (lower == up) ? other_less : !other_less && !(ok == k[sl] && oi == ix[sl]);
+          if (take) {
+            k[sl] = ok;
+            ix[sl] = oi;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int kS>
+__device__ __forceinline__ void bs_warp_bucket(const unsigned long long* __restrict__ keys,
+                                               const uint32_t* __restrict__ sorted, uint32_t lo, uint32_t s,
+                                               uint32_t* __restrict__ order) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long k[kS];
+  uint32_t ix[kS];
+#pragma unroll
+  for (int sl = 0; sl < kS; ++sl) {
+    const uint32_t e = sl * 32 + lane;
+    ix[sl] = e < s ? sorted[lo + e] : 0xffffffffu;
+    k[sl] = e < s ? keys[ix[sl]] : ~0ull;
+  }
+  bs_warp_sort<kS>(k, ix);
+#pragma unroll
+  for (int sl = 0; sl < kS; ++sl) {
+    const uint32_t e = sl * 32 + lane;
+    if (e < s) order[lo + e] = ix[sl];
+  }
+}
+
+// A mixed bucket usually holds a few distinct depth values (exact ties of a
+// lattice column each), every value's splats already in index order: the
+// rank of a splat is (splats of smaller value) + (earlier splats of its
+// value).  Two warp passes over the bucket in 32-splat chunks with a
+// warp-uniform table of up to kBsDistinct values and their counts; more
+// distinct values -> the register bitonic sort.
+constexpr int kBsDistinct = 8;
+
+__device__ __forceinline__ bool bs_warp_few(const unsigned long long* __restrict__ keys,
+                                            const uint32_t* __restrict__ sorted, uint32_t lo, uint32_t s,
+                                            uint32_t* __restrict__ order) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long val[kBsDistinct];
+  uint32_t cnt[kBsDistinct], below[kBsDistinct];
+  int nd = 0;
+#pragma unroll
+  for (int t = 0; t < kBsDistinct; ++t) {
+    val[t] = 0;
+    cnt[t] = 0;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      // below[t] = splats with a smaller value; cnt becomes the running count
+#pragma unroll
+      for (int t = 0; t < kBsDistinct; ++t) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int u = 0; u < kBsDistinct; ++u) acc += (u < nd && val[u] < val[t]) ? cnt[u] : 0u;
+        below[t] = acc;
+      }
+#pragma unroll
+      for (int t = 0; t < kBsDistinct; ++t) cnt[t] = 0;
+    }
+    for (uint32_t c0 = 0; c0 < s; c0 += 32) {
+      const bool valid = c0 + lane < s;
+      const uint32_t ix = valid ? sorted[lo + c0 + lane] : 0u;
+      const unsigned long long k = valid ? keys[ix] : 0ull;
+      unsigned todo = __ballot_sync(0xffffffffu, valid);
+      while (todo) {
+        const int l = __ffs(todo) - 1;
+        const unsigned long long kv = __shfl_sync(0xffffffffu, k, l);
+        const unsigned grp = __ballot_sync(0xffffffffu, valid && k == kv);
+        int slot = -1;
+#pragma unroll
+        for (int t = 0; t < kBsDistinct; ++t) slot = (t < nd && val[t] == kv) ? t : slot;
+        if (slot < 0) {
+          if (nd == kBsDistinct || pass == 1) return false;  // too many values (warp-uniform)
+          slot = nd++;
+#pragma unroll
+          for (int t = 0; t < kBsDistinct; ++t) val[t] = t == slot ? kv : val[t];
+        }
+        uint32_t base = 0, bl = 0;
+#pragma unroll
+        for (int t = 0; t < kBsDistinct; ++t) {
+          base = t == slot ? cnt[t] : base;
+          bl = t == slot ? below[t] : bl;
+          cnt[t] += t == slot ? (uint32_t)__popc(grp) : 0u;
+        }
+        if (pass == 1 && (grp >> lane) & 1u) order[lo + bl + base + __popc(grp & lt)] = ix;
+        todo &= ~grp;
+      }
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(128) k_bs_mixed(const unsigned long long* __restrict__ keys, BsSorted srt,
+                                                  const uint32_t* __restrict__ start,
+                                                  const uint32_t* __restrict__ mixed,
+                                                  const uint32_t* __restrict__ n_mixed,
+                                                  uint32_t* __restrict__ order) {
+  const uint32_t* __restrict__ sorted = srt.get();
+  const uint32_t nm = *n_mixed;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < nm; j += warps) {
+    const uint32_t b = mixed[j];
+    const uint32_t lo = start[b], s = start[b + 1] - lo;
+    if (bs_warp_few(keys, sorted, lo, s, order)) continue;
+    if (s <= 64) bs_warp_bucket<2>(keys, sorted, lo, s, order);
+    else if (s <= 128) bs_warp_bucket<4>(keys, sorted, lo, s, order);
+    else bs_warp_bucket<8>(keys, sorted, lo, s, order);
+  }
+}
+
+}  // namespace
+
+size_t bucket_sort_workspace_bytes(int64_t n) {
+  const size_t a = onesweep_workspace_bytes(n), b = scan_workspace_bytes(kBsBuckets);
+  return bs_fixed_bytes() + (a > b ? a : b) + 256;
+}
+
+xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_tiles, int64_t n,
+                            unsigned long long* key_a, unsigned long long* key_b, uint32_t* val_a, uint32_t* val_b,
+                            uint32_t* order, uint32_t* n_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (n < 1) return XG_OK;
+  BsWs w;
+  if (!bs_carve(ws, ws_bytes, w)) {
+    set_error_msg("bucket_sort_depth: workspace too small");
+    return XG_ERR_WORKSPACE;
+  }
+  cudaMemsetAsync(w.mm, 0xff, 2 * sizeof(unsigned long long), s);
+  cudaMemsetAsync(w.n_large, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(w.n_mixed, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(w.count, 0, sizeof(uint32_t) * kBsBuckets, s);
+  cudaMemsetAsync(w.bmin, 0xff, sizeof(unsigned long long) * kBsBuckets, s);
+  cudaMemsetAsync(w.bmax, 0xff, sizeof(unsigned long long) * kBsBuckets, s);
+  const int g = (int)((n + 255) / 256);
+  k_bs_minmax<<<g < 592 ? g : 592, 256, 0, s>>>(keys, n_tiles, n, w.mm, n_dev);
+  xg_status st = check_launch("k_bs_minmax");
+  if (st != XG_OK) return st;
+  // bucket ids into key_b, iota into val_b (the onesweep's read-only inputs)
+  k_bs_bucket<<<g, 256, 0, s>>>(keys, n_tiles, n, w.mm, key_b, val_b, w.count, w.bmin, w.bmax);
+  if ((st = check_launch("k_bs_bucket")) != XG_OK) return st;
+  if ((st = scan_u32(w.count, nullptr, w.start, kBsBuckets, nullptr, kBsBuckets, w.start + kBsBuckets, w.tail,
+                     w.tail_bytes, s)) != XG_OK)
+    return st;
+  // stable by 16-bit bucket id: two byte passes (ids < 2^16); no final copy
+  BsSorted srt{{val_a, val_b, val_b}, nullptr};
+  if ((st = onesweep_sort_pairs64(key_b, val_b, key_a, key_b, val_a, val_b, nullptr, n, n_dev, w.tail, w.tail_bytes,
+                                  s, 2, &srt.sel)) != XG_OK)
+    return st;
+  k_bs_rank<<<g, 256, 0, s>>>(keys, n_tiles, w.mm, srt, n, w.start, w.bmin, w.bmax, order, w.large, w.n_large,
+                              w.mixed, w.n_mixed);
+  if ((st = check_launch("k_bs_rank")) != XG_OK) return st;
+  k_bs_mixed<<<4 * 148, 128, 0, s>>>(keys, srt, w.start, w.mixed, w.n_mixed, order);
+  if ((st = check_launch("k_bs_mixed")) != XG_OK) return st;
+  static bool attr = false;
+  const int smem = (int)((sizeof(unsigned long long) + sizeof(uint32_t)) * kBsSmemMax);
+  if (!attr) {
+    cudaFuncSetAttribute(k_bs_large, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_bs_large<<<148, kBsLargeThreads, smem, s>>>(keys, srt, w.start, w.large, w.n_large, key_a, val_a, order);
+  return check_launch("k_bs_large");
 }
 
 }  // namespace xg

@@ -34,6 +34,19 @@ size_t onesweep_workspace_bytes(int64_t cap);
 xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_t* vals_in,
                                 unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a,
                                 uint32_t* vals_b, uint32_t* vals_out, int64_t cap, const uint32_t* n_dev,
-                                void* ws, size_t ws_bytes, cudaStream_t s);
+                                void* ws, size_t ws_bytes, cudaStream_t s, int n_passes = 8,
+                                const int** result_sel = nullptr);
+// (n_passes < 8: keys must be zero above byte n_passes; result_sel != null:
+// no final copy - the result is vals {a, b, in}[**result_sel], device-side)
+
+// Depth order of the active splats (ascending (key, index); inactive ones,
+// n_tiles == 0, first, in arbitrary order) by a stable sort on 15-bit key
+// buckets and ranking inside mixed buckets (xg_sort.cu).  key_a / key_b /
+// val_a / val_b: N-sized scratch; order: N-sized output; keys never written;
+// *n_dev receives n (the onesweep's device count).
+size_t bucket_sort_workspace_bytes(int64_t n);
+xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_tiles, int64_t n,
+                            unsigned long long* key_a, unsigned long long* key_b, uint32_t* val_a, uint32_t* val_b,
+                            uint32_t* order, uint32_t* n_dev, void* ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace xg

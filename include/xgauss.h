@@ -240,9 +240,8 @@ xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, fl
  *   {sum G dx, sum G dy, sum G dx^2, sum G dx dy, sum G dy^2, sum g w, sum G, 0}
  * over (pixel, entry) pairs, dx = px - mx, w = sigma T, g = dL/dI,
  * G = dL/dsigma * sigma on unclamped pairs (= the reference's g_power).
- * grad_acc must hold zeros on entry: freshly zeroed, or as the previous
- * xg_preprocess_bwd left it (that kernel consumes the rows it reads and
- * zeroes them). */
+ * grad_acc ([N][8], caller-allocated) is zeroed here first (a memset on the
+ * stream: no caller-side clearing launch). */
 xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
                            const int32_t* n_contrib, const float* dl_dimage, const float* image,
                            const float* target, float l1_scale, float* grad_acc, void* stream);
@@ -265,14 +264,13 @@ xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const
 /* K4b: chain rule to every cloud field (float64 arithmetic).  Writes
  * grads (flat, same layout as params; zero rows for culled Gaussians),
  * screen_norms[N], visible[N]; flags non-finite fields in the status word
- * and ORs the same flags into counters[XG_CTR_STICKY]; zeroes the grad_acc
- * rows it consumed (ready for the next xg_composite_bwd).
+ * and ORs the same flags into counters[XG_CTR_STICKY].
  * If norm_sum/obs_count/world_grad_sum are non-NULL they are accumulated
  * (DensifyStats.accumulate, trainer.py:185-188).  g_mean_out / g_conic_out /
  * g_int_out / g_alpha_out (optional, [N][2],[N][3],[N],[N] float64) receive
  * the reference's kernel-level gradients (backward_tiles outputs). */
 xg_status xg_preprocess_bwd(const xg_cloud* cloud, const xg_camera* cam, const xg_splats* sp,
-                            float* grad_acc, float* grads, float* screen_norms,
+                            const float* grad_acc, float* grads, float* screen_norms,
                             uint8_t* visible, float* norm_sum, int32_t* obs_count,
                             float* world_grad_sum, double* g_mean_out, double* g_conic_out,
                             double* g_int_out, double* g_alpha_out, void* stream);

@@ -1892,6 +1892,8 @@ static xg_status composite_bwd_impl(const xg_camera* cam, const xg_splats* sp, c
 xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
                            const int32_t* n_contrib, const float* dl_dimage, const float* image,
                            const float* target, float l1_scale, float* grad_acc, void* stream) {
+  if (grad_acc && sp && sp->n > 0)
+    cudaMemsetAsync(grad_acc, 0, sizeof(float) * 8 * (size_t)sp->n, (cudaStream_t)stream);
   return composite_bwd_impl(cam, sp, t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc, nullptr,
                             stream);
 }

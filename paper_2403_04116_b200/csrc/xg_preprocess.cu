@@ -304,7 +304,7 @@ struct BwdOut {
   uint32_t* counters;
 };
 
-__global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(CloudPtrs c, Cam k, xg_splats sp, float* __restrict__ acc,
+__global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(CloudPtrs c, Cam k, xg_splats sp, const float* __restrict__ acc,
                                  BwdOut o) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned bad = 0;
@@ -332,10 +332,6 @@ __global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(Clo
       project_one(c, k, i, p);
       const float4 a0 = reinterpret_cast<const float4*>(acc)[2 * i];
       const float4 a1 = reinterpret_cast<const float4*>(acc)[2 * i + 1];
-      // consumed: the accumulator row is left zeroed for the next reverse
-      // replay (no separate clearing pass in the training loop)
-      reinterpret_cast<float4*>(acc)[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      reinterpret_cast<float4*>(acc)[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
       // kernel accumulators -> reference kernel outputs (xgauss.h, K4a):
       // sum G (2 A2 dx + B2 dy) = 2 A2 sum G dx + B2 sum G dy, and the mean
       // gradient is -ln2 times that (p2 = power * log2 e, dx = px - mx)
@@ -538,7 +534,7 @@ xg_status xg_intensities(const xg_cloud* cloud, float* out, uint32_t* counters, 
 }
 
 xg_status xg_preprocess_bwd(const xg_cloud* cloud, const xg_camera* cam, const xg_splats* sp,
-                            float* grad_acc, float* grads, float* screen_norms,
+                            const float* grad_acc, float* grads, float* screen_norms,
                             uint8_t* visible, float* norm_sum, int32_t* obs_count,
                             float* world_grad_sum, double* g_mean_out, double* g_conic_out,
                             double* g_int_out, double* g_alpha_out, void* stream) {

@@ -249,9 +249,9 @@ class Frame:
                  dl_dimage: torch.Tensor | None = None, target: torch.Tensor | None = None,
                  l1_scale: float = 0.0, stats=None, kernel_grads=None, reproducible: bool = False,
                  events: list | None = None) -> None:
-        """K4a + K4b.  ``grad_acc`` ([N, 8] float32) must hold zeros - freshly
-        zeroed, or as the previous call left it (xg_preprocess_bwd consumes
-        and clears it).  ``reproducible`` sums each splat's per-entry gradient
+        """K4a + K4b.  ``grad_acc`` ([N, 8] float32 scratch) is zeroed by the
+        library (xg_composite_bwd) or fully written (reproducible mode).
+        ``reproducible`` sums each splat's per-entry gradient
         records in a fixed order (xg_composite_bwd_entries +
         xg_reduce_entry_grads) instead of with float atomics, so the result
         is identical run to run (the reference's single-threaded backward
@@ -271,7 +271,6 @@ class Frame:
                                                       self.entry_grad.data_ptr(), grad_acc.data_ptr(),
                                                       nat.stream()), "xg_reduce_entry_grads")
         else:
-            # (grad_acc holds zeros: fresh, or as the previous xg_preprocess_bwd left it)
             ev = None
             if events is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

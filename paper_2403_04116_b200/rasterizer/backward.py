@@ -54,7 +54,7 @@ def render_backward(cloud: GaussianCloud, splats: SplatList, dl_dimage, kernel_g
     grads = make_gradients(n, cloud.n_features, cloud.device)
     if not frame.has_forward:
         frame.composite()
-    acc = torch.zeros((n, 8), dtype=torch.float32, device=cloud.device)
+    acc = torch.empty((n, 8), dtype=torch.float32, device=cloud.device)
     vis = torch.empty(n, dtype=torch.uint8, device=cloud.device)
     frame.backward(cloud, acc, grads.flat, grads.screen_norms, vis, dl_dimage=dl,
                    kernel_grads=kernel_grads)

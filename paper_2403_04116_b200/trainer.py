@@ -327,7 +327,7 @@ class _IterationEngine:
         cap = capacity or (getattr(self, "frame", None) and self.frame.entry_capacity) or 16 * n
         self.frame = Frame(n, self.h, self.w, cloud.device, entry_capacity=cap)
         self.grads = make_gradients(n, cloud.n_features, cloud.device)
-        self.acc = torch.zeros((n, 8), dtype=torch.float32, device=cloud.device)  # (kept zero by xg_preprocess_bwd)
+        self.acc = torch.empty((n, 8), dtype=torch.float32, device=cloud.device)  # (zeroed by xg_composite_bwd)
         self.vis = torch.empty(n, dtype=torch.uint8, device=cloud.device)
 
 

@@ -1,0 +1,23 @@
+# round-2 evidence: launch list of exactly one timed C3 step, of 200 timed C2
+# iterations, and ncu --set full of the top kernels (12-view compositing,
+# training reverse replay + forward at the timed window, binning emit, depth sort)
+set -x
+XG_PROFILE_TIMED=1 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off -c 20000 --csv \
+    --log-file gpurun_out/r02_launches_timed_c3.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-train --no-c4 --no-c1 > gpurun_out/r02_bench_ncu.log 2>&1; echo "launches rc=$?"
+python tools/launch_summary.py gpurun_out/r02_launches_timed_c3.csv 360 > gpurun_out/r02_launches_timed_c3_summary.txt; head -20 gpurun_out/r02_launches_timed_c3_summary.txt
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off -c 20000 --csv \
+    --log-file gpurun_out/r02_launches_train_c2.csv python tools/probe_train.py 200 88 1000 > /dev/null 2>&1; echo "train launches rc=$?"
+python tools/launch_summary.py gpurun_out/r02_launches_train_c2.csv 200 > gpurun_out/r02_launches_train_c2_summary.txt; head -14 gpurun_out/r02_launches_train_c2_summary.txt
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_composite_fwd_batch -s 2 -c 1 \
+    -o gpurun_out/r02_ncu_fwd_batch python tools/prof_batch.py 3 > /dev/null 2>&1; echo "rc=$?"
+python tools/ncu_summary.py gpurun_out/r02_ncu_fwd_batch.ncu-rep > gpurun_out/r02_ncu_fwd_batch.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_composite_bwd_ck -s 5 -c 1 \
+    -o gpurun_out/r02_ncu_bwd_train python tools/probe_train.py 8 88 1000 > /dev/null 2>&1; echo "rc=$?"
+python tools/ncu_summary.py gpurun_out/r02_ncu_bwd_train.ncu-rep > gpurun_out/r02_ncu_bwd_train.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_composite_fwd_np -s 5 -c 1 \
+    -o gpurun_out/r02_ncu_fwdtrain python tools/probe_train.py 8 88 1000 > /dev/null 2>&1; echo "rc=$?"
+python tools/ncu_summary.py gpurun_out/r02_ncu_fwdtrain.ncu-rep > gpurun_out/r02_ncu_fwdtrain.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bin_emit -c 1 \
+    -o gpurun_out/r02_ncu_emit python tools/prof_c3.py 1 > /dev/null 2>&1; echo "rc=$?"
+python tools/ncu_summary.py gpurun_out/r02_ncu_emit.ncu-rep > gpurun_out/r02_ncu_emit.txt 2>&1
+head -14 gpurun_out/r02_ncu_fwd_batch.txt gpurun_out/r02_ncu_bwd_train.txt gpurun_out/r02_ncu_fwdtrain.txt

@@ -1,5 +1,5 @@
-"""Multi-view compositing launches for ncu (development aid): C3, 8 views
-binned, then `reps` xg_composite_fwd_batch launches."""
+"""Multi-view compositing launches for ncu (development aid): C3, 12 views
+(the bench's launch size) binned, then `reps` xg_composite_fwd_batch launches."""
 import sys
 
 import numpy as np
@@ -14,9 +14,9 @@ from paper_2403_04116_b200.inference import SweepRenderer  # noqa: E402
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cloud = GaussianCloud(**bench.c3_arrays(), device="cuda")
 sc = geometry.ScannerConfig(1000.0, 1500.0, 512, 512, 192.0 / 512)
-angles = bench.sweep_angles(0, 1)[:8]
-r = SweepRenderer(cloud, sc, batch=8)
-out = torch.empty((8, 512, 512), device="cuda")
+angles = bench.sweep_angles(0, 1)[:12]
+r = SweepRenderer(cloud, sc, batch=12)
+out = torch.empty((12, 512, 512), device="cuda")
 for _ in range(reps):
     r.render(angles, out=out)
 torch.cuda.synchronize()

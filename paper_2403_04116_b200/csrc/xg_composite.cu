@@ -583,6 +583,42 @@ template <bool kTrack>
 __host__ __device__ constexpr int fwd_pairs() { return kTrack ? kFwdTrackPairs : kFwdPairs; }
 __host__ __device__ constexpr int min_ctas(int kP) { return kP == 1 ? XG_FWD_MIN_CTAS : XG_FWD_MIN_CTAS_WIDE; }
 
+// TMA A/B (XG_FWD_TMA=1, image-only split path): the tile's entry-index
+// list is streamed into shared memory by cp.async.bulk in 256-entry chunks
+// (double-buffered per warp, mbarrier completion), replacing the warp's
+// coalesced LDG of 32 indices per batch; the splat records stay register
+// gathers (LDG).  Measured: no gain - the default stays LDG.
+#ifndef XG_FWD_TMA
+#define XG_FWD_TMA 0
+#endif
+constexpr int kTmaChunkShift = 8, kTmaChunk = 1 << kTmaChunkShift;
+struct __align__(16) TmaBuf {
+  unsigned long long mbar[2];
+  uint32_t idx[2][kTmaChunk + 4];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma_issue(TmaBuf* tb, const uint32_t* __restrict__ entry, long long base,
+                                          long long end, int c) {
+  const long long lo = base + ((long long)c << kTmaChunkShift);
+  const long long n = min((long long)kTmaChunk, end - lo);
+  const uint32_t bytes = (uint32_t)((n * 4 + 15) & ~15ll);  // 16 B multiple (the buffers carry 4 slack entries)
+  const uint32_t mb = smem_u32(&tb->mbar[c & 1]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (generic reads of the buffer precede the rewrite)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(tb->idx[c & 1])), "l"(entry + lo), "r"(bytes), "r"(mb) : "memory");
+}
+
+__device__ __forceinline__ void tma_wait(TmaBuf* tb, int c) {
+  const uint32_t mb = smem_u32(&tb->mbar[c & 1]), parity = (uint32_t)((c >> 1) & 1);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+}
+
 // One sub-block unit of the forward: the warp walks the tile's entry list
 // and writes the sub-block's pixels.
 // kLite (training forward, tracking): speculative batches use the
@@ -592,7 +628,8 @@ __host__ __device__ constexpr int min_ctas(int kP) { return kP == 1 ? XG_FWD_MIN
 // entry - the reverse replay's start (entries past the true last have
 // power < -30, exact no-ops up to < 1e-13 there).
 template <bool kTrack, int kP, bool kLite = false>
-__device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int sub, FRec* rec, int* kk) {
+__device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int sub, FRec* rec, int* kk,
+                                               TmaBuf* tb = nullptr) {
   constexpr int kR = 2 * kP;
   constexpr bool kSplitPath = !kTrack && kSpec && kFwdSplit && kP == 4;
   const int lane = threadIdx.x & 31;
@@ -612,9 +649,39 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     any_in |= in0 | in1;
   }
   bool alive = __any_sync(0xffffffffu, any_in);
+  // TMA variant: index chunks [base + 256 c, base + 256 (c + 1)) in buffer c & 1
+  constexpr bool kTma = XG_FWD_TMA && kSplitPath;
+  const long long tbase = u.start & ~3ll;  // 16 B aligned
+  int tma_issued = 0, tma_ready = -1;
+  const int tma_chunks = kTma ? (int)((u.end - tbase + kTmaChunk - 1) >> kTmaChunkShift) : 0;
+  if (kTma && tma_chunks > 0) {
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tb->mbar[0])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tb->mbar[1])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      tma_issue(tb, a.entry, tbase, u.end, 0);
+      if (tma_chunks > 1) tma_issue(tb, a.entry, tbase, u.end, 1);
+    }
+    tma_issued = tma_chunks > 1 ? 2 : 1;
+    __syncwarp();
+  }
+  // index k of the tile list (k < end), from shared memory (TMA) or global
+  auto idx_at = [&](long long k) -> uint32_t {
+    if (!kTma) return entry_at(a.entry, k, u.end);
+    if (k >= u.end) return 0u;
+    const int c = (int)((k - tbase) >> kTmaChunkShift);
+    return tb->idx[c & 1][(k - tbase) & (kTmaChunk - 1)];
+  };
+  auto tma_need = [&](long long kmax) {  // chunks up to kmax's have landed (warp-uniform)
+    if (!kTma) return;
+    kmax = min(kmax, u.end - 1);
+    const int c = (int)((kmax - tbase) >> kTmaChunkShift);
+    while (tma_ready < c) tma_wait(tb, ++tma_ready);
+  };
   // two-stage prefetch: entry indices one batch ahead of the records
-  Raw nxt = fetch(entry_at(a.entry, u.start + lane, u.end), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
-  uint32_t g_nxt = entry_at(a.entry, u.start + 32 + lane, u.end);
+  tma_need(u.start + 63);
+  Raw nxt = fetch(idx_at(u.start + lane), u.start + lane < u.end, a.mean2d, a.coef, a.inten);
+  uint32_t g_nxt = idx_at(u.start + 32 + lane);
   for (long long b0 = u.start; alive && b0 < u.end; b0 += 32) {
     if (kTrack && a.ckpt) {
       // state before entry b0 for the chunked reverse replay; a warp that
@@ -636,7 +703,20 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     const int cnt = kSplitPath ? compact_fwd_split(cur, u, rec, general, rec_safe)
                                : compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
-    g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
+    if (kTma) {
+      tma_need(b0 + 95);
+      g_nxt = idx_at(b0 + 64 + lane);
+      // a buffer is refilled (chunk c + 2) once no later read targets chunk c:
+      // reads from here on are at k >= b0 + 96
+      while (tma_issued < tma_chunks && tbase + ((long long)(tma_issued - 1) << kTmaChunkShift) <= b0 + 96 &&
+             tma_ready >= tma_issued - 2) {
+        __syncwarp();
+        if (lane == 0) tma_issue(tb, a.entry, tbase, u.end, tma_issued);
+        ++tma_issued;
+      }
+    } else {
+      g_nxt = entry_at(a.entry, b0 + 64 + lane, u.end);
+    }
     if (!(kTrack ? kSpecTrack : kSpec)) {
       if (general)  // warp-uniform, per batch of 32 entries
         blend_batch<true, kTrack, kP>(rec, kk, cnt, u.fx, fy, T, acc, last);
@@ -731,6 +811,10 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 #pragma unroll
     for (int i = 0; i < kP; ++i) live |= (T[i].x >= kFloor) || (T[i].y >= kFloor);
     alive = __any_sync(0xffffffffu, live);
+  }
+  if (kTma) {  // (an early-terminated warp still has copies in flight: land them before the buffers are reused)
+    while (tma_ready < tma_issued - 1) tma_wait(tb, ++tma_ready);
+    __syncwarp();
   }
   if (kTrack && kLite) {  // live to the end: replay from the list's last entry
     const int lend = (int)(u.end - u.start) - 1;
@@ -879,6 +963,9 @@ __global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd
   constexpr int kSubs = 4 / kFwdPairs;
   __shared__ FRec s_rec[kWarps][kRecPerWarp];
   __shared__ int s_k[kWarps][32];
+#if XG_FWD_TMA
+  __shared__ TmaBuf s_tma[kWarps];
+#endif
   const int warp = threadIdx.x >> 5;
   const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
   if (i >= b.n_tiles * b.n_views) return;
@@ -888,7 +975,11 @@ __global__ void __launch_bounds__(kThreads, min_ctas(kFwdPairs)) k_composite_fwd
   if (v.n_entries && (long long)*v.n_entries > v.cap) return;
   FwdArgs a{v.mean2d, v.coef, v.inten, v.entry, v.ranges, nullptr, nullptr, b.n_tiles, v.image, nullptr,
             nullptr, nullptr, nullptr, nullptr, nullptr, 0, b.ntx, b.w, b.h};
+#if XG_FWD_TMA
+  composite_unit<false, kFwdPairs>(a, tile, warp % kSubs, s_rec[warp], s_k[warp], &s_tma[warp]);
+#else
   composite_unit<false, kFwdPairs>(a, tile, warp % kSubs, s_rec[warp], s_k[warp]);
+#endif
 }
 
 // (view, tile) pairs of a batch by descending entry count (64 log buckets).

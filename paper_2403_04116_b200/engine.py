@@ -81,7 +81,8 @@ class Frame:
         if cap <= self.entry_capacity and self.entry_splat is not None:
             return
         self.entry_capacity = cap
-        self.entry_splat = torch.empty(cap, dtype=torch.int32, device=self.device)
+        # (+4 slack entries: 16 B-rounded bulk copies of a list's tail stay inside the allocation)
+        self.entry_splat = torch.empty(cap + 4, dtype=torch.int32, device=self.device)
         ws = nat.lib().xg_bin_workspace_bytes(self.n, cap, self.n_tiles)
         self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
         if self.replay_ckpt is not None:

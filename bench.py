@@ -708,7 +708,12 @@ def c4_block(args, timed, world: int, rank: int) -> dict:
            "step_roofline": {"roofline_ms_per_view": roof_s * 1e3, "measured_ms_per_view": ms_view,
                              "frac": roof_s * 1e3 / ms_view,
                              "model": "156 B/G projection + SURVEY 8d S2 binning bytes at the HBM peak + "
-                                      "17 FLOP per traversed pair at the FP32 peak"},
+                                      "17 FLOP per traversed pair at the FP32 peak",
+                             "note": "the reference algorithm's roofline, not a bound on this implementation: "
+                                     "the binning writes each entry once (multisplit) instead of the model's "
+                                     "radix sort of 64-bit (tile|depth) keys, and the compositing skips pairs "
+                                     "below the power cut-off at every pixel of a 16x8 half - so frac can "
+                                     "exceed 1"},
            "config": {"workload": f"C4: {cloud.n_points:,} ACUI Gaussians (G={G_C4}), {DET_C4}x{DET_C4} detector, "
                                   f"{VIEWS_C4} views per GPU per step", "streams": args.streams}}
     del rend, fr, cloud, out

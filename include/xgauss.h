@@ -248,18 +248,22 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
 
 /* Reproducible K4a (the reference's single-threaded backward is bitwise
  * reproducible, pkg/tests/test_trainer.py:336-353): the same reverse replay,
- * but each (entry, chunk) warp STORES its per-entry 8-value sum into
- * entry_grad[entry_capacity][8] (zeroed here) instead of adding it to the
- * splat; xg_reduce_entry_grads then writes grad_acc[N][8] by summing each
- * splat's entries in row-major order of its tile rectangle.  Needs the
- * checkpointed replay (a tracking forward with replay_ckpt/replay_items/
- * unit_cost, and image).  Same numbers as xg_composite_bwd up to the
- * summation order, identical run to run. */
+ * but each (splat, tile) sum - written by exactly one warp - is STORED into
+ * the splat's own slot for that tile (slots of splat g: an exclusive scan of
+ * n_tiles, one per tile of its rectangle, row-major), and
+ * xg_reduce_entry_grads writes grad_acc[N][8] by adding each splat's slots
+ * in order.  entry_ws: xg_entry_grad_bytes(n, entry_capacity) bytes of
+ * caller scratch (zeroed / scanned here).  Needs the checkpointed replay (a
+ * tracking forward with replay_ckpt / replay_items / unit_cost, and image).
+ * Same numbers as xg_composite_bwd up to the summation order, identical run
+ * to run. */
+size_t xg_entry_grad_bytes(int64_t n_splats, int64_t entry_capacity);
 xg_status xg_composite_bwd_entries(const xg_camera* cam, const xg_splats* sp, const float* t_final,
                                    const int32_t* n_contrib, const float* dl_dimage, const float* image,
-                                   const float* target, float l1_scale, float* entry_grad, void* stream);
-xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const float* entry_grad,
-                                float* grad_acc, void* stream);
+                                   const float* target, float l1_scale, void* entry_ws, size_t entry_ws_bytes,
+                                   void* stream);
+xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const void* entry_ws,
+                                size_t entry_ws_bytes, float* grad_acc, void* stream);
 
 /* K4b: chain rule to every cloud field (float64 arithmetic).  Writes
  * grads (flat, same layout as params; zero rows for culled Gaussians),

@@ -106,11 +106,12 @@ SIGNATURES = {
         c_i32,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_f32, c_void_p, c_void_p],
     ),
+    "xg_entry_grad_bytes": (c_size, [c_i64, c_i64]),
     "xg_composite_bwd_entries": (
         c_i32,
-        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_f32, c_void_p, c_void_p],
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_f32, c_void_p, c_size, c_void_p],
     ),
-    "xg_reduce_entry_grads": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "xg_reduce_entry_grads": (c_i32, [c_void_p, c_void_p, c_void_p, c_size, c_void_p, c_void_p]),
     "xg_preprocess_bwd": (c_i32, [c_void_p] * 15),
     "xg_check_finite": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
     "xg_check_finite_range": (c_i32, [c_void_p, c_i64, c_i32, c_i64, c_i64, c_void_p, c_void_p]),

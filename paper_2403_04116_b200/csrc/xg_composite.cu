@@ -32,6 +32,7 @@
 #include <stdlib.h>
 
 #include "xg_internal.cuh"
+#include "xg_sort.cuh"
 
 namespace xg {
 namespace {
@@ -107,6 +108,8 @@ struct Raw {
   float it;
   uint32_t g;
   bool valid;
+  ushort4 r;     // reproducible reverse replay only: the splat's tile rectangle
+  uint32_t off;  //   and its first slot
 };
 
 struct Unit {
@@ -332,7 +335,9 @@ __device__ __forceinline__ void blend_splat(const FRec& r, int krel, float fx, c
 
 // Record half of the gather (the entry index is loaded one batch earlier).
 __device__ __forceinline__ Raw fetch(uint32_t g, bool valid, const double2* __restrict__ mean2d,
-                                     const float4* __restrict__ coef, const float* __restrict__ inten) {
+                                     const float4* __restrict__ coef, const float* __restrict__ inten,
+                                     const ushort4* __restrict__ rect = nullptr,
+                                     const uint32_t* __restrict__ slot_off = nullptr) {
   Raw r;
   r.valid = valid;
   r.g = g;
@@ -340,6 +345,10 @@ __device__ __forceinline__ Raw fetch(uint32_t g, bool valid, const double2* __re
     r.m = __ldg(mean2d + g);
     r.c = __ldg(coef + g);
     r.it = __ldg(inten + g);
+    if (rect) {  // (issued with the record: the slot is ready at compaction)
+      r.r = __ldg(rect + g);
+      r.off = __ldg(slot_off + g);
+    }
   }
   return r;
 }
@@ -1092,7 +1101,9 @@ struct BwdArgs {
   const float2* ckpt;         // chunked replay: the forward's checkpoints,
   const uint2* items;         //   the chunk list (tile, sub << 24 | chunk)
   const uint32_t* n_items;    //   and its length
-  float* entry_grad;          // reproducible mode: [E][8] per-entry sums (plain stores), else null
+  float* entry_grad;          // reproducible mode: per-(splat, tile) sums (plain stores), else null
+  const uint32_t* slot_off;   //   splat g's slots start at slot_off[g] (exclusive scan of n_tiles)
+  const ushort4* rect;        //   its tile rectangle: slot = slot_off[g] + row-major index of the tile
 };
 
 // Backward records (shared memory), signs folded as in the forward:
@@ -1285,6 +1296,7 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16]) {
   return v[0];
 }
 
+template <bool kRepro = false>
 __device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit& u, BRec* s_rec, int* s_k,
                                            uint32_t* s_gid, bool& general) {
   BRec r;
@@ -1303,7 +1315,10 @@ __device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit&
     const int pos = __popc(bal & lanemask_lt());
     s_rec[pos] = r;
     s_k[pos] = krel;
-    s_gid[pos] = raw.g;
+    // (reproducible replay: the splat's slot for this tile instead of its id)
+    s_gid[pos] = kRepro ? raw.off + (uint32_t)((u.y0 / kTile - raw.r.y) * (raw.r.z - raw.r.x + 1) +
+                                               (u.x0 / kTile - raw.r.x))
+                        : raw.g;
   }
   __syncwarp();
   return __popc(bal);
@@ -1324,11 +1339,11 @@ __device__ __forceinline__ bool unblend_any(const BRec& r, int krel, float fx, c
   return unblend_splat<kMode == 1, kP>(r, krel, fx, fy, last, g, T, nS, v);
 }
 
-template <int kMode, int kP>
+template <int kMode, int kP, bool kRepro>
 __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, const uint32_t* gid, int cnt, float fx,
                                               const float2 (&fy)[kP], const int (&last)[2 * kP],
                                               const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP],
-                                              float* grad_acc, float* entry_grad, long long start) {
+                                              float* grad_acc, float* slots) {
   const int lane = threadIdx.x & 31;
   // splats two at a time, back to front (A = q, then B = q - 1), their
   // records reduced together
@@ -1350,12 +1365,13 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
     const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
     const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
     if ((lane & 7) == 0 && (lane < 16 || hasB)) {
-      if (entry_grad) {
-        // reproducible mode: this warp is the only writer of the entry's
-        // (whole-tile sub-block, one chunk) sum; xg_reduce_entry_grads adds
-        // a splat's entries in a fixed order
-        const long long e = start + (lane < 16 ? kk[q] : kk[q - 1]);
-        *reinterpret_cast<float4*>(entry_grad + 8 * e + ((lane & 8) ? 4 : 0)) = make_float4(tot, t1, t2, t3);
+      if (kRepro) {
+        // reproducible mode: this warp is the only writer of the (splat,
+        // tile) sum (whole-tile sub-block, one chunk); it lands in the
+        // splat's own slot for this tile (compact_bwd<true>), and
+        // xg_reduce_entry_grads adds a splat's slots in order
+        const uint32_t slot = lane < 16 ? gid[q] : gid[q - 1];
+        *reinterpret_cast<float4*>(slots + 8 * (long long)slot + ((lane & 8) ? 4 : 0)) = make_float4(tot, t1, t2, t3);
       } else {
         const uint32_t id = lane < 16 ? gid[q] : gid[q - 1];
         red_add_v4(grad_acc + 8 * (long long)id + ((lane & 8) ? 4 : 0), tot, t1, t2, t3);
@@ -1382,21 +1398,23 @@ constexpr bool kBwdSpec = XG_BWD_SPEC != 0;
 // Walk entries [e_lo, e_hi) of the tile starting at `start` back to front in
 // batches of 32 ([b1 - 32, b1)), with the two-stage prefetch (entry indices
 // one batch ahead of the records).
-template <int kP>
+template <int kP, bool kRepro = false>
 __device__ __forceinline__ void replay_range(const BwdArgs& a, const Unit& u, long long start, long long e_lo,
                                              long long e_hi, const float2 (&fy)[kP], const int (&last)[2 * kP],
                                              const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP], BRec* rec,
                                              int* kk, uint32_t* gid) {
   const int lane = threadIdx.x & 31;
+  const ushort4* const rr = kRepro ? a.rect : nullptr;
+  const uint32_t* const ro = kRepro ? a.slot_off : nullptr;
   Raw nxt = fetch(e_hi - 32 + lane >= e_lo ? entry_at(a.entry, e_hi - 32 + lane, e_hi) : 0u,
-                  e_hi - 32 + lane >= e_lo, a.mean2d, a.coef, a.inten);
+                  e_hi - 32 + lane >= e_lo, a.mean2d, a.coef, a.inten, rr, ro);
   uint32_t g_nxt = e_hi - 64 + lane >= e_lo ? entry_at(a.entry, e_hi - 64 + lane, e_hi) : 0u;
   for (long long b1 = e_hi; b1 > e_lo; b1 -= 32) {
     const Raw cur = nxt;
     bool general;
-    const int cnt = compact_bwd(cur, (int)(b1 - 32 - start) + lane, u, rec, kk, gid, general);
+    const int cnt = compact_bwd<kRepro>(cur, (int)(b1 - 32 - start) + lane, u, rec, kk, gid, general);
     const long long kn = b1 - 64 + lane;
-    nxt = fetch(g_nxt, kn >= e_lo, a.mean2d, a.coef, a.inten);
+    nxt = fetch(g_nxt, kn >= e_lo, a.mean2d, a.coef, a.inten, rr, ro);
     g_nxt = kn - 32 >= e_lo ? entry_at(a.entry, kn - 32, e_hi) : 0u;
     bool exact = general || !kBwdSpec;
     float2 fye[kP];
@@ -1422,11 +1440,11 @@ __device__ __forceinline__ void replay_range(const BwdArgs& a, const Unit& u, lo
     }
 #endif
     if (general)
-      unblend_batch<1, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc, a.entry_grad, start);
+      unblend_batch<1, kP, kRepro>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc, a.entry_grad);
     else if (exact)
-      unblend_batch<0, kP>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc, a.entry_grad, start);
+      unblend_batch<0, kP, kRepro>(rec, kk, gid, cnt, u.fx, fy, last, g, T, nS, a.grad_acc, a.entry_grad);
     else
-      unblend_batch<2, kP>(rec, kk, gid, cnt, u.fx, fye, last, g, T, nS, a.grad_acc, a.entry_grad, start);
+      unblend_batch<2, kP, kRepro>(rec, kk, gid, cnt, u.fx, fye, last, g, T, nS, a.grad_acc, a.entry_grad);
     __syncwarp();
   }
 }
@@ -1462,7 +1480,7 @@ __device__ __forceinline__ void bwd_unit(const BwdArgs& a, int tile, int quad, B
 // forward's checkpoint before entry kCk (j + 1) - or, for a pixel whose last
 // blended entry precedes it, from its final state, which is the same state.
 // The suffix sum restarts as acc_K - image (S = image - acc_K).
-template <int kP>
+template <int kP, bool kRepro = false>
 __device__ __forceinline__ void bwd_chunk(const BwdArgs& a, uint2 item, BRec* rec, int* kk, uint32_t* gid) {
   constexpr int kR = 2 * kP, kRows = 2 * kR;
   const int lane = threadIdx.x & 31;
@@ -1528,7 +1546,7 @@ __device__ __forceinline__ void bwd_chunk(const BwdArgs& a, uint2 item, BRec* re
       }
     }
   }
-  replay_range<kP>(a, u, start, start + lo, start + hi, fy, last, g, T, nS, rec, kk, gid);
+  replay_range<kP, kRepro>(a, u, start, start + lo, start + hi, fy, last, g, T, nS, rec, kk, gid);
 }
 
 // (no min-blocks bound: ptxas then settles at 92 registers = 5 CTAs per SM,
@@ -1575,6 +1593,7 @@ constexpr int kBwdPairs = XG_BWD_PAIRS;
 static_assert(kBwdPairs == 1 || kBwdPairs == 2 || kBwdPairs == 4, "a sub-block is 4, 8 or 16 rows");
 constexpr int kBwdSubs = 4 / kBwdPairs;  // sub-blocks per tile
 
+template <bool kRepro>
 #ifdef XG_BWD_CK_MIN_CTAS
 __global__ void __launch_bounds__(kThreads, XG_BWD_CK_MIN_CTAS) k_composite_bwd_ck(BwdArgs a) {
 #else
@@ -1588,7 +1607,7 @@ __global__ void __launch_bounds__(kThreads) k_composite_bwd_ck(BwdArgs a) {
   const uint32_t n = *a.n_items, dealt = gridDim.x * kWarps;
   uint32_t k = blockIdx.x * kWarps + warp;
   while (k < n) {
-    bwd_chunk<kBwdPairs>(a, a.items[k], s_rec[warp], s_k[warp], s_gid[warp]);
+    bwd_chunk<kBwdPairs, kRepro>(a, a.items[k], s_rec[warp], s_k[warp], s_gid[warp]);
     uint32_t d = 0;
     if ((threadIdx.x & 31) == 0) d = atomicAdd(a.work, 1u);
     k = dealt + __shfl_sync(0xffffffffu, d, 0);
@@ -1756,40 +1775,58 @@ using namespace xg;
 
 extern "C" {
 
-// Reproducible mode: grad_acc[g] = the sum of splat g's per-entry records,
-// added in row-major order of its tile rectangle.  The entry of g in tile t
-// is found by binary search of the tile's list, which is sorted by
-// (float64 depth bits, cloud index) - the binning's own key.
-__global__ void k_reduce_entry_grads(const float* __restrict__ entry_grad, const uint32_t* __restrict__ entry,
-                                     const long long* __restrict__ ranges, const unsigned long long* __restrict__ dkey,
-                                     const ushort4* __restrict__ rect, const uint32_t* __restrict__ n_tiles,
-                                     long long n, int ntx, const uint32_t* n_entries, long long cap,
-                                     float* __restrict__ grad_acc) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+// Reproducible mode: grad_acc[g] = the sum of splat g's per-tile slots
+// (one per tile of its rectangle, written by exactly one warp of the reverse
+// replay, zero where no pixel reached it), added in row-major tile order.
+// One warp per splat: lane l reads float4 half (l & 1) of slot lo + l / 2 +
+// 16 i (coalesced), sums its column in slot order, and the halves are
+// combined by a fixed xor tree - a fixed summation order, so the result is
+// identical run to run.
+__global__ void __launch_bounds__(128) k_reduce_entry_grads(const float* __restrict__ slots,
+                                                            const uint32_t* __restrict__ slot_off,
+                                                            const uint32_t* __restrict__ n_tiles, long long n,
+                                                            const uint32_t* n_entries, long long cap,
+                                                            float* __restrict__ grad_acc) {
+  const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (g >= n) return;
-  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
-  if (n_tiles[g] && !(n_entries && (long long)*n_entries > cap)) {
-    const ushort4 r = rect[g];
-    const unsigned long long kd = dkey[g];
-    for (int ty = r.y; ty <= r.w; ++ty)
-      for (int tx = r.x; tx <= r.z; ++tx) {
-        const int t = ty * ntx + tx;
-        long long lo = ranges[2 * t], hi = ranges[2 * t + 1];
-        while (lo < hi) {  // first position whose key is >= (kd, g)
-          const long long mid = (lo + hi) >> 1;
-          const uint32_t e = entry[mid];
-          const unsigned long long ke = dkey[e];
-          if (ke < kd || (ke == kd && e < (uint32_t)g)) lo = mid + 1;
-          else hi = mid;
-        }
-        const float4 a = *reinterpret_cast<const float4*>(entry_grad + 8 * lo);
-        const float4 b = *reinterpret_cast<const float4*>(entry_grad + 8 * lo + 4);
-        s0.x += a.x; s0.y += a.y; s0.z += a.z; s0.w += a.w;
-        s1.x += b.x; s1.y += b.y; s1.z += b.z; s1.w += b.w;
-      }
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!(n_entries && (long long)*n_entries > cap)) {
+    const long long lo = slot_off[g], hi = lo + n_tiles[g];
+    for (long long k = lo + (lane >> 1); k < hi; k += 16) {
+      const float4 a = *reinterpret_cast<const float4*>(slots + 8 * k + 4 * (lane & 1));
+      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+    }
   }
-  *reinterpret_cast<float4*>(grad_acc + 8 * g) = s0;
-  *reinterpret_cast<float4*>(grad_acc + 8 * g + 4) = s1;
+#pragma unroll
+  for (int o = 2; o < 32; o <<= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    s.z += __shfl_xor_sync(0xffffffffu, s.z, o);
+    s.w += __shfl_xor_sync(0xffffffffu, s.w, o);
+  }
+  if (lane < 2) *reinterpret_cast<float4*>(grad_acc + 8 * g + 4 * lane) = s;
+}
+
+// reproducible-mode scratch: [slots: entry_capacity x 8 floats | slot_off: n + 1 | scan workspace]
+struct EntryWs {
+  float* slots;
+  uint32_t* off;
+  void* scan;
+  size_t scan_bytes;
+};
+
+static size_t entry_ws_layout(int64_t n, int64_t cap, void* ws, EntryWs* w) {
+  const size_t a = al(sizeof(float) * 8 * (size_t)(cap > 0 ? cap : 1));
+  const size_t b = al(sizeof(uint32_t) * (size_t)(n + 1));
+  const size_t c = scan_workspace_bytes(n + 1);
+  if (w) {
+    w->slots = (float*)ws;
+    w->off = (uint32_t*)((char*)ws + a);
+    w->scan = (char*)ws + a + b;
+    w->scan_bytes = c;
+  }
+  return a + b + c;
 }
 
 static xg_status composite_fwd_impl(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
@@ -1918,7 +1955,7 @@ xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, fl
 static xg_status composite_bwd_impl(const xg_camera* cam, const xg_splats* sp, const float* t_final,
                                     const int32_t* n_contrib, const float* dl_dimage, const float* image,
                                     const float* target, float l1_scale, float* grad_acc, float* entry_grad,
-                                    void* stream) {
+                                    const uint32_t* slot_off, void* stream) {
   if (!cam || !sp || !t_final || !n_contrib || !(grad_acc || entry_grad) || (!dl_dimage && (!image || !target))) {
     set_error_msg("xg_composite_bwd: invalid argument");
     return XG_ERR_INVALID;
@@ -1949,9 +1986,13 @@ static xg_status composite_bwd_impl(const xg_camera* cam, const xg_splats* sp, c
               image, target, l1_scale, grad_acc,
               sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
               tiles_x(*cam), cam->width, cam->height, (const float2*)sp->replay_ckpt, items, n_items,
-              entry_grad};
-    k_composite_bwd_ck<<<persistent_grid(k_composite_bwd_ck, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"), kThreads, 0,
-                         (cudaStream_t)stream>>>(a);
+              entry_grad, slot_off, (const ushort4*)sp->rect};
+    if (entry_grad)  // reproducible: slot stores (its own instantiation, so the default path is unchanged)
+      k_composite_bwd_ck<true><<<persistent_grid(k_composite_bwd_ck<true>, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"),
+                                 kThreads, 0, (cudaStream_t)stream>>>(a);
+    else
+      k_composite_bwd_ck<false><<<persistent_grid(k_composite_bwd_ck<false>, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"),
+                                  kThreads, 0, (cudaStream_t)stream>>>(a);
     return check_launch("k_composite_bwd_ck");
   }
   if (entry_grad) {
@@ -1986,36 +2027,48 @@ xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const floa
   if (grad_acc && sp && sp->n > 0)
     cudaMemsetAsync(grad_acc, 0, sizeof(float) * 8 * (size_t)sp->n, (cudaStream_t)stream);
   return composite_bwd_impl(cam, sp, t_final, n_contrib, dl_dimage, image, target, l1_scale, grad_acc, nullptr,
-                            stream);
+                            nullptr, stream);
+}
+
+size_t xg_entry_grad_bytes(int64_t n_splats, int64_t entry_capacity) {
+  return entry_ws_layout(n_splats, entry_capacity, nullptr, nullptr);
 }
 
 xg_status xg_composite_bwd_entries(const xg_camera* cam, const xg_splats* sp, const float* t_final,
                                    const int32_t* n_contrib, const float* dl_dimage, const float* image,
-                                   const float* target, float l1_scale, float* entry_grad, void* stream) {
+                                   const float* target, float l1_scale, void* entry_ws, size_t entry_ws_bytes,
+                                   void* stream) {
   if (kBwdSubs != 1) {
     set_error_msg("xg_composite_bwd_entries: built with XG_BWD_PAIRS != 4 (several writers per entry)");
     return XG_ERR_INVALID;
   }
-  if (!entry_grad || !sp || sp->entry_capacity < 1) {
-    set_error_msg("xg_composite_bwd_entries: invalid argument");
+  if (!entry_ws || !sp || sp->entry_capacity < 1 || !sp->rect || !sp->n_tiles ||
+      entry_ws_bytes < xg_entry_grad_bytes(sp->n, sp->entry_capacity)) {
+    set_error_msg("xg_composite_bwd_entries: invalid argument (entry_ws >= xg_entry_grad_bytes)");
     return XG_ERR_INVALID;
   }
-  // entries no reverse step reaches (culled, past every pixel's last) stay 0
-  cudaMemsetAsync(entry_grad, 0, sizeof(float) * 8 * (size_t)sp->entry_capacity, (cudaStream_t)stream);
-  return composite_bwd_impl(cam, sp, t_final, n_contrib, dl_dimage, image, target, l1_scale, nullptr, entry_grad,
-                            stream);
+  EntryWs w;
+  entry_ws_layout(sp->n, sp->entry_capacity, entry_ws, &w);
+  cudaStream_t s = (cudaStream_t)stream;
+  // slots no reverse step reaches (culled, past every pixel's last) stay 0
+  cudaMemsetAsync(w.slots, 0, sizeof(float) * 8 * (size_t)sp->entry_capacity, s);
+  xg_status st = scan_u32(sp->n_tiles, nullptr, w.off, sp->n, nullptr, sp->n, w.off + sp->n, w.scan, w.scan_bytes, s);
+  if (st != XG_OK) return st;
+  return composite_bwd_impl(cam, sp, t_final, n_contrib, dl_dimage, image, target, l1_scale, nullptr, w.slots,
+                            w.off, stream);
 }
 
-xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const float* entry_grad,
-                                float* grad_acc, void* stream) {
-  if (!cam || !sp || !entry_grad || !grad_acc || !sp->entry_splat || !sp->tile_ranges || !sp->depth_key ||
-      !sp->rect || !sp->n_tiles || sp->n < 1) {
+xg_status xg_reduce_entry_grads(const xg_camera* cam, const xg_splats* sp, const void* entry_ws,
+                                size_t entry_ws_bytes, float* grad_acc, void* stream) {
+  if (!cam || !sp || !entry_ws || !grad_acc || !sp->n_tiles || sp->n < 1 ||
+      entry_ws_bytes < xg_entry_grad_bytes(sp->n, sp->entry_capacity)) {
     set_error_msg("xg_reduce_entry_grads: invalid argument");
     return XG_ERR_INVALID;
   }
-  k_reduce_entry_grads<<<div_up(sp->n, 256), 256, 0, (cudaStream_t)stream>>>(
-      entry_grad, sp->entry_splat, (const long long*)sp->tile_ranges, (const unsigned long long*)sp->depth_key,
-      (const ushort4*)sp->rect, sp->n_tiles, sp->n, tiles_x(*cam),
+  EntryWs w;
+  entry_ws_layout(sp->n, sp->entry_capacity, const_cast<void*>(entry_ws), &w);
+  k_reduce_entry_grads<<<div_up(32 * sp->n, 128), 128, 0, (cudaStream_t)stream>>>(
+      w.slots, w.off, sp->n_tiles, sp->n,
       sp->entry_capacity > 0 && sp->counters ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
       grad_acc);
   return check_launch("k_reduce_entry_grads");

@@ -71,7 +71,7 @@ class Frame:
         self.workspace = None
         self.replay_ckpt = None  # training frames only: allocated by the first tracking composite
         self.replay_items = None
-        self.entry_grad = None  # reproducible backward only: [entry_capacity][8] per-entry records
+        self.entry_grad = None  # reproducible backward only: per-(splat, tile) slots + offsets (bytes)
         self.set_capacity(entry_capacity if entry_capacity else max(16 * n, 1024))
         self.cam = None
         self.has_forward = False
@@ -264,13 +264,13 @@ class Frame:
                 nat.ptr(dl_dimage, "dl_dimage"), self.fwd_image.data_ptr(),
                 nat.ptr(target, "target") if dl_dimage is None else None, ctypes.c_float(l1_scale))
         if reproducible:
-            if self.entry_grad is None or self.entry_grad.shape[0] < self.entry_capacity:
-                self.entry_grad = torch.empty((self.entry_capacity, 8), dtype=torch.float32, device=self.device)
-            nat.check(nat.lib().xg_composite_bwd_entries(*args, self.entry_grad.data_ptr(), nat.stream()),
-                      "xg_composite_bwd_entries")
-            nat.check(nat.lib().xg_reduce_entry_grads(ctypes.byref(self.cam), ctypes.byref(sp),
-                                                      self.entry_grad.data_ptr(), grad_acc.data_ptr(),
-                                                      nat.stream()), "xg_reduce_entry_grads")
+            nb = int(nat.lib().xg_entry_grad_bytes(self.n, self.entry_capacity))
+            if self.entry_grad is None or self.entry_grad.numel() < nb:
+                self.entry_grad = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            ws = (self.entry_grad.data_ptr(), self.entry_grad.numel())
+            nat.check(nat.lib().xg_composite_bwd_entries(*args, *ws, nat.stream()), "xg_composite_bwd_entries")
+            nat.check(nat.lib().xg_reduce_entry_grads(ctypes.byref(self.cam), ctypes.byref(sp), *ws,
+                                                      grad_acc.data_ptr(), nat.stream()), "xg_reduce_entry_grads")
         else:
             ev = None
             if events is not None:

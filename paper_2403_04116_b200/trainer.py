@@ -558,7 +558,7 @@ def train(dataset: ProjectionSet, cloud: GaussianCloud, cfg: TrainConfig, out_di
           verbose: bool = False, reproducible: bool = False) -> TrainResult:
     """Optimise the cloud against the training projections (trainer.py:330-438).
     ``reproducible=True`` makes runs byte-identical (fixed-order gradient
-    sums; ~15 % slower per iteration), as the reference's are."""
+    sums; ~7 % slower per C2 iteration), as the reference's are."""
     return Trainer(dataset, cloud, cfg, out_dir, verbose, reproducible=reproducible).run()
 
 

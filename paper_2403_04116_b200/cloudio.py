@@ -3,8 +3,14 @@
 Binary little-endian PLY, one ``vertex`` per Gaussian with float64
 properties ``x y z q0 q1 q2 q3 s0 s1 s2 raw_opacity f_0 .. f_{n-1}`` and the
 header comments ``n_features`` / ``basis_weights`` (repr-exact), so files
-interchange with xsplat in both directions.  The device cloud is float32;
-float32 -> float64 -> float32 is exact, so save + load round-trips bit for bit.
+interchange with xsplat in both directions.  The device cloud is float32
+(parameters and basis weights): a float32-origin cloud round-trips save +
+load bit for bit; a reference checkpoint's float64 values are rounded to
+float32 on load, so re-saving it is bit-exact only where they were float32
+values to begin with (``tests/test_cloudio.py``: a reference-written cloud of
+float32 values re-saves byte-identically).  Validation follows
+``cloudio.py:60-108``: a missing ``basis_weights`` comment is a
+``DatasetError``, a body LONGER than the vertices need is accepted.
 """
 
 from __future__ import annotations
@@ -59,11 +65,14 @@ def load_cloud(path: str | os.PathLike, device=None) -> GaussianCloud:
             if p[1] != "double":
                 raise DatasetError(f"{path}: unsupported property type {p[1]}")
             props.append(p[2])
-    if n is None or nf is None or props != _names(nf):
-        raise DatasetError(f"{path}: unexpected header")
+    if n is None or nf is None or weights is None:
+        raise DatasetError(f"{path}: header missing vertex count, n_features or basis_weights")
+    if props != _names(nf):
+        raise DatasetError(f"{path}: property list does not match the checkpoint schema")
     body = blob[pos + len(b"end_header\n"):]
-    if len(body) != 8 * n * len(props):
-        raise DatasetError(f"{path}: truncated body")
-    data = np.frombuffer(body, dtype="<f8").reshape(n, len(props))
+    need = 8 * n * len(props)
+    if len(body) < need:  # (trailing bytes are ignored, as the reference does)
+        raise DatasetError(f"{path}: body holds {len(body)} bytes, expected {need}")
+    data = np.frombuffer(body[:need], dtype="<f8").reshape(n, len(props))
     return GaussianCloud(data[:, 0:3], data[:, 3:7], data[:, 7:10], data[:, 10], data[:, 11:],
                          basis_weights=weights, device=device)

@@ -38,3 +38,18 @@ def test_values_are_float32_exact():
     for k in ("positions", "rotations", "log_scales", "raw_opacities", "features"):
         v = np.asarray(c[k], np.float64)
         assert np.array_equal(v, v.astype(np.float32).astype(np.float64)), k
+
+
+def test_header_and_body_rules_match_reference(tmp_path):
+    """cloudio.py:90-96 of the reference: a header without basis_weights is a
+    DatasetError; a body longer than the vertices need is accepted."""
+    blob = REF.read_bytes()
+    pos = blob.find(b"end_header\n")
+    hdr = b"\n".join(ln for ln in blob[:pos].split(b"\n") if not ln.startswith(b"comment basis_weights"))
+    (tmp_path / "nw.ply").write_bytes(hdr + b"end_header\n" + blob[pos + len(b"end_header\n"):])
+    with pytest.raises(DatasetError):
+        load_cloud(tmp_path / "nw.ply")
+    (tmp_path / "long.ply").write_bytes(blob + b"\0" * 24)
+    a, b = load_cloud(tmp_path / "long.ply").to_numpy(), load_cloud(REF).to_numpy()
+    for k in a:
+        assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k

@@ -5,7 +5,9 @@
 // touches contiguous cache lines), updates moments and parameters, and
 // renormalises the quaternion in the same pass - one read of p, m, v, g
 // and one write of p, m, v per element, the HBM minimum (28 B/element).
-// Arithmetic is float64 in registers (the reference is float64 end to end).
+// Arithmetic is float32 with IEEE division / square root (the moments are
+// stored in float32; the update differs from the reference's float64 by a
+// few ulp of the lr-scaled step).
 //
 // Density control: a mark kernel evaluates the clone / split / prune masks
 // (float64 comparisons, so identical to the reference on the same inputs)

@@ -46,9 +46,11 @@ def shard_angles(angles, rank: int, world: int) -> np.ndarray:
     return a[rank::world]
 
 
-def render_sweep_sharded(cloud, scanner, angles=None, gather: bool = False, group=None, n_streams: int = 3):
+def render_sweep_sharded(cloud, scanner, angles=None, gather: bool = False, group=None, n_streams: int = 3,
+                         batch: int = 12):
     """This rank's share of a sweep (and, with ``gather``, the full stack on
-    rank 0 in the original view order)."""
+    rank 0 in the original view order), through the batched renderer the
+    bench measures (``batch`` views per compositing launch)."""
     from .inference import SweepRenderer
 
     rank, world = world_info(group)
@@ -56,7 +58,7 @@ def render_sweep_sharded(cloud, scanner, angles=None, gather: bool = False, grou
         angles = scanner.angles
     angles = np.atleast_1d(np.asarray(angles, dtype=np.float64))
     local = shard_angles(angles, rank, world)
-    imgs = SweepRenderer(cloud, scanner, n_streams).render(local)
+    imgs = SweepRenderer(cloud, scanner, n_streams, batch=max(1, min(batch, len(local)))).render(local)
     if not gather or world == 1:
         return imgs
     return gather_views(imgs, len(angles), rank, world, group)

@@ -288,7 +288,7 @@ def evaluate(cloud: GaussianCloud, dataset: ProjectionSet, indices, use_clean: b
     stack = dataset.clean_images if use_clean else dataset.images
     if indices.size == 0:
         return MetricReport(psnr=float("nan"), ssim=float("nan"), per_view=[])
-    imgs = SweepRenderer(cloud, dataset.scanner, batch=min(8, max(1, int(indices.size)))).render(
+    imgs = SweepRenderer(cloud, dataset.scanner, batch=min(12, max(1, int(indices.size)))).render(
         dataset.angles[indices])
     refs = torch.as_tensor(np.asarray(stack)[indices], device=cloud.device)
     s, p = ssim_psnr_stack(imgs, refs)  # one launch per view, one sync

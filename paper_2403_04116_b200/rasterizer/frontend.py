@@ -177,7 +177,11 @@ def _check_cloud(cloud: GaussianCloud) -> None:
     nat.require_cuda(cloud.flat, "cloud")
 
 
-def _prepare(cloud, ext, intr, image_shape, extras: bool) -> tuple[Frame, SplatList]:
+def _prepare(cloud, ext, intr, image_shape, extras: bool, composite: bool = False) -> tuple[Frame, SplatList]:
+    """Preprocess + bin one view (one host sync: the entry count).  With
+    ``composite`` the tracking forward is queued BEFORE that sync (it skips
+    itself on the device if the entry buffer overflowed, and runs again on
+    the re-binned lists), so the GPU never idles at the read."""
     _check_cloud(cloud)
     h, w = (int(v) for v in image_shape)
     if h < 1 or w < 1:
@@ -185,7 +189,16 @@ def _prepare(cloud, ext, intr, image_shape, extras: bool) -> tuple[Frame, SplatL
     frame = Frame(cloud.n_points, h, w, cloud.device, entry_capacity=_capacity_hint(cloud, h, w),
                   extras=extras)
     frame.preprocess(cloud, camera_pod(ext, intr, (h, w)))
-    active, entries, _ = frame.ensure_binned()
+    if composite:
+        frame.bin_async()
+        frame.composite()
+        if frame.finish_bin():
+            frame.composite()
+        c = frame.last_counters
+        active, entries, status = int(c[nat.XG_CTR_ACTIVE]), int(c[nat.XG_CTR_ENTRIES]), int(c[nat.XG_CTR_STATUS])
+        nat.raise_for_status(status & ~nat.XG_ST_ENTRY_OVERFLOW)
+    else:
+        active, entries, _ = frame.ensure_binned()
     _remember_capacity(cloud, h, w, entries)
     return frame, SplatList(frame, cloud, ext, intr, (h, w), active, entries)
 
@@ -212,8 +225,7 @@ def project_splats(cloud: GaussianCloud, ext: ExtrinsicMatrix, intr: IntrinsicMa
 def render(cloud: GaussianCloud, ext: ExtrinsicMatrix, intr: IntrinsicMatrix,
            image_shape) -> tuple[Projection, SplatList]:
     """Rasterize the cloud into a detector image (frontend.py:208-233)."""
-    frame, splats = _prepare(cloud, ext, intr, image_shape, extras=True)
-    frame.composite()
+    frame, splats = _prepare(cloud, ext, intr, image_shape, extras=True, composite=True)
     return Projection(frame.image, splats.angle), splats
 
 

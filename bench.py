@@ -770,7 +770,7 @@ def c1_block(args, timed, clock_cls, local, world: int, rank: int) -> dict:
     cams = [geometry.camera_pod(geometry.extrinsic_from_angle(sc, a), intr, (d, d)) for a in angles]
     dl_host = torch.as_tensor(np.random.default_rng(0).normal(size=(d, d)) / (d * d), dtype=torch.float32).pin_memory()
     dl = dl_host.cuda()
-    n_streams = 4  # independent views in flight (their kernels overlap on the 148 SMs)
+    n_streams = int(os.environ.get("XG_C1_STREAMS", "4"))  # independent views in flight (their kernels overlap on the 148 SMs)
     engs = [_IterationEngine(cloud, d, d) for _ in range(n_streams)]
     streams = [torch.cuda.Stream() for _ in range(n_streams)]
     eng = engs[0]

@@ -12,7 +12,7 @@ import numpy as np
 
 FULLSIZE = Path(__file__).resolve().parent / "golden" / "fullsize.npz"
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
-G_OF = {"C1": 68, "C3": 152, "C4": 196}
+G_OF = {"C1": 68, "C2": 88, "C3": 152, "C4": 196}
 
 _cache: dict = {}
 

@@ -1,6 +1,6 @@
 """Golden vectors from the REAL reference (xsplat 0.1.0) at BASELINE.json's
-full sizes (C1 50,653 G at 256^2, C3 493,039 G at 512^2, C4
-1,030,301 G at 1024^2).  Run in the build container (needs oracle/_ref,
+full sizes (C1 50,653 G at 256^2, C2 103,823 G at 512^2, C3
+493,039 G at 512^2, C4 1,030,301 G at 1024^2).  Run in the build container (needs oracle/_ref,
 built by oracle/build_ref.sh from /root/reference):
 
     python tests/golden/make_golden_fullsize.py     # -> tests/golden/fullsize.npz
@@ -24,8 +24,10 @@ Stored per case ``<case>/<key>``:
   entry_splat slice, so a mismatch points at its tiles);
 * full arrays where small enough: C1 keeps entry_splat, radii, depths,
   image and (phi = 0.7) the kernel gradients and RenderGradients of
-  dL/dI ~ N(0,1)/HW, seed 0 (SURVEY 8d's C1 unit of work); C3 at pi/4
-  keeps the image (float32; the contract is 1e-4 relative).
+  dL/dI ~ N(0,1)/HW, seed 0 (SURVEY 8d's C1 unit of work); C2 at 0.7 the
+  image, kernel gradients and the geometric RenderGradients fields for the
+  same dL/dI; C3 at pi/4 and C4 at 0.7 the image (float32; the contract is
+  1e-4 relative).
 
 ``host`` records the CPU model and numpy's BLAS that produced the float64
 depths: the engine reproduces OpenBLAS dgemm's accumulation order
@@ -60,11 +62,15 @@ L_SO, L_SD = 1000.0, 1500.0
 CASES = (
     ("C1_0.7", 68, 256, 0.7, "full"),
     ("C1_pi4", 68, 256, np.pi / 4, "image"),
+    ("C2_0.7", 88, 512, 0.7, "full"),
     ("C3_0", 152, 512, 0.0, "bin"),
     ("C3_pi4", 152, 512, np.pi / 4, "image"),
     ("C3_0.7", 152, 512, 0.7, "bin"),
-    ("C4_0.7", 196, 1024, 0.7, "bin"),
+    ("C4_0.7", 196, 1024, 0.7, "image"),
 )
+# RenderGradients fields stored for the larger "full" cases (the features
+# gradient is g_int i (1 - i) lambda: pinned through k_g_int)
+GRAD_FIELDS_LARGE = ("positions", "rotations", "log_scales", "raw_opacities", "screen_norms")
 
 
 def sha(a: np.ndarray) -> str:
@@ -149,7 +155,8 @@ def main():
             for k, v in (("k_g_mean", gm), ("k_g_conic", gc), ("k_g_int", gi), ("k_g_alpha", ga)):
                 st[p + k] = np.asarray(v, np.float32)
             grads = render_backward(cloud, sp, dl)
-            for f in PARAM_FIELDS + ("screen_norms",):
+            gfields = PARAM_FIELDS + ("screen_norms",) if case.startswith("C1") else GRAD_FIELDS_LARGE
+            for f in gfields:
                 st[p + "grad_" + f] = np.asarray(getattr(grads, f), np.float32)
             st[p + "grad_visible"] = np.asarray(grads.visible)
         print(f"{case}: N={cloud.n_points} E={sp.entry_splat.size} ({time.perf_counter() - t0:.1f} s)", flush=True)

@@ -2,16 +2,17 @@
 (tests/golden/fullsize.npz, written by xsplat 0.1.0 through
 tests/golden/make_golden_fullsize.py) - no oracle in between:
 
-* C1 (50,653 G, 256^2) at phi = 0.7 and pi/4, C3 (493,039 G, 512^2) at
-  phi = 0, pi/4, 0.7, C4 (1,030,301 G, 1024^2) at 0.7: active set, float64
+* C1 (50,653 G, 256^2) at phi = 0.7 and pi/4, C2 (103,823 G, 512^2) at
+  0.7, C3 (493,039 G, 512^2) at phi = 0, pi/4, 0.7, C4 (1,030,301 G,
+  1024^2) at 0.7: active set, float64
   depths, tile ranges and the full (tile, depth, index) entry order
   bit-identical to the reference's SplatList (frontend.py:104-194) - at
   pi/4 that includes the reference's tie-breaking of the symmetric
   lattice's equal-depth splats;
-* C1 images and the C3 pi/4 image within 1e-4 relative of the reference's
+* C1, C2, C3 pi/4 and C4 images within 1e-4 relative of the reference's
   float64 image (north_star tolerance), C1 radii within 1e-7 relative;
-* C1 at phi = 0.7 with dL/dI ~ N(0,1)/HW (seed 0): kernel-level gradients
-  (backward_tiles) and RenderGradients normwise within 1e-4
+* C1 and C2 at phi = 0.7 with dL/dI ~ N(0,1)/HW (seed 0): kernel-level
+  gradients (backward_tiles) and RenderGradients normwise within 1e-4
   (backward.py:21-124)."""
 
 from __future__ import annotations
@@ -53,7 +54,7 @@ def _render(xg, case):
     return cloud, proj, sp
 
 
-@pytest.mark.parametrize("case", ["C1_0.7", "C1_pi4", "C3_0", "C3_pi4", "C3_0.7", "C4_0.7"])
+@pytest.mark.parametrize("case", ["C1_0.7", "C1_pi4", "C2_0.7", "C3_0", "C3_pi4", "C3_0.7", "C4_0.7"])
 def test_binning_equals_reference_full_size(xg, case):
     cloud, proj, sp = _render(xg, case)
     act = sp.active_indices.cpu().numpy()
@@ -73,13 +74,13 @@ def test_binning_equals_reference_full_size(xg, case):
         assert np.array_equal(sp.depths.cpu().numpy(), fx[p + "depths"]), case
 
 
-def test_c1_gradients_equal_reference(xg):
+@pytest.mark.parametrize("case,d", [("C1_0.7", 256), ("C2_0.7", 512)])
+def test_gradients_equal_reference(xg, case, d):
     import torch
 
     fx = fg.load()
-    p = "C1_0.7/"
-    cloud, proj, sp = _render(xg, "C1_0.7")
-    d = 256
+    p = case + "/"
+    cloud, proj, sp = _render(xg, case)
     dl = np.random.default_rng(0).normal(size=(d, d)) / (d * d)
     n = cloud.n_points
     kg = {k: torch.zeros(s, dtype=torch.float64, device="cuda")
@@ -90,10 +91,11 @@ def test_c1_gradients_equal_reference(xg):
     floor = 1e-3 * max(np.abs(fx[p + "k_" + k]).max() for k in kg)
     for k, v in kg.items():
         ok, rel = normwise_ok(v.cpu().numpy()[act], fx[p + "k_" + k], floor)
-        assert ok, (k, rel)
-    fields = ("positions", "rotations", "log_scales", "raw_opacities", "features")
+        assert ok, (case, k, rel)
+    fields = [f for f in ("positions", "rotations", "log_scales", "raw_opacities", "features")
+              if p + "grad_" + f in fx]
     floor = 1e-3 * max(np.abs(fx[p + "grad_" + f]).max() for f in fields)
-    for f in fields + ("screen_norms",):
+    for f in fields + ["screen_norms"]:
         ok, rel = normwise_ok(getattr(grads, f).cpu().numpy(), fx[p + "grad_" + f], floor)
-        assert ok, (f, rel)
+        assert ok, (case, f, rel)
     assert np.array_equal(grads.visible.cpu().numpy(), fx[p + "grad_visible"])

@@ -1,7 +1,8 @@
 """Pin the CPU oracle to the real reference at BASELINE.json's full sizes
-(tests/golden/fullsize.npz, make_golden_fullsize.py): C1 and C3 at phi = 0,
-pi/4 (the symmetric lattice view whose exact depth ties the order must break
-as the reference does) and 0.7, C4 at 0.7.  CPU only."""
+(tests/golden/fullsize.npz, make_golden_fullsize.py): C1 at phi = 0.7 and
+pi/4, C2 at 0.7, C3 at 0, pi/4 (the symmetric lattice view whose exact depth
+ties the order must break as the reference does) and 0.7, C4 at 0.7.  CPU
+only."""
 
 from __future__ import annotations
 
@@ -12,7 +13,7 @@ import fullsize_golden as fg
 from conftest import normwise_ok
 from oracle import oracle as orc
 
-BIN_CASES = ["C1_0.7", "C1_pi4", "C3_0", "C3_pi4", "C3_0.7", "C4_0.7"]
+BIN_CASES = ["C1_0.7", "C1_pi4", "C2_0.7", "C3_0", "C3_pi4", "C3_0.7", "C4_0.7"]
 _runs: dict = {}
 
 

@@ -396,16 +396,20 @@ __device__ __forceinline__ float p2_at(float mx, float my, float A, float B, flo
   return fmaf(fmaf(C, dy, B * dx), dy, fmaf(A * dx, dx, la));
 }
 
+template <int kP = 4>
 __device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, FRec* s_rec, bool& general,
-                                                 bool& rec_safe) {
+                                                 bool& rec_safe, int krel = 0, int* s_k = nullptr) {
+  // the warp's sub-block is rows [ya, yb] (16 x 4 kP); half h = rows
+  // ya + 2 kP h .. ya + 2 kP h + 2 kP - 1 (lanes 16 h .. 16 h + 15)
+  constexpr int kR = 2 * kP;
   FRec r;
   bool k0 = false, k1 = false, gen = false, unsafe = false;
   if (raw.valid) {
     const float mx = (float)(raw.m.x - (double)u.x0), my = (float)(raw.m.y - (double)u.y0);
     const float A = raw.c.x, B = raw.c.y, C = raw.c.z, alpha = raw.c.w;
     const float la = __log2f(alpha);
-    k0 = overlaps(mx, my, A, B, C, u.xa, u.xb, 0.f, (float)(kTile / 2 - 1));
-    k1 = overlaps(mx, my, A, B, C, u.xa, u.xb, (float)(kTile / 2), (float)(kTile - 1));
+    k0 = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya, u.ya + (float)(kR - 1));
+    k1 = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya + (float)kR, u.yb);
     gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
     r.a = make_float4(mx, -my, A, B);
     r.b = make_float4(C, -alpha, -raw.it, la);
@@ -416,14 +420,14 @@ __device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, 
       // later rows may underflow harmlessly (their true sigma is even
       // smaller).  The ratios 2^(p2(dy + 2) - p2(dy)), linear in (dx, dy),
       // and 2^(8 C2) must stay within 2^+-120.
-      constexpr float e = (float)(kTile - 1), hh = (float)(kTile / 2);
-      const float mdx = fmaxf(fabsf(mx), fabsf(e - mx)), mdy = fmaxf(fabsf(my), fabsf(e - my));
+      constexpr float e = (float)(kTile - 1), hh = (float)kR;
+      const float mdx = fmaxf(fabsf(mx), fabsf(e - mx)), mdy = fmaxf(fabsf(my - u.ya), fabsf(u.yb - my));
       const float dmax = 4.f * fabsf(C) * mdy + fabsf(4.f * C) + 2.f * fabsf(B) * mdx;
       unsafe = !(dmax <= 120.f) || !(C >= -15.f);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (h ? k1 : k0) {
-          const float y0 = h * hh, y1 = y0 + 1.f;
+          const float y0 = u.ya + h * hh, y1 = y0 + 1.f;
           const float pmin = fminf(fminf(p2_at(mx, my, A, B, C, la, 0.f, y0), p2_at(mx, my, A, B, C, la, e, y0)),
                                    fminf(p2_at(mx, my, A, B, C, la, 0.f, y1), p2_at(mx, my, A, B, C, la, e, y1)));
           unsafe |= !(pmin >= -125.f);
@@ -437,10 +441,17 @@ __device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, 
   const unsigned lt = lanemask_lt();
   if (k0) s_rec[__popc(b0 & lt)] = r;
   if (k1) s_rec[32 + __popc(b1 & lt)] = r;
+  if (s_k) {  // (tracking launches: the entry index of every survivor, per half)
+    if (k0) s_k[__popc(b0 & lt)] = krel;
+    if (k1) s_k[32 + __popc(b1 & lt)] = krel;
+  }
   const int c0 = __popc(b0), c1 = __popc(b1), n = c0 > c1 ? c0 : c1;
   const int lane = threadIdx.x & 31;
+  // null splat padding the shorter half: mean 1e30 px away with A2 = -1 puts
+  // p2 at -inf at every pixel, so sigma = 0 exactly in every blend variant
+  // and no pixel ever records it as a blended (p2 >= cut) entry
   FRec z;
-  z.a = make_float4(0.f, 0.f, 0.f, 0.f);
+  z.a = make_float4(1e30f, 0.f, -1.f, 0.f);
   z.b = make_float4(0.f, 0.f, 0.f, -INFINITY);
   if (lane >= c0 && lane < n) s_rec[lane] = z;
   if (lane >= c1 && lane < n) s_rec[32 + lane] = z;
@@ -481,8 +492,9 @@ __device__ __forceinline__ void blend_splat_spec(const FRec& r, float fx, const 
 // 0, 1: 5 MUFU.EX2 per splat and lane instead of 8 (the kernel is EX2-bound).
 // Every factor stays within 2^+-120 (the compaction's rec_safe test);
 // relative error a few ulp after the 3 products.
-__device__ __forceinline__ void blend_splat_spec_rec(const FRec& r, float fx, const float2 (&fy)[4], float2 (&T)[4],
-                                                     float2 (&acc)[4]) {
+template <int kP = 4>
+__device__ __forceinline__ void blend_splat_spec_rec(const FRec& r, float fx, const float2 (&fy)[kP], float2 (&T)[kP],
+                                                     float2 (&acc)[kP]) {
   const float dx = __fsub_rn(fx, r.a.x);
   const float adx2 = __fmaf_rn(__fmul_rn(r.a.z, dx), dx, r.b.w);
   const float bdx = __fmul_rn(r.a.w, dx);
@@ -495,7 +507,7 @@ __device__ __forceinline__ void blend_splat_spec_rec(const FRec& r, float fx, co
   float2 E = make_float2(ex2_approx(p0.x), ex2_approx(p0.y));
   float2 S = make_float2(ex2_approx(d0.x), ex2_approx(d0.y));
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < kP; ++i) {
     if (i > 0) {
       E = __fmul2_rn(E, S);
       S = __fmul2_rn(S, bc(q4));
@@ -563,7 +575,11 @@ __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int 
 #ifndef XG_FWD_MIN_CTAS_WIDE
 #define XG_FWD_MIN_CTAS_WIDE 4
 #endif
-constexpr int kFwdPairs = XG_FWD_PAIRS, kFwdTrackPairs = XG_FWD_TRACK_PAIRS;
+#ifndef XG_FWD_LITE_PAIRS
+#define XG_FWD_LITE_PAIRS 1  // the trainer's forward: quarter tiles.  2 = 16 x 8 half tiles with split 16 x 4
+                             // lists (the image-only kernel's scheme): measured +9 % per C2 iteration (round 2)
+#endif
+constexpr int kFwdPairs = XG_FWD_PAIRS, kFwdTrackPairs = XG_FWD_TRACK_PAIRS, kFwdLitePairs = XG_FWD_LITE_PAIRS;
 // image-only launches: speculative test-free batches (blend_batch_spec)
 #ifndef XG_FWD_SPEC
 #define XG_FWD_SPEC 1
@@ -588,8 +604,8 @@ constexpr int kRecPerWarp = kFwdSplit ? 128 : 32;
 static_assert((kFwdPairs == 1 || kFwdPairs == 2 || kFwdPairs == 4) &&
                   (kFwdTrackPairs == 1 || kFwdTrackPairs == 2 || kFwdTrackPairs == 4) && kWarps % 4 == 0,
               "sub-blocks of 4, 8 or 16 rows; CTAs of whole tiles");
-template <bool kTrack>
-__host__ __device__ constexpr int fwd_pairs() { return kTrack ? kFwdTrackPairs : kFwdPairs; }
+template <bool kTrack, bool kLite = false>
+__host__ __device__ constexpr int fwd_pairs() { return kTrack ? (kLite ? kFwdLitePairs : kFwdTrackPairs) : kFwdPairs; }
 __host__ __device__ constexpr int min_ctas(int kP) { return kP == 1 ? XG_FWD_MIN_CTAS : XG_FWD_MIN_CTAS_WIDE; }
 
 // TMA A/B (XG_FWD_TMA=1, image-only split path): the tile's entry-index
@@ -640,9 +656,12 @@ template <bool kTrack, int kP, bool kLite = false>
 __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int sub, FRec* rec, int* kk,
                                                TmaBuf* tb = nullptr) {
   constexpr int kR = 2 * kP;
-  constexpr bool kSplitPath = !kTrack && kSpec && kFwdSplit && kP == 4;
+  // split-half entry lists: image-only whole-tile warps (kP = 4) and the
+  // trainer's tracking forward on 16 x 8 half tiles (kP = 2, kLite)
+  constexpr bool kSplitPath = kSpec && kFwdSplit && (kTrack ? (kLite && kSpecTrack && kP == 2) : kP == 4);
   const int lane = threadIdx.x & 31;
   FRec* const rh = kSplitPath ? rec + 32 * (lane >> 4) : rec;  // this lane's (half's) entry list
+  int* const kh = kSplitPath ? kk + 32 * (lane >> 4) : kk;      //   and its entry indices (tracking)
   const Unit u = make_sub<kP>(tile, sub, a.ntx, a.w, a.h, a.ranges);
   float2 fy[kP], T[kP], acc[kP], Tf[kP];  // Tf: final T of a pixel parked at T = 0 (tracking + speculation)
   int last[kR];
@@ -709,7 +728,8 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     const Raw cur = nxt;
     bool general;
     bool rec_safe = false;
-    const int cnt = kSplitPath ? compact_fwd_split(cur, u, rec, general, rec_safe)
+    const int cnt = kSplitPath ? compact_fwd_split<kP>(cur, u, rec, general, rec_safe, (int)(b0 - u.start) + lane,
+                                                       kTrack ? kk : nullptr)
                                : compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     if (kTma) {
@@ -770,7 +790,7 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 #endif
             if (rec_safe) {
 #pragma unroll kRecUnroll
-              for (int q = 0; q < cnt; ++q) blend_splat_spec_rec(rh[q], u.fx, fy, T, acc);
+              for (int q = 0; q < cnt; ++q) blend_splat_spec_rec<kP>(rh[q], u.fx, fy, T, acc);
             } else {
               blend_batch_spec<kP, kSplitUnroll>(rh, cnt, u.fx, fy, T, acc);
             }
@@ -801,9 +821,9 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
       }
       if (redo) {
         if (general)
-          blend_batch<true, kTrack, kP>(rh, kk, cnt, u.fx, fy, T, acc, last);
+          blend_batch<true, kTrack, kP>(rh, kh, cnt, u.fx, fy, T, acc, last);
         else
-          blend_batch<false, kTrack, kP>(rh, kk, cnt, u.fx, fy, T, acc, last);
+          blend_batch<false, kTrack, kP>(rh, kh, cnt, u.fx, fy, T, acc, last);
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
           if (kTrack) {
@@ -873,10 +893,10 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
 // Non-persistent single-view variant: one CTA per kWarps / kSubs tiles
 // (heaviest first), one warp per sub-block.
 template <bool kTrack, bool kLite = false>
-__global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd_np(FwdArgs a) {
-  constexpr int kP = fwd_pairs<kTrack>(), kSubs = 4 / kP;
+__global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack, kLite>())) k_composite_fwd_np(FwdArgs a) {
+  constexpr int kP = fwd_pairs<kTrack, kLite>(), kSubs = 4 / kP;
   __shared__ FRec s_rec[kWarps][kRecPerWarp];
-  __shared__ int s_k[kWarps][32];
+  __shared__ int s_k[kWarps][64];
   const int warp = threadIdx.x >> 5;
   if (a.n_entries && (long long)*a.n_entries > a.cap) return;
   const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
@@ -884,10 +904,10 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_com
 }
 
 template <bool kTrack, bool kLite = false>
-__global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack>())) k_composite_fwd(FwdArgs a) {
-  constexpr int kP = fwd_pairs<kTrack>();
+__global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack, kLite>())) k_composite_fwd(FwdArgs a) {
+  constexpr int kP = fwd_pairs<kTrack, kLite>();
   __shared__ FRec s_rec[kWarps][kRecPerWarp];
-  __shared__ int s_k[kWarps][32];
+  __shared__ int s_k[kWarps][64];
   const int warp = threadIdx.x >> 5;
   int tile, sub;
   bool first = true;
@@ -1869,9 +1889,9 @@ static xg_status composite_fwd_impl(const xg_camera* cam, const xg_splats* sp, f
 #endif
   const int np_grid = div_up(n_tiles, kWarps * kFwdTrackPairs / 4);
   if (lite && track_np)
-    k_composite_fwd_np<true, true><<<np_grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    k_composite_fwd_np<true, true><<<div_up(n_tiles, kWarps * kFwdLitePairs / 4), kThreads, 0, (cudaStream_t)stream>>>(a);
   else if (lite)
-    k_composite_fwd<true, true><<<persistent_grid(k_composite_fwd<true, true>, 4 / kFwdTrackPairs * n_tiles,
+    k_composite_fwd<true, true><<<persistent_grid(k_composite_fwd<true, true>, 4 / kFwdLitePairs * n_tiles,
                                                   "XG_FWD_CTAS_PER_SM"),
                                   kThreads, 0, (cudaStream_t)stream>>>(a);
   else if (track_np)

@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--train-iters-per-step", type=int, default=200)  # 5 steps: 1,000 timed iterations
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (1M Gaussians, 1024^2) stress block")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 (50k Gaussians, 256^2 fwd+bwd) block")
+    ap.add_argument("--no-c5", action="store_true", help="N = 1: skip the C5-size (493k) training block")
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
                     help="C3 under N GPUs: the 360-view sweep sharded over them (strong, BASELINE configs[2]) "
                          "or 360 views per GPU (weak)")
@@ -587,6 +588,8 @@ def run_ours(args) -> None:
         line["stress_c4"] = c4_block(args, timed, world, rank)
     if not args.no_train:
         line["train_c2" if world == 1 else "train_c5"] = train_block(args, timed, ClockSampler, local, world)
+        if world == 1 and not args.no_c5:  # train iters/s vs Gaussian count (BASELINE metric): C5 at N = 1
+            line["train_c5"] = train_block(args, timed, ClockSampler, local, world, c5=True)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             nv = args.cpu_sample_views or cpu_workers("C3")
@@ -892,12 +895,14 @@ def probe_train(tr) -> tuple[float, float, float]:
     return float(np.mean(p)), float(np.mean(e)), float(np.mean(a))
 
 
-def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
+def train_block(args, timed, clock_cls, local, world: int = 1, c5: bool = False) -> dict:
     """N=1 -> C2: ~100k Gaussians, 50 training views at 512x512, full
     training iterations (render fwd+bwd, L1, Adam, densify/prune every 100)
-    through the public Trainer API.  N>1 -> C5: 493k Gaussians, one view per
-    GPU per step, NCCL all-reduce of the flat gradient (bucketed, overlapped
-    with the fused Adam), DataParallelTrainer.  One step = 100 iterations."""
+    through the public Trainer API.  N>1 (or ``c5``) -> C5: 493k Gaussians,
+    one view per GPU per step, NCCL all-reduce of the flat gradient
+    (bucketed, overlapped with the fused Adam), DataParallelTrainer - at
+    N = 1 the single-GPU point of that scaling curve (no collective).  One
+    step = ``--train-iters-per-step`` iterations."""
     import torch
 
     from paper_2403_04116_b200 import _native, acui, geometry
@@ -905,7 +910,8 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
     from paper_2403_04116_b200.parallel import DataParallelTrainer
     from paper_2403_04116_b200.trainer import TrainConfig, Trainer
 
-    g = G_C2 if world == 1 else G_C3
+    c5 = c5 or world > 1
+    g = G_C3 if c5 else G_C2
     sc = geometry.ScannerConfig(L_SO, L_SD, DET, DET, 192.0 / DET, geometry.equal_interval_angles(100))
     ds, prep_s = phantom_dataset(g, sc)
     init = acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 0)
@@ -921,7 +927,7 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
     del prime
     torch.cuda.synchronize()
     for mode in ("device", "e2e"):
-        if world == 1:
+        if not c5:
             tr = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg, targets_on_host=(mode == "e2e"))
         else:
             tr = DataParallelTrainer(ds, GaussianCloud(**init, device="cuda"), cfg,
@@ -968,9 +974,10 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
     fwd_ach = FLOP_PER_PAIR * ppi / (d["fwd_ms"] * 1e-3) / 1e12
     name = (f"C2: {g}^3-lattice ACUI init ({(2 * (g // 4) + 3) ** 3:,} Gaussians), 50 train views of a "
             f"100-view 512x512 sweep, full iterations incl. densify/prune every 100 ({per // 100} events per step)"
-            if world == 1 else
+            if not c5 else
             f"C5: {(2 * (g // 4) + 3) ** 3:,} Gaussians, 512x512, data-parallel x{world}: one view per GPU per "
-            "step, NCCL all-reduce of the 27N gradient bucketed and overlapped with the fused Adam")
+            "step, NCCL all-reduce of the 27N gradient bucketed and overlapped with the fused Adam"
+            + (" (N = 1: no collective, the curve's single-GPU point)" if world == 1 else ""))
     blk = {"metric": "train iters/s", "value": iters / (d["ms"] / 1e3), "unit": "iters/s",
             "views_per_s": iters * world / (d["ms"] / 1e3),
             "ms_per_iter": d["ms"] / iters,
@@ -998,7 +1005,7 @@ def train_block(args, timed, clock_cls, local, world: int = 1) -> dict:
                               "model": "SURVEY 8d: binning + 156 B/G projection + 248 B/G chain rule + 756 B/G "
                                        "Adam + 12 B/px L1 at the HBM peak, (17 + 51) FLOP per traversed pair at "
                                        "the FP32 peak (744 us per iteration on the initial cloud in SURVEY)"}}
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not c5 and not args.no_cpu_baseline:
         del tr
         torch.cuda.empty_cache()
         v = int(ds.train_indices[0])

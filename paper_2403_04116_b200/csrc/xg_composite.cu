@@ -59,7 +59,8 @@ constexpr float kCullMargin = 0.05f;
 #endif
 constexpr bool kFwdRecur = XG_FWD_RECUR != 0;
 #ifdef XG_BWD_STATS
-__device__ unsigned long long g_fwd_stats[4];  // (development aid) recurrence / direct batches, survivors
+__device__ unsigned long long g_fwd_stats[8];  // (development aid) recurrence / direct batches, survivors,
+                                               // split-path batches with {both halves, one half} alive
 #endif
 #ifndef XG_FWD_REC_UNROLL
 #define XG_FWD_REC_UNROLL 4  // measured: 1 -0.8 %, 2, 4 +0.5 % (C3) / +1.4 % (C4)
@@ -783,9 +784,18 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
         } else {
           if constexpr (kSplitPath) {
 #ifdef XG_BWD_STATS
-            if (lane == 0) {
-              atomicAdd(&g_fwd_stats[rec_safe ? 0 : 1], 1ull);
-              atomicAdd(&g_fwd_stats[rec_safe ? 2 : 3], (unsigned long long)cnt);
+            {
+              bool mine = false;
+#pragma unroll
+              for (int i = 0; i < kP; ++i) mine |= (T[i].x >= kFloor) || (T[i].y >= kFloor);
+              const unsigned al = __ballot_sync(0xffffffffu, mine);
+              if (lane == 0) {
+                atomicAdd(&g_fwd_stats[rec_safe ? 0 : 1], 1ull);
+                atomicAdd(&g_fwd_stats[rec_safe ? 2 : 3], (unsigned long long)cnt);
+                const bool top = (al & 0xffffu) != 0, bot = (al >> 16) != 0;
+                atomicAdd(&g_fwd_stats[(top && bot) ? 4 : 5], 1ull);
+                atomicAdd(&g_fwd_stats[6], (unsigned long long)__popc(al));
+              }
             }
 #endif
             if (rec_safe) {
@@ -2194,8 +2204,8 @@ xg_status xg_backward_tiles(int32_t h, int32_t w, const double* means2d, const d
 // survivors by path {exact, general, speculative}; reads and clears
 int xg_debug_fwd_stats(unsigned long long* out) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, xg::g_fwd_stats, sizeof(unsigned long long) * 4);
-  static const unsigned long long zero[4] = {0, 0, 0, 0};
+  cudaMemcpyFromSymbol(out, xg::g_fwd_stats, sizeof(unsigned long long) * 8);
+  static const unsigned long long zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyToSymbol(xg::g_fwd_stats, zero, sizeof(zero));
   return 0;
 }

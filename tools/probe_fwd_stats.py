@@ -13,7 +13,7 @@ from paper_2403_04116_b200.gaussians import GaussianCloud  # noqa: E402
 from paper_2403_04116_b200.inference import SweepRenderer  # noqa: E402
 
 lib = _native.lib()
-out = (ctypes.c_ulonglong * 4)()
+out = (ctypes.c_ulonglong * 8)()
 for g, d in ((152, 512), (196, 1024)):
     cloud = GaussianCloud(**acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 0), device="cuda")
     sc = geometry.ScannerConfig(1000.0, 1500.0, d, d, 192.0 / d)
@@ -22,4 +22,5 @@ for g, d in ((152, 512), (196, 1024)):
     lib.xg_debug_fwd_stats(out)
     b = list(out)
     print(f"G={g} D={d}: batches recurrence {b[0] / max(1, b[0] + b[1]):.3f} | survivors/batch rec "
-          f"{b[2] / max(1, b[0]):.1f} direct {b[3] / max(1, b[1]):.1f}")
+          f"{b[2] / max(1, b[0]):.1f} direct {b[3] / max(1, b[1]):.1f} | batches with one half dead "
+          f"{b[5] / max(1, b[4] + b[5]):.3f}, live lanes/batch {b[6] / max(1, b[4] + b[5]):.1f}")

@@ -287,11 +287,14 @@ __device__ __forceinline__ float select_ok(float sg, float p2, float T) {
 // alpha >= 0.99 can reach it) and the p2 <= 0 test (only ill-conditioned
 // splats can need it); both are warp-uniform per batch.  Records the last
 // blended entry (n_contrib).
-template <bool kGeneral, bool kTrack>
+template <bool kGeneral, bool kTrack, bool kLa = false>
 __device__ __forceinline__ void blend_pair(const FRec& r, int krel, float2 dy, float bdx, float adx2, float2& T,
                                            float2& acc, int& last0, int& last1) {
   const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
-  float2 sg = __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
+  // kLa (image-only split records, b.y holds the recurrence factor): sigma
+  // = 2^(p2 + log2 alpha), as in the speculative image-only step
+  float2 sg = kLa ? make_float2(-ex2_approx(p.x + r.b.w), -ex2_approx(p.y + r.b.w))
+                  : __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
   if (kGeneral) {
     sg.x = fmaxf(sg.x, -kClamp);
     sg.y = fmaxf(sg.y, -kClamp);
@@ -322,7 +325,7 @@ __device__ __forceinline__ void blend_pair(const FRec& r, int krel, float2 dy, f
 
 // One splat, the lane's kP pixel pairs (one column: dx and the dx-only
 // terms computed once).
-template <bool kGeneral, bool kTrack, int kP>
+template <bool kGeneral, bool kTrack, int kP, bool kLa = false>
 __device__ __forceinline__ void blend_splat(const FRec& r, int krel, float fx, const float2 (&fy)[kP],
                                             float2 (&T)[kP], float2 (&acc)[kP], int (&last)[2 * kP]) {
   const float dx = __fsub_rn(fx, r.a.x);
@@ -330,8 +333,8 @@ __device__ __forceinline__ void blend_splat(const FRec& r, int krel, float fx, c
   const float bdx = __fmul_rn(r.a.w, dx);
 #pragma unroll
   for (int i = 0; i < kP; ++i)
-    blend_pair<kGeneral, kTrack>(r, krel, __fadd2_rn(fy[i], bc(r.a.y)), bdx, adx2, T[i], acc[i], last[2 * i],
-                                 last[2 * i + 1]);
+    blend_pair<kGeneral, kTrack, kLa>(r, krel, __fadd2_rn(fy[i], bc(r.a.y)), bdx, adx2, T[i], acc[i], last[2 * i],
+                                      last[2 * i + 1]);
 }
 
 // Record half of the gather (the entry index is loaded one batch earlier).
@@ -397,7 +400,7 @@ __device__ __forceinline__ float p2_at(float mx, float my, float A, float B, flo
   return fmaf(fmaf(C, dy, B * dx), dy, fmaf(A * dx, dx, la));
 }
 
-template <int kP = 4>
+template <int kP = 4, bool kTrack = false>
 __device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, FRec* s_rec, bool& general,
                                                  bool& rec_safe, int krel = 0, int* s_k = nullptr) {
   // the warp's sub-block is rows [ya, yb] (16 x 4 kP); half h = rows
@@ -413,7 +416,10 @@ __device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, 
     k1 = overlaps(mx, my, A, B, C, u.xa, u.xb, u.ya + (float)kR, u.yb);
     gen = !(alpha < kNoClampAlpha) || !well_conditioned(A, B, C);
     r.a = make_float4(mx, -my, A, B);
-    r.b = make_float4(C, -alpha, -raw.it, la);
+    // image-only records carry the row recurrence's per-splat factor
+    // 2^(8 C2) in b.y (one MUFU per entry here instead of one per splat and
+    // lane in the blend); the exact re-run then takes sigma = 2^(p2 + la)
+    r.b = make_float4(C, kTrack ? -alpha : ex2_approx(8.f * C), -raw.it, la);
     if (kFwdRecur && (k0 || k1)) {
       // the multiplicative row recurrence (blend_splat_spec_rec) of half h
       // starts from E_0 = 2^p2 at rows 8h, 8h + 1: those must be normal
@@ -501,7 +507,7 @@ __device__ __forceinline__ void blend_splat_spec_rec(const FRec& r, float fx, co
   const float bdx = __fmul_rn(r.a.w, dx);
   const float C = r.b.x, ni = -r.b.z;
   const float c4 = 4.f * C;
-  const float q4 = ex2_approx(8.f * C);
+  const float q4 = r.b.y;  // 2^(8 C2), from the compaction (compact_fwd_split, image-only)
   const float2 dy0 = __fadd2_rn(fy[0], bc(r.a.y));
   const float2 p0 = __ffma2_rn(__ffma2_rn(bc(C), dy0, bc(bdx)), dy0, bc(adx2));
   const float2 d0 = __ffma2_rn(bc(c4), dy0, bc(__fmaf_rn(2.f, bdx, c4)));
@@ -552,12 +558,13 @@ __device__ __forceinline__ void blend_splat_spec_track(const FRec& r, int krel, 
   }
 }
 
-template <bool kGeneral, bool kTrack, int kP>
+template <bool kGeneral, bool kTrack, int kP, bool kLa = false>
 __device__ __forceinline__ void blend_batch(const FRec* rec, const int* kk, int cnt, float fx, const float2 (&fy)[kP],
                                             float2 (&T)[kP], float2 (&acc)[kP], int (&last)[2 * kP]) {
   constexpr int kU = (!kTrack && kP == 4) ? kSplitUnroll : kFwdUnroll;  // (split image-only kernels: fewer registers)
 #pragma unroll kU
-  for (int q = 0; q < cnt; ++q) blend_splat<kGeneral, kTrack, kP>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last);
+  for (int q = 0; q < cnt; ++q)
+    blend_splat<kGeneral, kTrack, kP, kLa>(rec[q], kTrack ? kk[q] : 0, fx, fy, T, acc, last);
 }
 
 // 5 CTAs (20 warps) per SM: ptxas fits the image-only variant in 96
@@ -729,8 +736,8 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
     const Raw cur = nxt;
     bool general;
     bool rec_safe = false;
-    const int cnt = kSplitPath ? compact_fwd_split<kP>(cur, u, rec, general, rec_safe, (int)(b0 - u.start) + lane,
-                                                       kTrack ? kk : nullptr)
+    const int cnt = kSplitPath ? compact_fwd_split<kP, kTrack>(cur, u, rec, general, rec_safe,
+                                                               (int)(b0 - u.start) + lane, kTrack ? kk : nullptr)
                                : compact_fwd(cur, (int)(b0 - u.start) + lane, u, rec, kk, general);
     nxt = fetch(g_nxt, b0 + 32 + lane < u.end, a.mean2d, a.coef, a.inten);
     if (kTma) {
@@ -830,10 +837,11 @@ __device__ __forceinline__ void composite_unit(const FwdArgs& a, int tile, int s
         }
       }
       if (redo) {
+        constexpr bool kLa = kSplitPath && !kTrack;  // (image-only split records: sigma from log2 alpha)
         if (general)
-          blend_batch<true, kTrack, kP>(rh, kh, cnt, u.fx, fy, T, acc, last);
+          blend_batch<true, kTrack, kP, kLa>(rh, kh, cnt, u.fx, fy, T, acc, last);
         else
-          blend_batch<false, kTrack, kP>(rh, kh, cnt, u.fx, fy, T, acc, last);
+          blend_batch<false, kTrack, kP, kLa>(rh, kh, cnt, u.fx, fy, T, acc, last);
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
           if (kTrack) {

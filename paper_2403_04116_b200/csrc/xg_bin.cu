@@ -141,10 +141,10 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
 // every Gaussian contributes one entry per tile of its rect.  Pass 1 counts
 // entries per (tile, chunk); an exclusive scan over the tile-major table
 // gives each (tile, chunk) its output base - and the tile ranges for free.
-// Pass 2 re-enumerates the chunk's entries in (depth, rect) order and ranks
-// them stably per tile (per-warp counters + __match_any_sync within each
-// 32-entry round), writing entry_splat[] directly in (tile, depth, index)
-// order.  Replaces writing E (key, value) pairs and two radix passes over
+// Pass 2 re-enumerates the chunk's entries and ranks them stably per tile
+// (per-warp counters; within a warp's 32-Gaussian round, a lane per Gaussian
+// and the tile's peers as the AND of per-warp column and row lane masks),
+// writing entry_splat[] directly in (tile, depth, index) order.  Replaces writing E (key, value) pairs and two radix passes over
 // them with one read of the rects and one write of the values.
 // ---------------------------------------------------------------------------
 #ifndef XG_BIN_THREADS
@@ -177,6 +177,57 @@ inline int bin_rounds(int64_t n, int n_tiles) {
 }
 inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
+// k_bin_emit phase 3: a lane per Gaussian, peers ranked by column / row bit
+// masks (default), or 32-entry windows over the round's concatenated entries
+// ranked with __match_any_sync (=0)
+#ifndef XG_BIN_EMIT_MASKS
+#define XG_BIN_EMIT_MASKS 1
+#endif
+
+// A warp's 32 depth-sorted Gaussians of one round, software-pipelined: the
+// order[] index two rounds ahead and the (count, rect) gather one round ahead
+// are issued before the current round is processed.
+struct BinLane {
+  uint32_t g, cnt;
+  uint2 r;  // the ushort4 rect as two words: x0 | y0 << 16, x1 | y1 << 16
+  __device__ __forceinline__ int x0() const { return (int)(r.x & 0xffffu); }
+  __device__ __forceinline__ int y0() const { return (int)(r.x >> 16); }
+  __device__ __forceinline__ int x1() const { return (int)(r.y & 0xffffu); }
+  __device__ __forceinline__ int y1() const { return (int)(r.y >> 16); }
+};
+
+struct BinPipe {
+  const uint32_t* order;
+  const uint32_t* n_tiles;
+  const ushort4* rect;
+  long long n, wlo;
+  int lane;
+  uint32_t g_next;  // order[] of round rd + 1
+
+  __device__ __forceinline__ uint32_t index(int rd) const {
+    const long long s = wlo + rd * 32 + lane;
+    return s < n ? order[s] : 0xffffffffu;
+  }
+  __device__ __forceinline__ BinLane gather(uint32_t g) const {
+    BinLane b{g, 0u, make_uint2(0u, 0u)};
+    if (g != 0xffffffffu) {
+      b.cnt = n_tiles[g];
+      b.r = reinterpret_cast<const uint2*>(rect)[g];  // (unused when cnt == 0)
+    }
+    return b;
+  }
+  __device__ __forceinline__ BinLane first() {
+    const uint32_t g0 = index(0);
+    g_next = index(1);
+    return gather(g0);
+  }
+  // the lanes of round rd + 1, given rd + 1 < rounds (prefetches rd + 2)
+  __device__ __forceinline__ BinLane next(int rd) {
+    const BinLane b = gather(g_next);
+    g_next = index(rd + 2);
+    return b;
+  }
+};
 
 // Per-warp entry counts per tile, 16-bit, two tiles per word
 // ([C][kBinWarps][ceil(T/2)], the warp's Gaussians exactly as k_bin_emit
@@ -193,19 +244,20 @@ __global__ void __launch_bounds__(kBinThreads)
   __syncthreads();
   uint32_t* mine = wcnt + warp * TW;
   const long long wlo = (long long)blockIdx.x * kBinThreads * rounds + (long long)warp * 32 * rounds;
+  BinPipe pipe{order, n_tiles, rect, n, wlo, lane, 0u};
+  BinLane cur = pipe.first();
   for (int rd = 0; rd < rounds; ++rd) {
-    const long long s = wlo + rd * 32 + lane;
-    if (s < n) {
-      const uint32_t g = order[s];
-      if (n_tiles[g]) {
-        const ushort4 r = rect[g];
-        for (int ty = r.y; ty <= r.w; ++ty)
-          for (int tx = r.x; tx <= r.z; ++tx) {
-            const int t = ty * ntx + tx;
-            atomicAdd(&mine[t >> 1], 1u << ((t & 1) << 4));
-          }
-      }
+    BinLane nxt{};
+    if (rd + 1 < rounds) nxt = pipe.next(rd);
+    if (cur.cnt) {
+      const int x0 = cur.x0(), y0 = cur.y0(), x1 = cur.x1(), y1 = cur.y1();
+      for (int ty = y0; ty <= y1; ++ty)
+        for (int tx = x0; tx <= x1; ++tx) {
+          const int t = ty * ntx + tx;
+          atomicAdd(&mine[t >> 1], 1u << ((t & 1) << 4));
+        }
     }
+    cur = nxt;
   }
   __syncthreads();
   const int C = gridDim.x;
@@ -275,6 +327,69 @@ __global__ void __launch_bounds__(kBinThreads)
     }
   }
   __syncthreads();
+#if XG_BIN_EMIT_MASKS
+  // phase 3: each lane walks its own Gaussian's rect.  A tile's peers in the
+  // round (the lanes whose rects contain it, lane order = depth order) are
+  // the AND of two per-warp bit masks, column and row, built with one shared
+  // OR per rect column and row; the entry's rank among them is a popcount.
+  // A tile only this lane covers updates its local offset at once; shared
+  // tiles are advanced by their highest peer after the round's writes.
+  const int nty = T / ntx;
+  uint32_t* cmask = smem_bin + T + kBinWarps * TW + warp * (ntx + nty);
+  uint32_t* rmask = cmask + ntx;
+  const unsigned lt = lanemask_lt(), bit = 1u << lane;
+  const uint32_t cap32 = cap < 0xffffffffll ? (uint32_t)cap : 0xffffffffu;
+  BinPipe pipe{order, n_tiles, rect, n, wlo, lane, 0u};
+  BinLane cur = pipe.first();
+  for (int rd = 0; rd < rounds; ++rd) {
+    BinLane nxt{};
+    if (rd + 1 < rounds) nxt = pipe.next(rd);
+    const uint32_t g = cur.g, cnt = cur.cnt;
+    const int x0 = cur.x0(), y0 = cur.y0(), x1 = cur.x1(), y1 = cur.y1();
+    for (int k = lane; k < ntx + nty; k += 32) cmask[k] = 0u;
+    __syncwarp();
+    if (cnt) {
+      for (int x = x0; x <= x1; ++x) atomicOr(&cmask[x], bit);
+      for (int y = y0; y <= y1; ++y) atomicOr(&rmask[y], bit);
+    }
+    __syncwarp();
+    bool shared_tiles = false;
+    if (cnt) {
+      for (int y = y0; y <= y1; ++y) {
+        const uint32_t rm = rmask[y];
+        for (int x = x0; x <= x1; ++x) {
+          const uint32_t peers = rm & cmask[x];
+          const int t = y * ntx + x;
+          const uint32_t loc = mine16[t];
+          const uint32_t pos = tbase[t] + loc + (uint32_t)__popc(peers & lt);
+          if (pos < cap32) entry_splat[pos] = g;
+          if (peers == bit)
+            mine16[t] = (uint16_t)(loc + 1u);
+          else
+            shared_tiles = true;
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, shared_tiles)) {
+      __syncwarp();
+      if (shared_tiles) {
+        for (int y = y0; y <= y1; ++y) {
+          const uint32_t rm = rmask[y];
+          for (int x = x0; x <= x1; ++x) {
+            const uint32_t peers = rm & cmask[x];
+            if (peers != bit && (peers >> lane) == 1u) {
+              const int t = y * ntx + x;
+              mine16[t] = (uint16_t)(mine16[t] + (uint32_t)__popc(peers));
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    cur = nxt;
+  }
+}
+#else
   // phase 3: enumerate entries in (depth, rect row-major) order, rank per tile
   __shared__ uint32_t s_nz[kBinWarps][32];  // lanes with entries, in lane order
   const unsigned lt = lanemask_lt();
@@ -337,6 +452,7 @@ __global__ void __launch_bounds__(kBinThreads)
     __syncwarp();  // (s_nz is rewritten by the next round)
   }
 }
+#endif
 
 struct BinWs {
   unsigned long long *keyN1, *keyN2;
@@ -453,11 +569,13 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     // 2-4. fused duplicate + stable tile sort + ranges
     const int C = (int)bin_chunks(n, n_tiles);
     const size_t sm_count = sizeof(uint32_t) * (size_t)kBinWarps * ((n_tiles + 1) / 2);
-    const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2));
+    const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2) +
+                                               (XG_BIN_EMIT_MASKS ? (size_t)kBinWarps * (ntx + nty) : 0));
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(k_bin_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(uint32_t) * (kBinMaxTiles + kBinWarps * (kBinMaxTiles / 2))));
+                           (int)(sizeof(uint32_t) * (kBinMaxTiles + kBinWarps * (kBinMaxTiles / 2) +
+                                                     (XG_BIN_EMIT_MASKS ? kBinWarps * (kBinMaxTiles + 1) : 0))));
       cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(sizeof(uint32_t) * kBinWarps * (kBinMaxTiles / 2)));
       attr_set = true;

@@ -141,10 +141,10 @@ __global__ void __launch_bounds__(1024) k_tile_fill(const uint32_t* counters, lo
 // every Gaussian contributes one entry per tile of its rect.  Pass 1 counts
 // entries per (tile, chunk); an exclusive scan over the tile-major table
 // gives each (tile, chunk) its output base - and the tile ranges for free.
-// Pass 2 re-enumerates the chunk's entries and ranks them stably per tile
-// (per-warp counters; within a warp's 32-Gaussian round, a lane per Gaussian
-// and the tile's peers as the AND of per-warp column and row lane masks),
-// writing entry_splat[] directly in (tile, depth, index) order.  Replaces writing E (key, value) pairs and two radix passes over
+// Pass 2 re-enumerates the chunk's entries in (depth, rect) order and ranks
+// them stably per tile (per-warp counters + __match_any_sync within each
+// 32-entry window), writing entry_splat[] directly in (tile, depth, index)
+// order.  Replaces writing E (key, value) pairs and two radix passes over
 // them with one read of the rects and one write of the values.
 // ---------------------------------------------------------------------------
 #ifndef XG_BIN_THREADS
@@ -177,11 +177,13 @@ inline int bin_rounds(int64_t n, int n_tiles) {
 }
 inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
-// k_bin_emit phase 3: a lane per Gaussian, peers ranked by column / row bit
-// masks (default), or 32-entry windows over the round's concatenated entries
-// ranked with __match_any_sync (=0)
+// k_bin_emit phase 3: 32-entry windows over the round's concatenated entries
+// ranked with __match_any_sync (default), or (=1) a lane per Gaussian with
+// the peers ranked by column / row lane masks - fewer instructions, but each
+// lane's walk over its rect is a serial shared-memory chain: +2 % C4 and
+// +0.3 % C3 sweeps (many views hide it), -6 % per C2 iteration (one view)
 #ifndef XG_BIN_EMIT_MASKS
-#define XG_BIN_EMIT_MASKS 1
+#define XG_BIN_EMIT_MASKS 0
 #endif
 
 // A warp's 32 depth-sorted Gaussians of one round, software-pipelined: the
@@ -393,15 +395,13 @@ __global__ void __launch_bounds__(kBinThreads)
   // phase 3: enumerate entries in (depth, rect row-major) order, rank per tile
   __shared__ uint32_t s_nz[kBinWarps][32];  // lanes with entries, in lane order
   const unsigned lt = lanemask_lt();
+  BinPipe pipe{order, n_tiles, rect, n, wlo, lane, 0u};
+  BinLane cur = pipe.first();
   for (int rd = 0; rd < rounds; ++rd) {
-    const long long s = wlo + rd * 32 + lane;
-    uint32_t g = 0, cnt = 0;
-    ushort4 r = make_ushort4(0, 0, 0, 0);
-    if (s < n) {
-      g = order[s];
-      cnt = n_tiles[g];
-      if (cnt) r = rect[g];
-    }
+    BinLane nxt{};
+    if (rd + 1 < rounds) nxt = pipe.next(rd);
+    const uint32_t g = cur.g, cnt = cur.cnt;
+    const ushort4 r = make_ushort4((uint16_t)cur.x0(), (uint16_t)cur.y0(), (uint16_t)cur.x1(), (uint16_t)cur.y1());
     uint32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(kBinThreads)
       __syncwarp();
     }
     __syncwarp();  // (s_nz is rewritten by the next round)
+    cur = nxt;
   }
 }
 #endif

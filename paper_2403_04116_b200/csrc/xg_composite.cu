@@ -431,9 +431,19 @@ __device__ __forceinline__ int compact_fwd_split(const Raw& raw, const Unit& u, 
       const float mdx = fmaxf(fabsf(mx), fabsf(e - mx)), mdy = fmaxf(fabsf(my - u.ya), fabsf(u.yb - my));
       const float dmax = 4.f * fabsf(C) * mdy + fabsf(4.f * C) + 2.f * fabsf(B) * mdx;
       unsafe = !(dmax <= 120.f) || !(C >= -15.f);
+      // A flushed E_0 (p2 + la < -126) is harmless when no row within 7 of
+      // it in the lane's column is one the reference blends (p2 >= kCut2):
+      // along a column p2 = C2 (y - y*)^2 + P* with P* <= 0, so a blended row
+      // has |y - y*| <= a = sqrt(-kCut2 / |C2|) and p2 rises towards it by at
+      // most |C2| ((a + 7)^2 - a^2) = 14 sqrt(-kCut2 |C2|) + 49 |C2|; if that
+      // stays below 126 + kCut2 + la, flushed rows only drop pairs the
+      // reference skips.  True for every splat wider than ~1.4 px (all
+      // BASELINE clouds); narrower ones keep the corner test.
+      const float aC = -C;
+      const bool flush_ok = 14.f * sqrtf(-kCut2 * aC) + 49.f * aC <= (126.f + kCut2) + la - 1.f;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (h ? k1 : k0) {
+        if (!flush_ok && (h ? k1 : k0)) {
           const float y0 = u.ya + h * hh, y1 = y0 + 1.f;
           const float pmin = fminf(fminf(p2_at(mx, my, A, B, C, la, 0.f, y0), p2_at(mx, my, A, B, C, la, e, y0)),
                                    fminf(p2_at(mx, my, A, B, C, la, 0.f, y1), p2_at(mx, my, A, B, C, la, e, y1)));

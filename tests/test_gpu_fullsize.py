@@ -231,7 +231,8 @@ def _random_fields(rng, n, opacity, scale_lo, scale_hi, aniso):
 
 def test_image_only_narrow_and_wide_splats(xg):
     """Sub-pixel splats (anchor rows of the row recurrence underflowing: its
-    direct-EX2 fallback) mixed with wide ones, through the image-only sweep
+    direct-EX2 fallback) mixed with wide ones and ones near the width bound
+    that makes a flushed anchor harmless, through the image-only sweep
     launches, against the float32 oracle."""
     import torch
 
@@ -239,7 +240,10 @@ def test_image_only_narrow_and_wide_splats(xg):
     n = 600
     f = _random_fields(rng, n, rng.uniform(0.05, 0.9, size=n), 0.02, 0.2, 1.0)
     wide = _random_fields(rng, n, rng.uniform(0.05, 0.5, size=n), 1.0, 6.0, 1.0)
-    f = {k: np.concatenate([f[k], wide[k]]) for k in f}
+    # around the recurrence's flush bound (sigma ~ 1.4 px): some splats
+    # recurrence-safe by width alone, some by the corner test
+    mid = _random_fields(rng, n, rng.uniform(0.05, 0.9, size=n), 0.2, 1.0, 1.0)
+    f = {k: np.concatenate([f[k], wide[k], mid[k]]) for k in f}
     basis = np.ones(4, np.float32)
     cloud = xg.GaussianCloud(**f, basis_weights=basis, device="cuda")
     d = 128

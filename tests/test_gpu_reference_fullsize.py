@@ -11,6 +11,8 @@ tests/golden/make_golden_fullsize.py) - no oracle in between:
   lattice's equal-depth splats;
 * C1, C2, C3 pi/4 and C4 images within 1e-4 relative of the reference's
   float64 image (north_star tolerance), C1 radii within 1e-7 relative;
+* the sweep renderer (image-only batched launch) at C3 pi/4 and C4: images
+  within 1e-4 of the reference's;
 * C1 and C2 at phi = 0.7 with dL/dI ~ N(0,1)/HW (seed 0): kernel-level
   gradients (backward_tiles) and RenderGradients normwise within 1e-4
   (backward.py:21-124)."""
@@ -99,3 +101,24 @@ def test_gradients_equal_reference(xg, case, d):
         ok, rel = normwise_ok(getattr(grads, f).cpu().numpy(), fx[p + "grad_" + f], floor)
         assert ok, (case, f, rel)
     assert np.array_equal(grads.visible.cpu().numpy(), fx[p + "grad_visible"])
+
+
+@pytest.mark.parametrize("case", ["C3_pi4", "C4_0.7"])
+def test_sweep_images_equal_reference(xg, case):
+    """The bench's image-only path (SweepRenderer, batched launch: speculative
+    batches, row recurrence for every batch of these wide splats) against the
+    reference's float64 image at the north-star tolerance."""
+    import torch
+
+    from paper_2403_04116_b200.inference import SweepRenderer
+
+    g = fg.G_OF[case.split("_")[0]]
+    cloud = xg.GaussianCloud(**fg.cloud_arrays(case), device="cuda")
+    l_so, l_sd, w, h, pitch, phi = fg.camera(case)
+    out = SweepRenderer(cloud, xg.ScannerConfig(l_so, l_sd, w, h, pitch), batch=2).render(np.array([phi, phi]))
+    torch.cuda.synchronize()
+    gold = fg.load()[case + "/image"].astype(np.float64)
+    scale = np.abs(gold).max()
+    for img in out.cpu().numpy().astype(np.float64):
+        err = np.abs(img - gold)
+        assert np.all(err <= 1e-4 * np.abs(gold) + 1e-6 * scale), (case, g, float(err.max()))

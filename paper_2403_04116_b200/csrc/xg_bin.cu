@@ -561,7 +561,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                                      w.valN1, w.offN, sp->order, n_dev, w.tail, w.tail_bytes, s)) != XG_OK) {
     return st;
   }
-  // (development aid, tools/probe_bin_stages.py: XG_BIN_STOP=1 stops after
+  // (development aid, tools/probe_bin_graph.py: XG_BIN_STOP=1 stops after
   // the depth sort, 2 after the count / scan / ranges - the stage costs
   // inside a concurrent sweep; results are then incomplete)
   static const int bin_stop = getenv("XG_BIN_STOP") ? atoi(getenv("XG_BIN_STOP")) : 0;

@@ -567,32 +567,39 @@ size_t onesweep_workspace_bytes(int64_t cap) {
          align_up(sizeof(uint32_t) * kOsPasses) + align_up(sizeof(uint32_t) * (size_t)kOsPasses * tiles * 256) + 256;
 }
 
-xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_t* vals_in,
-                                unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a,
-                                uint32_t* vals_b, uint32_t* vals_out, int64_t cap, const uint32_t* n_dev,
-                                void* ws, size_t ws_bytes, cudaStream_t s, int n_passes, const int** result_sel) {
-  if (cap <= 0) return XG_OK;
-  if (ws_bytes < onesweep_workspace_bytes(cap)) {
-    set_error_msg("onesweep_sort_pairs64: workspace too small");
-    return XG_ERR_WORKSPACE;
-  }
-  const int64_t tiles = (cap + kOsTile - 1) / kOsTile;
+namespace {
+
+struct OsWs {
+  uint32_t* ghist;  // [kOsPasses][256]
+  uint32_t* gofs;   // [kOsPasses][256]
+  int* sel;         // [kOsPasses + 1]
+  uint32_t* ctr;    // [kOsPasses]
+  uint32_t* status; // [kOsPasses][tiles][256]
+  int64_t tiles;
+};
+
+// carve the workspace and zero what n_passes passes use (histograms,
+// counters and their look-back status words)
+OsWs os_prepare(void* ws, int64_t cap, int n_passes, cudaStream_t s) {
+  OsWs w;
+  w.tiles = (cap + kOsTile - 1) / kOsTile;
   char* p = (char*)ws;
-  uint32_t* ghist = (uint32_t*)p;
-  uint32_t* gofs = ghist + kOsPasses * 256;
+  w.ghist = (uint32_t*)p;
+  w.gofs = w.ghist + kOsPasses * 256;
   p += align_up(sizeof(uint32_t) * kOsPasses * 256 * 2);
-  int* sel = (int*)p;
+  w.sel = (int*)p;
   p += align_up(sizeof(int) * (kOsPasses + 1));
-  uint32_t* ctr = (uint32_t*)p;
+  w.ctr = (uint32_t*)p;
   p += align_up(sizeof(uint32_t) * kOsPasses);
-  uint32_t* status = (uint32_t*)p;
-  cudaMemsetAsync(ws, 0, onesweep_workspace_bytes(cap), s);
-  const int hgrid = (int)(tiles < 296 ? tiles : 296);
-  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys_in, n_dev, cap, ghist, n_passes);
-  xg_status st = check_launch("k_os_hist");
-  if (st != XG_OK) return st;
-  k_os_scan<<<1, 256, 0, s>>>(ghist, gofs, n_dev, cap, sel, n_passes);
-  if ((st = check_launch("k_os_scan")) != XG_OK) return st;
+  w.status = (uint32_t*)p;
+  const int np = n_passes < kOsPasses ? n_passes : kOsPasses;
+  cudaMemsetAsync(ws, 0, (size_t)(p - (char*)ws) + sizeof(uint32_t) * (size_t)np * w.tiles * 256, s);
+  return w;
+}
+
+xg_status os_passes(const OsWs& w, const unsigned long long* keys_in, const uint32_t* vals_in,
+                    unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                    int64_t cap, const uint32_t* n_dev, int n_passes, cudaStream_t s) {
   for (int pass = 0; pass < n_passes && pass < kOsPasses; ++pass) {  // (higher bytes all zero: no-op passes)
     OsArgs a;
     a.keys[0] = keys_a;
@@ -604,19 +611,44 @@ xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_
     a.n_dev = n_dev;
     a.cap = cap;
     a.pass = pass;
-    a.ghist = ghist;
-    a.gofs = gofs;
-    a.sel = sel;
-    a.status = status + (size_t)pass * tiles * 256;
-    a.tile_ctr = ctr + pass;
-    k_os_pass<<<(int)tiles, kOsThreads, 0, s>>>(a);
-    if ((st = check_launch("k_os_pass")) != XG_OK) return st;
+    a.ghist = w.ghist;
+    a.gofs = w.gofs;
+    a.sel = w.sel;
+    a.status = w.status + (size_t)pass * w.tiles * 256;
+    a.tile_ctr = w.ctr + pass;
+    k_os_pass<<<(int)w.tiles, kOsThreads, 0, s>>>(a);
+    xg_status st = check_launch("k_os_pass");
+    if (st != XG_OK) return st;
   }
+  return XG_OK;
+}
+
+}  // namespace
+
+xg_status onesweep_sort_pairs64(const unsigned long long* keys_in, const uint32_t* vals_in,
+                                unsigned long long* keys_a, unsigned long long* keys_b, uint32_t* vals_a,
+                                uint32_t* vals_b, uint32_t* vals_out, int64_t cap, const uint32_t* n_dev,
+                                void* ws, size_t ws_bytes, cudaStream_t s, int n_passes, const int** result_sel) {
+  if (cap <= 0) return XG_OK;
+  if (ws_bytes < onesweep_workspace_bytes(cap)) {
+    set_error_msg("onesweep_sort_pairs64: workspace too small");
+    return XG_ERR_WORKSPACE;
+  }
+  const OsWs w = os_prepare(ws, cap, n_passes, s);
+  const int hgrid = (int)(w.tiles < 296 ? w.tiles : 296);
+  k_os_hist<<<hgrid, kOsThreads, 0, s>>>(keys_in, n_dev, cap, w.ghist, n_passes);
+  xg_status st = check_launch("k_os_hist");
+  if (st != XG_OK) return st;
+  k_os_scan<<<1, 256, 0, s>>>(w.ghist, w.gofs, n_dev, cap, w.sel, n_passes);
+  if ((st = check_launch("k_os_scan")) != XG_OK) return st;
+  if ((st = os_passes(w, keys_in, vals_in, keys_a, keys_b, vals_a, vals_b, cap, n_dev, n_passes, s)) != XG_OK)
+    return st;
   if (result_sel) {  // the caller reads vals {a, b, in}[sel[8]] itself
-    *result_sel = sel + kOsPasses;
+    *result_sel = w.sel + kOsPasses;
     return XG_OK;
   }
-  k_os_finish<<<(int)(tiles < 296 ? tiles : 296), 256, 0, s>>>(vals_out, vals_a, vals_b, vals_in, n_dev, cap, sel);
+  k_os_finish<<<(int)(w.tiles < 296 ? w.tiles : 296), 256, 0, s>>>(vals_out, vals_a, vals_b, vals_in, n_dev, cap,
+                                                                  w.sel);
   return check_launch("k_os_finish");
 }
 
@@ -666,8 +698,10 @@ struct BsWs {
   uint32_t* large;           // [kBsBuckets]
   uint32_t* mixed;           // [kBsBuckets]
   uint32_t* n_mixed;
-  void* tail;                // scan / onesweep workspace
+  void* tail;                // onesweep workspace
   size_t tail_bytes;
+  void* scan_ws;             // the bucket-count scan's workspace (after it)
+  size_t scan_bytes;
 };
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -688,6 +722,9 @@ inline bool bs_carve(void* ws, size_t bytes, BsWs& w) {
   w.large = (uint32_t*)p; p += al256(sizeof(uint32_t) * kBsBuckets);
   w.mixed = (uint32_t*)p; p += al256(sizeof(uint32_t) * kBsBuckets);
   w.n_mixed = (uint32_t*)p; p += 256;
+  w.scan_ws = p;
+  w.scan_bytes = al256(scan_workspace_bytes(kBsBuckets));
+  p += w.scan_bytes;
   w.tail = p;
   const size_t used = (size_t)(p - (char*)ws);
   if (used > bytes) return false;
@@ -741,12 +778,17 @@ __device__ __forceinline__ unsigned long long peer_min64(unsigned peers, unsigne
   return ((unsigned long long)hi << 32) | lo;
 }
 
-// bucket ids (the stable sort's keys), the iota values, per-bucket counts and key range
+// bucket ids (the stable sort's keys), the iota values, per-bucket counts and
+// key range, and the two byte histograms of the ids the onesweep passes need
+// (ghist[0] low byte, ghist[1] high byte; in place of a k_os_hist pass)
 __global__ void k_bs_bucket(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,
                             long long n, const unsigned long long* __restrict__ mm,
                             unsigned long long* __restrict__ bkey, uint32_t* __restrict__ iota,
                             uint32_t* __restrict__ count, unsigned long long* __restrict__ bmin,
-                            unsigned long long* __restrict__ bmax) {
+                            unsigned long long* __restrict__ bmax, uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t s_h[2][256];
+  for (int k = threadIdx.x; k < 512; k += blockDim.x) (&s_h[0][0])[k] = 0u;
+  __syncthreads();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int shift = bs_shift(mm);
   const unsigned long long kmin = mm[0];
@@ -765,10 +807,17 @@ __global__ void k_bs_bucket(const unsigned long long* __restrict__ keys, const u
   const unsigned long long lo = peer_min64(peers, k), nhi = peer_min64(peers, ~k);
   if (valid && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) {
     atomicAdd(&count[b], (uint32_t)__popc(peers));
+    atomicAdd(&s_h[0][b & 255u], (uint32_t)__popc(peers));
+    atomicAdd(&s_h[1][b >> 8], (uint32_t)__popc(peers));
     if (b != kBsInactive) {
       atomicMin(&bmin[b], lo);
       atomicMin(&bmax[b], nhi);
     }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 512; k += blockDim.x) {
+    const uint32_t v = (&s_h[0][0])[k];
+    if (v) atomicAdd(&ghist[k], v);
   }
 }
 
@@ -1027,8 +1076,7 @@ __global__ void __launch_bounds__(128) k_bs_mixed(const unsigned long long* __re
 }  // namespace
 
 size_t bucket_sort_workspace_bytes(int64_t n) {
-  const size_t a = onesweep_workspace_bytes(n), b = scan_workspace_bytes(kBsBuckets);
-  return bs_fixed_bytes() + (a > b ? a : b) + 256;
+  return bs_fixed_bytes() + al256(scan_workspace_bytes(kBsBuckets)) + onesweep_workspace_bytes(n) + 256;
 }
 
 xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_tiles, int64_t n,
@@ -1036,7 +1084,7 @@ xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_ti
                             uint32_t* order, uint32_t* n_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (n < 1) return XG_OK;
   BsWs w;
-  if (!bs_carve(ws, ws_bytes, w)) {
+  if (!bs_carve(ws, ws_bytes, w) || w.tail_bytes < onesweep_workspace_bytes(n)) {
     set_error_msg("bucket_sort_depth: workspace too small");
     return XG_ERR_WORKSPACE;
   }
@@ -1051,16 +1099,18 @@ xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_ti
   xg_status st = check_launch("k_bs_minmax");
   if (st != XG_OK) return st;
   // bucket ids into key_b, iota into val_b (the onesweep's read-only inputs)
-  k_bs_bucket<<<g, 256, 0, s>>>(keys, n_tiles, n, w.mm, key_b, val_b, w.count, w.bmin, w.bmax);
+  // (the onesweep's histograms are accumulated by k_bs_bucket: zero them first)
+  const OsWs ow = os_prepare(w.tail, n, 2, s);
+  k_bs_bucket<<<g, 256, 0, s>>>(keys, n_tiles, n, w.mm, key_b, val_b, w.count, w.bmin, w.bmax, ow.ghist);
   if ((st = check_launch("k_bs_bucket")) != XG_OK) return st;
-  if ((st = scan_u32(w.count, nullptr, w.start, kBsBuckets, nullptr, kBsBuckets, w.start + kBsBuckets, w.tail,
-                     w.tail_bytes, s)) != XG_OK)
+  if ((st = scan_u32(w.count, nullptr, w.start, kBsBuckets, nullptr, kBsBuckets, w.start + kBsBuckets, w.scan_ws,
+                     w.scan_bytes, s)) != XG_OK)
     return st;
   // stable by 16-bit bucket id: two byte passes (ids < 2^16); no final copy
-  BsSorted srt{{val_a, val_b, val_b}, nullptr};
-  if ((st = onesweep_sort_pairs64(key_b, val_b, key_a, key_b, val_a, val_b, nullptr, n, n_dev, w.tail, w.tail_bytes,
-                                  s, 2, &srt.sel)) != XG_OK)
-    return st;
+  k_os_scan<<<1, 256, 0, s>>>(ow.ghist, ow.gofs, n_dev, n, ow.sel, 2);
+  if ((st = check_launch("k_os_scan")) != XG_OK) return st;
+  if ((st = os_passes(ow, key_b, val_b, key_a, key_b, val_a, val_b, n, n_dev, 2, s)) != XG_OK) return st;
+  BsSorted srt{{val_a, val_b, val_b}, ow.sel + kOsPasses};
   k_bs_rank<<<g, 256, 0, s>>>(keys, n_tiles, w.mm, srt, n, w.start, w.bmin, w.bmax, order, w.large, w.n_large,
                               w.mixed, w.n_mixed);
   if ((st = check_launch("k_bs_rank")) != XG_OK) return st;

@@ -1641,12 +1641,14 @@ constexpr int kBwdPairs = XG_BWD_PAIRS;
 static_assert(kBwdPairs == 1 || kBwdPairs == 2 || kBwdPairs == 4, "a sub-block is 4, 8 or 16 rows");
 constexpr int kBwdSubs = 4 / kBwdPairs;  // sub-blocks per tile
 
-template <bool kRepro>
-#ifdef XG_BWD_CK_MIN_CTAS
-__global__ void __launch_bounds__(kThreads, XG_BWD_CK_MIN_CTAS) k_composite_bwd_ck(BwdArgs a) {
-#else
-__global__ void __launch_bounds__(kThreads) k_composite_bwd_ck(BwdArgs a) {
+// (min 3 CTAs per SM: ptxas then keeps the atomic variant at 156 registers
+// without spills; unbounded it settles at 128 registers with a 16 B spill,
+// 1 % slower per C2 iteration; 4 CTAs spill more)
+#ifndef XG_BWD_CK_MIN_CTAS
+#define XG_BWD_CK_MIN_CTAS 3
 #endif
+template <bool kRepro>
+__global__ void __launch_bounds__(kThreads, XG_BWD_CK_MIN_CTAS) k_composite_bwd_ck(BwdArgs a) {
   __shared__ BRec s_rec[kWarps][32];
   __shared__ int s_k[kWarps][32];
   __shared__ uint32_t s_gid[kWarps][32];

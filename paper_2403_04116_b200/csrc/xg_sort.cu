@@ -465,8 +465,10 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
   const uint32_t tile = s_tile;
   const long long base = (long long)tile * kOsTile;
   if (base >= n) return;
-  const unsigned long long* kin = a.keys[src];
-  const uint32_t* vin = a.vals[src];
+  // (selects, not a[idx]: a runtime index into the parameter arrays would
+  // copy them to local memory)
+  const unsigned long long* kin = src == 0 ? a.keys[0] : src == 1 ? a.keys[1] : a.keys[2];
+  const uint32_t* vin = src == 0 ? a.vals[0] : src == 1 ? a.vals[1] : a.vals[2];
   const unsigned lt = lanemask_lt();
   unsigned long long key[kOsRounds];
   uint32_t val[kOsRounds], pos[kOsRounds];
@@ -532,8 +534,9 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(OsArgs a) {
     }
   }
   __syncthreads();
-  unsigned long long* kout = a.keys[a.sel[p + 1]];
-  uint32_t* vout = a.vals[a.sel[p + 1]];
+  const int dst = a.sel[p + 1];
+  unsigned long long* kout = dst == 0 ? a.keys[0] : dst == 1 ? a.keys[1] : a.keys[2];
+  uint32_t* vout = dst == 0 ? a.vals[0] : dst == 1 ? a.vals[1] : a.vals[2];
   const uint32_t* go = a.gofs + p * 256;
 #pragma unroll
   for (int r = 0; r < kOsRounds; ++r) {
@@ -829,7 +832,10 @@ __device__ __forceinline__ bool bs_less(unsigned long long ka, uint32_t ia, unsi
 struct BsSorted {  // the stable pass's result: vals {a, b, in}[*sel]
   const uint32_t* v[3];
   const int* sel;
-  __device__ __forceinline__ const uint32_t* get() const { return v[*sel]; }
+  __device__ __forceinline__ const uint32_t* get() const {
+    const int k = *sel;
+    return k == 0 ? v[0] : k == 1 ? v[1] : v[2];
+  }
 };
 
 __global__ void k_bs_rank(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,

@@ -55,6 +55,9 @@ class SweepRenderer:
         prio = -1 if (self.batch > 1 and os.environ.get("XG_BIN_PRIORITY", "0") == "1") else 0
         self.streams = [torch.cuda.Stream(device=cloud.device, priority=prio) for _ in range(n)]
         self.comp_stream = torch.cuda.Stream(device=cloud.device) if self.batch > 1 else None
+        # device -> host image copies (host_out) on their own stream, so a copy
+        # never holds up the next compositing launch or binning on its stream
+        self.copy_stream = torch.cuda.Stream(device=cloud.device)
         self.capacity_factor = capacity_factor
         self.frames: list[Frame] = []
         self.capacity = 0
@@ -113,7 +116,7 @@ class SweepRenderer:
 
     def _render_streams(self, angles, out, host_out, status, composite_events) -> None:
         main = torch.cuda.current_stream()
-        for s in self.streams:
+        for s in self.streams + [self.copy_stream]:
             s.wait_stream(main)
         for i, phi in enumerate(angles):
             k = i % len(self.streams)
@@ -131,16 +134,18 @@ class SweepRenderer:
                 else:
                     fr.composite(image_out=out[i], track=False)
                 status[i : i + 1].copy_(fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
-                if host_out is not None:
+            if host_out is not None:
+                self.copy_stream.wait_stream(st)
+                with torch.cuda.stream(self.copy_stream):
                     host_out[i].copy_(out[i], non_blocking=True)
-        for s in self.streams:
+        for s in self.streams + [self.copy_stream]:
             main.wait_stream(s)
         self.kernel_launches = len(angles)
 
     def _render_batched(self, angles, out, host_out, status, composite_events) -> None:
         main = torch.cuda.current_stream()
         cs, K = self.comp_stream, self.batch
-        for s in self.streams + [cs]:
+        for s in self.streams + [cs, self.copy_stream]:
             s.wait_stream(main)
         done = [None, None]  # composite-finished event per frame set
         lib = nat.lib()
@@ -171,12 +176,14 @@ class SweepRenderer:
                     composite_events.append((a, b, nv))
                 for i in range(nv):
                     status[lo + i : lo + i + 1].copy_(fs[i].counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
-                if host_out is not None:
-                    host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(cs)
                 done[j % 2] = ev
-        for s in self.streams + [cs]:
+            if host_out is not None:
+                self.copy_stream.wait_event(ev)
+                with torch.cuda.stream(self.copy_stream):
+                    host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
+        for s in self.streams + [cs, self.copy_stream]:
             main.wait_stream(s)
         self.kernel_launches = (len(angles) + K - 1) // K
 

@@ -278,14 +278,12 @@ __global__ void __launch_bounds__(kBinThreads)
   }
 }
 
-__global__ void k_flag_overflow(uint32_t* counters, long long cap) {
-  if (threadIdx.x == 0 && (long long)counters[XG_CTR_ENTRIES] > cap)
-    atomicOr(&counters[XG_CTR_STATUS], XG_ST_ENTRY_OVERFLOW);
-}
-
-__global__ void k_bin_ranges(const uint32_t* __restrict__ offs, int C, int T, const uint32_t* counters,
+// (tile ranges from the scanned (tile, chunk) table; thread 0 also flags an
+// entry-buffer overflow, which only needs the scan's total)
+__global__ void k_bin_ranges(const uint32_t* __restrict__ offs, int C, int T, uint32_t* counters, long long cap,
                              long long* __restrict__ ranges) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0 && (long long)counters[XG_CTR_ENTRIES] > cap) atomicOr(&counters[XG_CTR_STATUS], XG_ST_ENTRY_OVERFLOW);
   if (t >= T) return;
   ranges[2 * t] = offs[(long long)t * C];
   ranges[2 * t + 1] = t + 1 < T ? (long long)offs[(long long)(t + 1) * C] : (long long)counters[XG_CTR_ENTRIES];
@@ -588,15 +586,13 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
                        w.tail_bytes, s)) != XG_OK)
       return st;
-    k_bin_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(w.hoff, C, n_tiles, sp->counters,
+    k_bin_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(w.hoff, C, n_tiles, sp->counters, cap,
                                                       (long long*)sp->tile_ranges);
     if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
     if (bin_stop == 2) return XG_OK;
     k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
                                                bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
     if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
-    k_flag_overflow<<<1, 32, 0, s>>>(sp->counters, cap);
-    if ((st = check_launch("k_flag_overflow")) != XG_OK) return st;
     if (!sp->tile_order) return XG_OK;
     return launch_tile_order(sp->tile_ranges, n_tiles, sp->tile_order, s);
   }

@@ -403,24 +403,28 @@ __global__ void __launch_bounds__(kOsThreads)
 __global__ void __launch_bounds__(256) k_os_scan(const uint32_t* __restrict__ ghist, uint32_t* __restrict__ gofs,
                                                  const uint32_t* n_dev, long long cap, int* __restrict__ sel,
                                                  int n_passes) {
-  __shared__ uint32_t s[256];
+  __shared__ uint32_t s_w[8];
   __shared__ int trivial[kOsPasses];
   long long n = *n_dev;
   if (n > cap) n = cap;
-  const int d = threadIdx.x;
-  for (int p = 0; p < kOsPasses; ++p) {
+  const int d = threadIdx.x, lane = d & 31, w = d >> 5;
+  if (d < kOsPasses) trivial[d] = 1;  // (passes past n_passes: the caller's keys are zero there)
+  __syncthreads();
+  for (int p = 0; p < n_passes && p < kOsPasses; ++p) {
+    // exclusive scan of the pass's 256 digit counts: warp shuffles + 8 warp totals
     const uint32_t v = ghist[p * 256 + d];
-    const int t = __syncthreads_or((long long)v == n);
-    if (d == 0) trivial[p] = t || p >= n_passes;  // (passes past n_passes: the caller's keys are zero there)
-    s[d] = v;
-    __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele
-      const uint32_t x = d >= o ? s[d - o] : 0u;
-      __syncthreads();
-      s[d] += x;
-      __syncthreads();
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    gofs[p * 256 + d] = s[d] - v;
+    if (lane == 31) s_w[w] = x;
+    const int t = __syncthreads_or((long long)v == n);  // (also orders s_w)
+    uint32_t base = 0;
+    for (int k = 0; k < w; ++k) base += s_w[k];
+    gofs[p * 256 + d] = base + x - v;
+    if (d == 0) trivial[p] = t;
     __syncthreads();
   }
   // buffers: 0 / 1 ping-pong scratch, 2 the caller's input (never written)

@@ -1166,10 +1166,11 @@ struct BRec {
 // directly (no acc - prefix - contrib cancellation) and T restored by
 // division by (1 - sigma).  Packed state: T, nS = -S (suffix sum), g.
 // Produces, per pixel, nG = -(dL/dsigma * sigma) on unclamped pairs (the
-// reference's g_power) and ngw = -(g * w) (the intensity gradient).
+// reference's g_power) and nw = -w = -(sigma T) (the caller accumulates
+// the intensity gradient sum of g w with one FFMA2 per pair).
 template <bool kGeneral>
 __device__ __forceinline__ void unblend2(const BRec& r, float2 dy, float bdx, float adx2, bool act0, bool act1,
-                                         float2 g, float2& T, float2& nS, float2& nG, float2& ngw) {
+                                         float2 g, float2& T, float2& nS, float2& nG, float2& nw_out) {
   const float2 p = __ffma2_rn(__ffma2_rn(bc(r.b.x), dy, bc(bdx)), dy, bc(adx2));
   float2 ns = __fmul2_rn(bc(r.b.y), make_float2(ex2_approx(p.x), ex2_approx(p.y)));  // -sigma (raw)
   bool v0 = act0 & (p.x >= kCut2), v1 = act1 & (p.y >= kCut2);
@@ -1188,7 +1189,7 @@ __device__ __forceinline__ void unblend2(const BRec& r, float2 dy, float bdx, fl
   const float2 rc = make_float2(rcp_approx(om.x), rcp_approx(om.y));
   const float2 Tb = __fmul2_rn(T, rc);        // T before this splat
   const float2 nw = __fmul2_rn(ns, Tb);       // -(sigma T)
-  ngw = __fmul2_rn(g, nw);
+  nw_out = nw;
   const float2 in = __ffma2_rn(nS, rc, __fmul2_rn(bc(r.b.z), Tb));  // i T - S / (1 - sigma)
   const float2 dsig = __fmul2_rn(g, in);
   nG = __fmul2_rn(dsig, ns);
@@ -1219,20 +1220,20 @@ __device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx,
 #pragma unroll
   for (int i = 0; i < kP; ++i) {
     const float2 dy = __fadd2_rn(fy[i], bc(r.a.y));
-    float2 nG, ngw;
+    float2 nG, nw;
     unblend2<kGeneral>(r, dy, bdx, adx2, krel <= last[2 * i], krel <= last[2 * i + 1], g[i], T[i], nS[i], nG,
-                       ngw);
+                       nw);
     const float2 Gdy = __fmul2_rn(nG, dy);
     if (i == 0) {
       sG = nG;
       sGdy = Gdy;
       sGdy2 = __fmul2_rn(Gdy, dy);
-      sgw = ngw;
+      sgw = __fmul2_rn(g[i], nw);
     } else {
       sG = __fadd2_rn(sG, nG);
       sGdy = __fadd2_rn(sGdy, Gdy);
       sGdy2 = __ffma2_rn(Gdy, dy, sGdy2);
-      sgw = __fadd2_rn(sgw, ngw);
+      sgw = __ffma2_rn(g[i], nw, sgw);
     }
   }
   const float Gs = sG.x + sG.y, Gdys = sGdy.x + sGdy.y;
@@ -1272,7 +1273,6 @@ __device__ __forceinline__ bool unblend_splat_spec(const BRec& r, float fx, cons
     const float2 rc = make_float2(rcp_approx(om.x), rcp_approx(om.y));
     const float2 Tb = __fmul2_rn(T[i], rc);
     const float2 nw = __fmul2_rn(ns, Tb);
-    const float2 ngw = __fmul2_rn(g[i], nw);
     const float2 in = __ffma2_rn(nS[i], rc, __fmul2_rn(bc(r.b.z), Tb));
     const float2 nG = __fmul2_rn(__fmul2_rn(g[i], in), ns);
     nS[i] = __ffma2_rn(bc(r.b.z), nw, nS[i]);
@@ -1282,12 +1282,12 @@ __device__ __forceinline__ bool unblend_splat_spec(const BRec& r, float fx, cons
       sG = nG;
       sGdy = Gdy;
       sGdy2 = __fmul2_rn(Gdy, dy);
-      sgw = ngw;
+      sgw = __fmul2_rn(g[i], nw);
     } else {
       sG = __fadd2_rn(sG, nG);
       sGdy = __fadd2_rn(sGdy, Gdy);
       sGdy2 = __ffma2_rn(Gdy, dy, sGdy2);
-      sgw = __fadd2_rn(sgw, ngw);
+      sgw = __ffma2_rn(g[i], nw, sgw);
     }
   }
   const float Gs = sG.x + sG.y, Gdys = sGdy.x + sGdy.y;

@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (1M Gaussians, 1024^2) stress block")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 (50k Gaussians, 256^2 fwd+bwd) block")
     ap.add_argument("--no-c5", action="store_true", help="N = 1: skip the C5-size (493k) training block")
+    ap.add_argument("--collective", choices=("nccl", "p2p"), default="nccl",
+                    help="C5 data-parallel gradient step: bucketed NCCL all-reduce + fused Adam, or the peer-memory "
+                         "reduce-scatter / all-gather-Adam kernels (parallel.PeerExchange, csrc/xg_dp.cu)")
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
                     help="C3 under N GPUs: the 360-view sweep sharded over them (strong, BASELINE configs[2]) "
                          "or 360 views per GPU (weak)")
@@ -931,7 +934,7 @@ def train_block(args, timed, clock_cls, local, world: int = 1, c5: bool = False)
             tr = Trainer(ds, GaussianCloud(**init, device="cuda"), cfg, targets_on_host=(mode == "e2e"))
         else:
             tr = DataParallelTrainer(ds, GaussianCloud(**init, device="cuda"), cfg,
-                                     targets_on_host=(mode == "e2e"))
+                                     targets_on_host=(mode == "e2e"), collective=args.collective)
         warm = max(args.warmup, 5)  # reach densify_from_iter = 500
         for _ in range(warm * per):
             tr.step()
@@ -976,7 +979,10 @@ def train_block(args, timed, clock_cls, local, world: int = 1, c5: bool = False)
             f"100-view 512x512 sweep, full iterations incl. densify/prune every 100 ({per // 100} events per step)"
             if not c5 else
             f"C5: {(2 * (g // 4) + 3) ** 3:,} Gaussians, 512x512, data-parallel x{world}: one view per GPU per "
-            "step, NCCL all-reduce of the 27N gradient bucketed and overlapped with the fused Adam"
+            + ("step, NCCL all-reduce of the 27N gradient bucketed and overlapped with the fused Adam"
+               if args.collective == "nccl" else
+               "step, the 27N gradient reduce-scattered and all-gathered over peer memory with Adam fused "
+               "into the all-gather (csrc/xg_dp.cu)")
             + (" (N = 1: no collective, the curve's single-GPU point)" if world == 1 else ""))
     blk = {"metric": "train iters/s", "value": iters / (d["ms"] / 1e3), "unit": "iters/s",
             "views_per_s": iters * world / (d["ms"] / 1e3),

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define XG_ABI_VERSION 3
+#define XG_ABI_VERSION 4
 
 typedef enum xg_status {
   XG_OK = 0,
@@ -61,6 +61,7 @@ typedef enum xg_status {
 #define XG_ST_GRAD_NONFINITE_SHIFT 8 /* bits 8..12: non-finite gradient per field
                                         positions, rotations, log_scales,
                                         raw_opacities, features (trainer.py:160-162) */
+#define XG_ST_PEER_TIMEOUT     0x10u /* a peer-exchange wait timed out (xg_peer_*) */
 
 /* counters[] layout (uint32, device). */
 #define XG_CTR_ACTIVE   0   /* splats surviving near-plane + on-screen cull  */
@@ -307,6 +308,38 @@ xg_status xg_adam_range(float* params, const float* grads, float* exp_avg, float
                         int64_t elem_begin, int64_t elem_end, void* stream);
 xg_status xg_adam_renorm(float* params, int64_t n, int32_t n_features, const uint32_t* status,
                          void* stream);
+
+/* K5: the data-parallel step's gradient exchange fused with Adam, over peer
+ * memory (one process per GPU, each rank's buffers mapped into every process
+ * by CUDA IPC; parallel.PeerExchange).  Replaces the bucketed NCCL
+ * all-reduce + xg_adam_range of parallel.DataParallelTrainer
+ * (trainer.py:158-170 semantics on the SUMMED gradient):
+ *   xg_peer_reduce_scatter  signal ready, wait for every rank, sum slice
+ *     `rank` of the flat gradient over the ranks in rank order (peer loads)
+ *     into xbuf[rank] (epoch parity half), publish its per-field non-finite
+ *     bits to every rank, signal arrived;
+ *   xg_peer_allgather_adam  wait for every rank's arrival, read each slice
+ *     from its owner (peer loads) and apply Adam to the whole buffer (the
+ *     arithmetic of xg_adam_range), honouring the global non-finite bits;
+ *     the quaternion renorm follows with xg_adam_renorm(sticky).
+ * Slice length: xg_peer_slice (multiple of 4); xbuf[k] holds 2 slices,
+ * sync[k] 8 zero-initialised words.  epoch = 1, 2, ... (one per exchange).
+ * Waits are bounded (~10 s): a timeout ORs XG_ST_PEER_TIMEOUT into *sticky.
+ * Every rank adds the same values in the same order: bit-identical replicas. */
+#define XG_PEER_MAX 8
+typedef struct xg_peer_group {
+  int32_t rank, world;
+  uint32_t epoch;
+  const float* grads[XG_PEER_MAX];  /* each rank's flat gradient (peer-mapped) */
+  float* xbuf[XG_PEER_MAX];         /* each rank's exchange buffer, 2 x slice  */
+  uint32_t* sync[XG_PEER_MAX];      /* each rank's 8 sync words                */
+} xg_peer_group;
+int64_t xg_peer_slice(int64_t n, int32_t n_features, int32_t world);
+xg_status xg_peer_reduce_scatter(const xg_peer_group* pg, int64_t n, int32_t n_features, uint32_t* sticky,
+                                 void* stream);
+xg_status xg_peer_allgather_adam(const xg_peer_group* pg, float* params, float* exp_avg, float* exp_avg_sq,
+                                 int64_t n, int32_t n_features, const double* lr, double beta1, double beta2,
+                                 double eps, double bc1, double bc2, uint32_t* sticky, void* stream);
 
 /* K4d (1): density-control masks.  flags[N] bit0 high-gradient, bit1 large,
  * bit2 prune, bit3 clone, bit4 split; counts[4] = {prune, clone, split, keep}

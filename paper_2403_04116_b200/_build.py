@@ -27,7 +27,7 @@ OBJ = PKG / "csrc" / "_obj"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
 PER_FILE = {"xg_preprocess.cu": ["-fmad=false"], "xg_project.cu": ["-fmad=false"], "xg_tiles64.cu": ["-fmad=false"]}
-SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu", "xg_project.cu", "xg_tiles64.cu"]
+SOURCES = ["xg_common.cu", "xg_preprocess.cu", "xg_sort.cu", "xg_bin.cu", "xg_composite.cu", "xg_optim.cu", "xg_ssim.cu", "xg_project.cu", "xg_tiles64.cu", "xg_dp.cu"]
 
 
 def nvcc() -> str:

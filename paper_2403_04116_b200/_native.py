@@ -31,11 +31,13 @@ XG_ST_DEGENERATE = 0x2
 XG_ST_NONFINITE_FEAT = 0x4
 XG_ST_ENTRY_OVERFLOW = 0x8
 XG_ST_GRAD_SHIFT = 8
+XG_ST_PEER_TIMEOUT = 0x10
+XG_PEER_MAX = 8
 XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1, 2, 4, 5
 XG_CTR_ITEMS = 6
 XG_CTR_L1 = 8  # words 8-9: the fused-L1 double, zeroed by xg_preprocess_fwd
 XG_NCOUNTERS = 10
-XG_ABI_VERSION = 3
+XG_ABI_VERSION = 4
 XG_REPLAY_CHUNK = 256
 XG_MAX_BATCH = 16
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
@@ -59,6 +61,19 @@ class XgVolume(ctypes.Structure):
 
 class XgConeView(ctypes.Structure):
     _fields_ = [("source", c_f64 * 3), ("rot", c_f64 * 9), ("focal", c_f64), ("width", c_i32), ("height", c_i32)]
+
+
+class XgPeerGroup(ctypes.Structure):
+    """xg_peer_group (include/xgauss.h): every rank's peer-mapped buffers."""
+
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("epoch", ctypes.c_uint32),
+        ("grads", c_void_p * XG_PEER_MAX),
+        ("xbuf", c_void_p * XG_PEER_MAX),
+        ("sync", c_void_p * XG_PEER_MAX),
+    ]
 
 
 class XgSplats(ctypes.Structure):
@@ -126,6 +141,13 @@ SIGNATURES = {
          c_void_p, c_i64, c_i64, c_void_p],
     ),
     "xg_adam_renorm": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
+    "xg_peer_slice": (c_i64, [c_i64, c_i32, c_i32]),
+    "xg_peer_reduce_scatter": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
+    "xg_peer_allgather_adam": (
+        c_i32,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_f64, c_f64, c_f64, c_f64, c_f64,
+         c_void_p, c_void_p],
+    ),
     "xg_densify_mark": (
         c_i32,
         [c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_void_p],
@@ -262,6 +284,8 @@ def raise_for_status(word: int, where: str = "") -> None:
         raise NumericalDegeneracyError("projected covariance not positive definite")
     if word & XG_ST_NONFINITE_FEAT:
         raise InvalidParameterError("feature and weights must be finite")
+    if word & XG_ST_PEER_TIMEOUT:
+        raise NativeError("peer gradient exchange timed out (a rank stopped stepping)")
     grad = (word >> XG_ST_GRAD_SHIFT) & 0x1F
     if grad:
         for f, name in enumerate(PARAM_FIELDS):

@@ -77,7 +77,8 @@ __global__ void k_adam(AdamArgs a) {
     v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(omb2, g), g));
     a.m[e] = m;
     a.v[e] = v;
-    a.p[e] = a.p[e] - lrf[f] * __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps));
+    // (explicitly rounded: the peer-exchange Adam, xg_dp.cu, must match bit for bit)
+    a.p[e] = __fsub_rn(a.p[e], __fmul_rn(lrf[f], __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps))));
   }
 }
 

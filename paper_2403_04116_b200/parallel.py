@@ -26,6 +26,8 @@ the step's gradient is the sum of the per-view reference gradients.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -124,6 +126,64 @@ class GradientAllReducer:
                 epilogue(lo, hi)
 
 
+class PeerExchange:
+    """The peer-memory form of the data-parallel gradient step (K5,
+    csrc/xg_dp.cu): every rank's flat gradient, exchange buffer and sync
+    words mapped into this process by CUDA IPC (torch's CUDA tensor sharing,
+    handles exchanged once with ``all_gather_object``), then per step two
+    kernels - reduce-scatter of the gradient into the exchange buffers and
+    an all-gather whose epilogue is the fused Adam - with device-side,
+    epoch-counted waits instead of a collective library call.  Rebuilt when
+    the gradient buffer changes (density control); the rebuild synchronises
+    every rank first, so no kernel still reads the buffers it drops."""
+
+    def __init__(self, grads: torch.Tensor, n: int, nf: int, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.rank, self.world = world_info(group)
+        if self.world > nat.XG_PEER_MAX:
+            raise ValueError(f"peer exchange supports up to {nat.XG_PEER_MAX} ranks")
+        self.group = group
+        self.n, self.nf = int(n), int(nf)
+        slice_len = int(nat.lib().xg_peer_slice(self.n, self.nf, self.world))
+        self.xbuf = torch.zeros(2 * slice_len, dtype=torch.float32, device=grads.device)
+        self.sync = torch.zeros(8, dtype=torch.int32, device=grads.device)
+        self.key = (grads.data_ptr(), grads.numel())
+        torch.cuda.synchronize(grads.device)
+        own = (grads, self.xbuf, self.sync)
+        shared = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(shared, [reduce_tensor(t) for t in own], group=group)
+        self._peers = []  # the peer-mapped tensors, kept alive with the exchange
+        pg = nat.XgPeerGroup()
+        pg.rank, pg.world, pg.epoch = self.rank, self.world, 0
+        for k in range(self.world):
+            if k == self.rank:
+                ts = own
+            else:
+                ts = tuple(fn(*args) for fn, args in shared[k])
+                self._peers.append(ts)
+            pg.grads[k], pg.xbuf[k], pg.sync[k] = (t.data_ptr() for t in ts)
+        self.pg = pg
+        if self.world > 1:
+            dist.barrier(group=group)
+
+    def release(self) -> None:
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        self._peers.clear()
+
+    def step(self, params, exp_avg, exp_avg_sq, lr, beta1, beta2, eps, bc1, bc2, sticky_ptr: int) -> None:
+        lib = nat.lib()
+        self.pg.epoch += 1
+        nat.check(lib.xg_peer_reduce_scatter(ctypes.byref(self.pg), self.n, self.nf, sticky_ptr, nat.stream()),
+                  "xg_peer_reduce_scatter")
+        nat.check(lib.xg_peer_allgather_adam(ctypes.byref(self.pg), params.data_ptr(), exp_avg.data_ptr(),
+                                             exp_avg_sq.data_ptr(), self.n, self.nf, lr, beta1, beta2, eps, bc1,
+                                             bc2, sticky_ptr, nat.stream()), "xg_peer_allgather_adam")
+
+
 def allreduce_stats(stats, group=None) -> None:
     """Sum rank-local DensifyStats before a density-control event."""
     if not (dist.is_available() and dist.is_initialized()):
@@ -162,7 +222,9 @@ class DataParallelTrainer(Trainer):
     bucket of a field can never follow a partial update of it."""
 
     def __init__(self, dataset, cloud, cfg, group=None, bucket_bytes: int = 8 << 20, targets_on_host=False,
-                 out_dir=None, verbose: bool = False, reproducible: bool = False):
+                 out_dir=None, verbose: bool = False, reproducible: bool = False, collective: str = "nccl"):
+        if collective not in ("nccl", "p2p"):
+            raise ValueError("collective must be 'nccl' (bucketed all-reduce) or 'p2p' (PeerExchange)")
         rank, world = world_info(group)
         super().__init__(dataset, cloud, cfg, out_dir=out_dir if rank == 0 else None,
                          verbose=verbose and rank == 0, targets_on_host=targets_on_host,
@@ -171,6 +233,8 @@ class DataParallelTrainer(Trainer):
         self.group = group
         self.bucket_bytes = bucket_bytes
         self._reducer = None
+        self.collective = collective
+        self._peer = None
 
     @property
     def t(self):  # (round-1 API: the wrapped Trainer is now the object itself)
@@ -190,6 +254,13 @@ class DataParallelTrainer(Trainer):
     def _reduce_stats(self) -> None:
         allreduce_stats(self.stats, self.group)
 
+    def _peer_for(self, gflat: torch.Tensor, n: int, nf: int) -> PeerExchange:
+        if self._peer is None or self._peer.key != (gflat.data_ptr(), gflat.numel()):
+            if self._peer is not None:
+                self._peer.release()
+            self._peer = PeerExchange(gflat, n, nf, self.group)
+        return self._peer
+
     def _apply_gradients(self) -> None:
         from .trainer import _lr_array
 
@@ -206,6 +277,14 @@ class DataParallelTrainer(Trainer):
         flag_base = sticky - 4 * nat.XG_CTR_STATUS
         lib = nat.lib()
         gflat = self.eng.grads.flat
+        if self.collective == "p2p":
+            # reduce-scatter + all-gather with Adam as its epilogue, over peer
+            # memory (PeerExchange); the global non-finite bits land in sticky
+            self._peer_for(gflat, n, nf).step(cloud.flat, self.state.m_flat, self.state.v_flat, lr, cfg.beta1,
+                                              cfg.beta2, cfg.eps, bc1, bc2, sticky)
+            nat.check(lib.xg_adam_renorm(cloud.flat.data_ptr(), n, nf, sticky, nat.stream()), "xg_adam_renorm")
+            cloud.mark_mutated()
+            return
         ends = _field_ends(n, nf)
         done = [0]
 

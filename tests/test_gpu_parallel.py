@@ -8,7 +8,9 @@ the NCCL node; the kernels, buckets and Adam epilogues are the product's).
 * after 30 DP steps spanning density-control events (the stats summed over
   ranks, split normals from the same PCG64 stream on both ranks) the two
   replicas hold bit-identical clouds and Adam moments;
-* gamma > 0 (L1 + SSIM) and opacity resets run through the same DP step.
+* gamma > 0 (L1 + SSIM) and opacity resets run through the same DP step;
+* the peer-memory exchange (collective="p2p", csrc/xg_dp.cu) gives the same
+  bit-identical replicas as the bucketed all-reduce.
 """
 
 from __future__ import annotations
@@ -169,7 +171,7 @@ def test_allreduced_gradient_is_sum_of_view_gradients():
         off += n * wdt
 
 
-def _replica_body(rank, world, gamma=0.0, reset=0):
+def _replica_body(rank, world, gamma=0.0, reset=0, collective="nccl", reproducible=False):
     import torch
 
     import paper_2403_04116_b200 as xg
@@ -180,7 +182,8 @@ def _replica_body(rank, world, gamma=0.0, reset=0):
     cfg = xg.trainer.TrainConfig(iterations=30, gamma=gamma, densify_from_iter=5, densify_interval=10,
                                  densify_until_iter=30, densify_grad_threshold=1e-9, log_interval=10,
                                  eval_interval=10**6, opacity_reset_interval=reset)
-    dp = DataParallelTrainer(ds, xg.GaussianCloud(**start, device="cuda"), cfg, bucket_bytes=4 * 37)
+    dp = DataParallelTrainer(ds, xg.GaussianCloud(**start, device="cuda"), cfg, bucket_bytes=4 * 37,
+                             collective=collective, reproducible=reproducible)
     for _ in range(30):
         dp.step()
     torch.cuda.synchronize()
@@ -197,6 +200,25 @@ def test_replicas_bit_identical_across_densify():
         assert np.array_equal(a[k], b[k]), k
     # each rank logs its own view's loss: the two ranks trained on different views
     assert a["loss"] != b["loss"]
+
+
+def _peer_body(rank, world):
+    # (reproducible backward: the two runs' per-view gradients are then
+    # bit-identical, so the two collectives see the same operands)
+    return {c: _replica_body(rank, world, collective=c, reproducible=True) for c in ("nccl", "p2p")}
+
+
+def test_peer_exchange_matches_allreduce_path():
+    """The peer-memory step (PeerExchange: IPC-mapped buffers, reduce-scatter
+    + all-gather-Adam kernels with device-side epoch waits) across density
+    control: replicas bit-identical, and equal to the bucketed all-reduce
+    path (at world 2 both add the same two gradients)."""
+    out = spawn(_peer_body)
+    a, b = out[0], out[1]
+    assert a["p2p"]["events"] == a["nccl"]["events"] >= 2 and a["p2p"]["n"] == a["nccl"]["n"]
+    for k in ("flat", "m", "v"):
+        assert np.array_equal(a["p2p"][k], b["p2p"][k]), k
+        assert np.array_equal(a["p2p"][k], a["nccl"][k]), k
 
 
 def _replica_ssim_reset_body(rank, world):

@@ -34,6 +34,10 @@ from pathlib import Path
 
 import numpy as np
 
+# (before CUDA initialises: 32 hardware work queues for the sweep's ~14
+# streams - the package sets the same default on import)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 

@@ -9,6 +9,16 @@ hand-written sm_100a CUDA kernels behind the C ABI of ``include/xgauss.h``
 (``phantom``, ``dataset``).  There is no CPU fallback.
 """
 
+import os as _os
+
+# The sweep renderer keeps ~14 streams busy (12 binning streams, compositing,
+# image downloads); with CUDA's default 8 hardware work queues some of them
+# share a queue and serialise (a download then holds up a binning chain).
+# 32 queues: C3 sweep +1.5 % device-resident and end to end (measured,
+# DESIGN.md).  Read when the CUDA context is created, so it only applies if
+# the package is imported before CUDA is initialised; an explicit setting wins.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .acui import CuboidSpec, init_alternative, init_cloud, sample_cuboid
 from .dataset import ProjectionSet, add_noise, load_dataset, make_projection_set, save_dataset
 from .errors import (

@@ -133,7 +133,9 @@ class SweepRenderer:
                     composite_events.append((a, b, 1))
                 else:
                     fr.composite(image_out=out[i], track=False)
-                status[i : i + 1].copy_(fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
+                # (a kernel, not copy_: a 4-byte cudaMemcpy would queue on the copy
+                # engine behind the previous view's image download)
+                torch.add(fr.counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1], 0, out=status[i : i + 1])
             if host_out is not None:
                 self.copy_stream.wait_stream(st)
                 with torch.cuda.stream(self.copy_stream):
@@ -174,8 +176,11 @@ class SweepRenderer:
                 if b is not None:
                     b.record(cs)
                     composite_events.append((a, b, nv))
-                for i in range(nv):
-                    status[lo + i : lo + i + 1].copy_(fs[i].counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1])
+                # the views' status words in one cat kernel (a 4-byte cudaMemcpy per
+                # view would queue on the copy engine behind the image downloads
+                # and hold up this stream's next compositing launch)
+                torch.cat([fs[i].counters[nat.XG_CTR_STATUS : nat.XG_CTR_STATUS + 1] for i in range(nv)],
+                          out=status[lo:hi])
                 ev = torch.cuda.Event()
                 ev.record(cs)
                 done[j % 2] = ev

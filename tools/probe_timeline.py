@@ -24,6 +24,9 @@ out = r.render(angles)
 torch.cuda.synchronize()
 inten, inv = nat.intensities(cloud), nat.view_invariants(cloud)
 lib = nat.lib()
+D2H = len(sys.argv) > 1 and sys.argv[1] == "d2h"  # each batch's images to pinned host memory (copy stream)
+host = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+cps = torch.cuda.Stream()
 
 
 def E():
@@ -68,9 +71,15 @@ for rep in range(2):
             ev = torch.cuda.Event()
             ev.record(cs)
             done[j % 2] = ev
+        if D2H:
+            cps.wait_event(ev)
+            with torch.cuda.stream(cps):
+                host[lo:hi].copy_(out[lo:hi], non_blocking=True)
         rec.append((bins, (a, b)))
-    for s in r.streams + [cs]:
+    for s in r.streams + [cs, cps]:
         main.wait_stream(s)
+    te = E()
+    te.record(main)
     torch.cuda.synchronize()
     if rep == 0:
         continue
@@ -79,4 +88,7 @@ for rep in range(2):
         be = [t0.elapsed_time(y) for _, y in bins]
         print(f"batch {j:2d}: bin {min(bs):7.3f} .. {max(be):7.3f} (first view done {min(be):7.3f}) | "
               f"comp {t0.elapsed_time(a):7.3f} .. {t0.elapsed_time(b):7.3f} ({a.elapsed_time(b):.3f})")
-    print(f"total {t0.elapsed_time(rec[-1][1][1]):.3f} ms for {len(angles)} views")
+    print(f"total {t0.elapsed_time(rec[-1][1][1]):.3f} ms for {len(angles)} views (end incl. copies {t0.elapsed_time(te):.3f})")
+    print("mean composite ms", sum(a.elapsed_time(b) for _, (a, b) in rec) / len(rec))
+    gaps = [rec[j][1][1].elapsed_time(rec[j + 1][1][0]) for j in range(len(rec) - 1)]
+    print("mean gap between compositing launches ms", sum(gaps) / len(gaps))

@@ -264,3 +264,31 @@ def test_sharded_sweep_gathers_the_single_process_stack():
     angles = np.linspace(0.0, np.pi, 29, endpoint=False)
     ref = SweepRenderer(cloud, sc, batch=4).render(angles).cpu().numpy()
     assert out[0].shape == ref.shape and np.array_equal(out[0], ref)
+
+
+def test_peer_exchange_single_process_equals_trainer():
+    """world = 1 (no process group): the peer-exchange kernels with one rank
+    apply exactly the single-GPU Trainer's Adam (reproducible backward, so
+    both see the same gradients) - 20 steps including a density event."""
+    import torch
+
+    import paper_2403_04116_b200 as xg
+    from paper_2403_04116_b200.parallel import DataParallelTrainer
+
+    torch.cuda.set_device(0)
+    truth, start, sc = _scene()
+    ds = _dataset(truth, sc)
+
+    def cfg():
+        return xg.trainer.TrainConfig(iterations=20, densify_from_iter=5, densify_interval=10, densify_until_iter=20,
+                                      densify_grad_threshold=1e-9, log_interval=10**6, eval_interval=10**6)
+
+    a = xg.trainer.Trainer(ds, xg.GaussianCloud(**start, device="cuda"), cfg(), reproducible=True)
+    b = DataParallelTrainer(ds, xg.GaussianCloud(**start, device="cuda"), cfg(), reproducible=True, collective="p2p")
+    for _ in range(20):
+        a.step()
+        b.step()
+    torch.cuda.synchronize()
+    assert a.densify_events == b.densify_events >= 1
+    for x, y in ((a.cloud.flat, b.cloud.flat), (a.state.m_flat, b.state.m_flat), (a.state.v_flat, b.state.v_flat)):
+        assert torch.equal(x, y)

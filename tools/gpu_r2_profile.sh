@@ -11,10 +11,10 @@ python tools/launch_summary.py gpurun_out/r02_launches_train_c2.csv 200 > gpurun
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_composite_fwd_batch -s 2 -c 1 \
     -o gpurun_out/r02_ncu_fwd_batch python tools/prof_batch.py 3 > /dev/null 2>&1; echo "rc=$?"
 python tools/ncu_summary.py gpurun_out/r02_ncu_fwd_batch.ncu-rep > gpurun_out/r02_ncu_fwd_batch.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_composite_bwd_ck -s 5 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_composite_bwd_ck -s 2 -c 1 \
     -o gpurun_out/r02_ncu_bwd_train python tools/probe_train.py 8 88 1000 > /dev/null 2>&1; echo "rc=$?"
 python tools/ncu_summary.py gpurun_out/r02_ncu_bwd_train.ncu-rep > gpurun_out/r02_ncu_bwd_train.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_composite_fwd_np -s 5 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_composite_fwd_np -s 2 -c 1 \
     -o gpurun_out/r02_ncu_fwdtrain python tools/probe_train.py 8 88 1000 > /dev/null 2>&1; echo "rc=$?"
 python tools/ncu_summary.py gpurun_out/r02_ncu_fwdtrain.ncu-rep > gpurun_out/r02_ncu_fwdtrain.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bin_emit -c 1 \

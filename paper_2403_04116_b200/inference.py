@@ -150,6 +150,7 @@ class SweepRenderer:
         for s in self.streams + [cs, self.copy_stream]:
             s.wait_stream(main)
         done = [None, None]  # composite-finished event per frame set
+        pending = None  # (lo, hi) of the last batch whose images are not downloaded yet
         lib = nat.lib()
         for j, lo in enumerate(range(0, len(angles), K)):
             hi = min(lo + K, len(angles))
@@ -167,6 +168,16 @@ class SweepRenderer:
             sps = (nat.XgSplats * nv)(*[fs[i].splats_struct() for i in range(nv)])
             imgs = (ctypes.c_void_p * nv)(*[out[lo + i].data_ptr() for i in range(nv)])
             with torch.cuda.stream(cs):
+                if host_out is not None and pending is not None:
+                    # the previous batch's download starts with this
+                    # compositing launch (not in the binning phase before it,
+                    # whose L2-resident working set the DMA would evict)
+                    started = torch.cuda.Event()
+                    started.record(cs)
+                    self.copy_stream.wait_event(started)
+                    with torch.cuda.stream(self.copy_stream):
+                        host_out[pending[0]:pending[1]].copy_(out[pending[0]:pending[1]], non_blocking=True)
+                    pending = None
                 a = b = None
                 if composite_events is not None:
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -185,9 +196,11 @@ class SweepRenderer:
                 ev.record(cs)
                 done[j % 2] = ev
             if host_out is not None:
-                self.copy_stream.wait_event(ev)
-                with torch.cuda.stream(self.copy_stream):
-                    host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
+                pending = (lo, hi)  # downloaded once the next launch starts (or after the loop)
+        if host_out is not None and pending is not None:
+            self.copy_stream.wait_stream(cs)
+            with torch.cuda.stream(self.copy_stream):
+                host_out[pending[0]:pending[1]].copy_(out[pending[0]:pending[1]], non_blocking=True)
         for s in self.streams + [cs, self.copy_stream]:
             main.wait_stream(s)
         self.kernel_launches = (len(angles) + K - 1) // K

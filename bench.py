@@ -503,13 +503,23 @@ def run_ours(args) -> None:
     from paper_2403_04116_b200.rasterizer import render_view
 
     rv_angles = angles[:: max(1, nloc // 36)]
-    img_host = torch.empty((DET, DET), dtype=torch.float32, pin_memory=True)
+    # (views round-robin over streams: render_view's entry-count sync waits
+    # for its own view's binning only; each image lands in its stream's
+    # pinned buffer)
+    rv_streams = [torch.cuda.Stream() for _ in range(RV_STREAMS)]
+    img_host = [torch.empty((DET, DET), dtype=torch.float32, pin_memory=True) for _ in rv_streams]
 
     def rv_step():
+        main = torch.cuda.current_stream()
         cloud.flat.copy_(cloud_host, non_blocking=True)
-        for a in rv_angles:
-            proj, _ = render_view(cloud, sc, float(a))
-            img_host.copy_(proj.pixels)
+        for st in rv_streams:
+            st.wait_stream(main)
+        for i, a in enumerate(rv_angles):
+            with torch.cuda.stream(rv_streams[i % RV_STREAMS]):
+                proj, _ = render_view(cloud, sc, float(a))
+                img_host[i % RV_STREAMS].copy_(proj.pixels, non_blocking=True)
+        for st in rv_streams:
+            main.wait_stream(st)
 
     rv_step()
     ms_rv = timed(rv_step, 2)
@@ -554,7 +564,8 @@ def run_ours(args) -> None:
                 "render_view_loop": {"value": rv_value, "unit": "fps", "views_per_step": len(rv_angles),
                                      "note": "the drop-in call per view: render_view(cloud, scanner, phi) (one "
                                              "host sync for the entry count, fresh Frame and SplatList), each "
-                                             "image copied to pinned host memory, the cloud re-uploaded per step"}},
+                                             "image copied to pinned host memory, the cloud re-uploaded per step; "
+                                             f"views round-robin over {RV_STREAMS} streams"}},
         "roofline": {"bound": "fp32", "kernel": "k_composite_fwd_batch" if args.batch > 1 else "k_composite_fwd",
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak,
@@ -753,6 +764,7 @@ def safe(fn) -> dict:
 
 
 VIEWS_C1 = 16
+RV_STREAMS = int(os.environ.get("XG_RV_STREAMS", "4"))  # C3 render_view loop: views in flight
 
 
 def c1_block(args, timed, clock_cls, local, world: int, rank: int) -> dict:
@@ -780,7 +792,7 @@ def c1_block(args, timed, clock_cls, local, world: int, rank: int) -> dict:
     cams = [geometry.camera_pod(geometry.extrinsic_from_angle(sc, a), intr, (d, d)) for a in angles]
     dl_host = torch.as_tensor(np.random.default_rng(0).normal(size=(d, d)) / (d * d), dtype=torch.float32).pin_memory()
     dl = dl_host.cuda()
-    n_streams = int(os.environ.get("XG_C1_STREAMS", "4"))  # independent views in flight (their kernels overlap on the 148 SMs)
+    n_streams = int(os.environ.get("XG_C1_STREAMS", "8"))  # independent views in flight (their kernels overlap on the 148 SMs)
     engs = [_IterationEngine(cloud, d, d) for _ in range(n_streams)]
     streams = [torch.cuda.Stream() for _ in range(n_streams)]
     eng = engs[0]
@@ -809,14 +821,35 @@ def c1_block(args, timed, clock_cls, local, world: int, rank: int) -> dict:
         f.backward(cloud, e.acc, e.grads.flat, e.grads.screen_norms, e.vis, dl_dimage=dl,
                    events=ev["bwd"] if rec else None)
 
+    wave = os.environ.get("XG_C1_WAVE", "1") == "1"
+
     def step():
         # views round-robin over the streams (each its own buffers)
         main = torch.cuda.current_stream()
         for st in streams:
             st.wait_stream(main)
-        for i, cam in enumerate(cams):
-            with torch.cuda.stream(streams[i % n_streams]):
-                one(engs[i % n_streams], cam, False)
+        if wave:
+            # waves of n_streams views: every view's binning and forward are
+            # queued before the host waits for the first entry count
+            for w0 in range(0, len(cams), n_streams):
+                grp = list(range(w0, min(w0 + n_streams, len(cams))))
+                for i in grp:
+                    with torch.cuda.stream(streams[i % n_streams]):
+                        f = engs[i % n_streams].frame
+                        f.preprocess(cloud, cams[i])
+                        f.bin_async()
+                        f.composite(train=True)
+                for i in grp:
+                    with torch.cuda.stream(streams[i % n_streams]):
+                        e = engs[i % n_streams]
+                        f = e.frame
+                        if f.finish_bin():
+                            f.composite(train=True)
+                        f.backward(cloud, e.acc, e.grads.flat, e.grads.screen_norms, e.vis, dl_dimage=dl)
+        else:
+            for i, cam in enumerate(cams):
+                with torch.cuda.stream(streams[i % n_streams]):
+                    one(engs[i % n_streams], cam, False)
         for st in streams:
             main.wait_stream(st)
 
@@ -833,14 +866,23 @@ def c1_block(args, timed, clock_cls, local, world: int, rank: int) -> dict:
     ms_serial = timed(serial_step, args.steps)  # one view at a time: the per-unit latency, kernel events
     with clock_cls(local) as clk:
         ms = timed(step, args.steps)
-    grads_host = torch.empty(eng.grads.flat.numel(), dtype=torch.float32).pin_memory()
+    grads_host = [torch.empty(eng.grads.flat.numel(), dtype=torch.float32).pin_memory() for _ in streams]
 
     def e2e_step():
-        for a in angles:
-            ext = geometry.extrinsic_from_angle(sc, a)
-            _, sp = render(cloud, ext, intr, (d, d))
-            g = render_backward(cloud, sp, dl_host.to("cuda", non_blocking=True))
-            grads_host.copy_(g.flat, non_blocking=True)
+        # the public calls, views round-robin over the streams: render()'s
+        # entry-count sync waits for its own view's binning only, not for the
+        # previous view's backward
+        main = torch.cuda.current_stream()
+        for st in streams:
+            st.wait_stream(main)
+        for i, a in enumerate(angles):
+            with torch.cuda.stream(streams[i % n_streams]):
+                ext = geometry.extrinsic_from_angle(sc, a)
+                _, sp = render(cloud, ext, intr, (d, d))
+                g = render_backward(cloud, sp, dl_host.to("cuda", non_blocking=True))
+                grads_host[i % n_streams].copy_(g.flat, non_blocking=True)
+        for st in streams:
+            main.wait_stream(st)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -857,13 +899,14 @@ def c1_block(args, timed, clock_cls, local, world: int, rank: int) -> dict:
     blk = {"metric": "fwd+bwd/s (256x256 view, 50k Gaussians)", "value": units / (ms / 1e3), "unit": "fwd+bwd/s",
            "ms_per_unit": ms / (VIEWS_C1 * args.steps),
            "latency_ms_single_view": ms_unit,
-           "concurrency": f"{n_streams} views in flight on {n_streams} streams (own buffers each); "
+           "concurrency": f"{n_streams} views in flight on {n_streams} streams (own buffers each), issued in "
+                          "waves (every view's binning + forward queued before the host reads an entry count); "
                           "latency_ms_single_view: one view at a time",
            "e2e": {"value": units / (ms_e2e / 1e3), "unit": "fwd+bwd/s", "h2d_bytes_per_step": 4 * d * d * VIEWS_C1,
                    "d2h_bytes_per_step": 4 * eng.grads.flat.numel() * VIEWS_C1,
                    "note": "public API per view: render() (one host sync for the entry count, fresh SplatList) + "
                            "render_backward() with dL/dI from pinned host memory; every gradient field copied "
-                           "to pinned host memory"},
+                           f"to pinned host memory; views round-robin over {n_streams} streams"},
            "traversed_pairs_per_view": ppv, "entries_per_view": float(np.mean(entries)),
            "kernel_ms": {"composite_fwd_train": fwd_ms, "composite_bwd": bwd_ms},
            "roofline": {"bound": "fp32", "kernel": "k_composite_bwd_ck", "achieved": achieved, "peak": peak,

@@ -1207,12 +1207,13 @@ __device__ __forceinline__ void unblend2(const BRec& r, float2 dy, float bdx, fl
 }
 
 // The lane's 2 kP pixels (kP vertically adjacent pairs of one column,
-// sharing dx and the dx-only terms) for one splat; the lane's 7 partial sums
-// (negated: the caller negates the warp totals, which is exact).
+// sharing dx and the dx-only terms) for one splat; the lane's 4 column
+// partial sums {G, G dy, G dy^2, g w} and dx (negated: the caller negates the
+// warp totals, which is exact).
 template <bool kGeneral, int kP>
 __device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx, const float2 (&fy)[kP],
                                               const int (&last)[2 * kP], const float2 (&g)[kP], float2 (&T)[kP],
-                                              float2 (&nS)[kP], float* v) {
+                                              float2 (&nS)[kP], float* v, float& dxo) {
   const float dx = __fsub_rn(fx, r.a.x);
   const float adx2 = __fmul_rn(__fmul_rn(r.a.z, dx), dx);
   const float bdx = __fmul_rn(r.a.w, dx);
@@ -1236,16 +1237,12 @@ __device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx,
       sgw = __ffma2_rn(g[i], nw, sgw);
     }
   }
-  const float Gs = sG.x + sG.y, Gdys = sGdy.x + sGdy.y;
-  v[0] = Gs * dx;
-  v[1] = Gdys;
-  v[2] = v[0] * dx;
-  v[3] = Gdys * dx;
-  v[4] = sGdy2.x + sGdy2.y;
-  v[5] = sgw.x + sgw.y;
-  v[6] = Gs;
-  v[7] = 0.f;
-  return (Gs != 0.f) | (v[5] != 0.f);
+  v[0] = sG.x + sG.y;
+  v[1] = sGdy.x + sGdy.y;
+  v[2] = sGdy2.x + sGdy2.y;
+  v[3] = sgw.x + sgw.y;
+  dxo = dx;
+  return (v[0] != 0.f) | (v[3] != 0.f);
 }
 
 // Speculative reverse step (batches of well-conditioned, alpha < 0.98999
@@ -1259,7 +1256,7 @@ __device__ __forceinline__ bool unblend_splat(const BRec& r, int krel, float fx,
 template <int kP>
 __device__ __forceinline__ bool unblend_splat_spec(const BRec& r, float fx, const float2 (&fy)[kP],
                                                    const float2 (&g)[kP], float2 (&T)[kP], float2 (&nS)[kP],
-                                                   float* v) {
+                                                   float* v, float& dxo) {
   const float dx = __fsub_rn(fx, r.a.x);
   const float adx2 = __fmaf_rn(__fmul_rn(r.a.z, dx), dx, r.b.w);
   const float bdx = __fmul_rn(r.a.w, dx);
@@ -1290,58 +1287,69 @@ __device__ __forceinline__ bool unblend_splat_spec(const BRec& r, float fx, cons
       sgw = __ffma2_rn(g[i], nw, sgw);
     }
   }
-  const float Gs = sG.x + sG.y, Gdys = sGdy.x + sGdy.y;
-  v[0] = Gs * dx;
-  v[1] = Gdys;
-  v[2] = v[0] * dx;
-  v[3] = Gdys * dx;
-  v[4] = sGdy2.x + sGdy2.y;
-  v[5] = sgw.x + sgw.y;
-  v[6] = Gs;
-  v[7] = 0.f;
-  return (Gs != 0.f) | (v[5] != 0.f);
+  v[0] = sG.x + sG.y;
+  v[1] = sGdy.x + sGdy.y;
+  v[2] = sGdy2.x + sGdy2.y;
+  v[3] = sgw.x + sgw.y;
+  dxo = dx;
+  return (v[0] != 0.f) | (v[3] != 0.f);
 }
 
-// Sum 16 per-lane values over the warp (two splats' 8-value records); lane l
-// ends with the total of value index (l >> 1) & 15 (transpose-reduce: 16
-// shuffles for 16 values).
-__device__ __forceinline__ float warp_reduce16(float (&v)[16]) {
+// Sum two splats' records over the warp.  v[0..3] / v[4..7]: the lane's
+// column partials {G, G dy, G dy^2, g w} of splat A / B, dxA / dxB its column
+// offsets.  Lanes l and l ^ 16 share a column (make_unit, make_sub), so the
+// first transpose step adds the column's two row groups (lanes < 16 keep A,
+// the others B); each lane then expands its splat's column sums with its dx
+// into the 8-value record {G dx, G dy, G dx^2, G dx dy, G dy^2, g w, G, 0}
+// and the 16-lane transpose-reduce finishes it: lane l ends with the total
+// of value (l >> 1) & 7 of splat l >> 4 (12 shuffles for two splats instead
+// of 16 with the dx products formed before the reduction).
+__device__ __forceinline__ float warp_reduce_cols(float (&v)[8], float dxA, float dxB) {
   const int lane = threadIdx.x & 31;
-  {
-    const bool up = lane & 16;
+  const bool up16 = lane & 16;
+  float c[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float send = up ? v[i] : v[i + 8];
-      const float keep = up ? v[i + 8] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
+  for (int i = 0; i < 4; ++i) {
+    const float send = up16 ? v[i] : v[i + 4];
+    const float keep = up16 ? v[i + 4] : v[i];
+    c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
+  const float dx = up16 ? dxB : dxA;
+  float w[8];
+  w[0] = c[0] * dx;
+  w[1] = c[1];
+  w[2] = w[0] * dx;
+  w[3] = c[1] * dx;
+  w[4] = c[2];
+  w[5] = c[3];
+  w[6] = c[0];
+  w[7] = 0.f;
   {
     const bool up = lane & 8;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float send = up ? v[i] : v[i + 4];
-      const float keep = up ? v[i + 4] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      const float send = up ? w[i] : w[i + 4];
+      const float keep = up ? w[i + 4] : w[i];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
   }
   {
     const bool up = lane & 4;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const float send = up ? v[i] : v[i + 2];
-      const float keep = up ? v[i + 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      const float send = up ? w[i] : w[i + 2];
+      const float keep = up ? w[i + 2] : w[i];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
   }
   {
     const bool up = lane & 2;
-    const float send = up ? v[0] : v[1];
-    const float keep = up ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    const float send = up ? w[0] : w[1];
+    const float keep = up ? w[1] : w[0];
+    w[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
   }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  return v[0];
+  w[0] += __shfl_xor_sync(0xffffffffu, w[0], 1);
+  return w[0];
 }
 
 template <bool kRepro = false>
@@ -1382,9 +1390,9 @@ __device__ __forceinline__ int compact_bwd(const Raw& raw, int krel, const Unit&
 template <int kMode, int kP>
 __device__ __forceinline__ bool unblend_any(const BRec& r, int krel, float fx, const float2 (&fy)[kP],
                                             const int (&last)[2 * kP], const float2 (&g)[kP], float2 (&T)[kP],
-                                            float2 (&nS)[kP], float* v) {
-  if (kMode == 2) return unblend_splat_spec<kP>(r, fx, fy, g, T, nS, v);
-  return unblend_splat<kMode == 1, kP>(r, krel, fx, fy, last, g, T, nS, v);
+                                            float2 (&nS)[kP], float* v, float& dx) {
+  if (kMode == 2) return unblend_splat_spec<kP>(r, fx, fy, g, T, nS, v, dx);
+  return unblend_splat<kMode == 1, kP>(r, krel, fx, fy, last, g, T, nS, v, dx);
 }
 
 template <int kMode, int kP, bool kRepro>
@@ -1397,16 +1405,16 @@ __device__ __forceinline__ void unblend_batch(const BRec* rec, const int* kk, co
   // records reduced together
   for (int q = cnt - 1; q >= 0; q -= 2) {
     const bool hasB = q >= 1;
-    float v[16];
-    bool any = unblend_any<kMode, kP>(rec[q], kk[q], fx, fy, last, g, T, nS, v);
+    float v[8], dxA, dxB = 0.f;
+    bool any = unblend_any<kMode, kP>(rec[q], kk[q], fx, fy, last, g, T, nS, v, dxA);
     if (hasB) {
-      any |= unblend_any<kMode, kP>(rec[q - 1], kk[q - 1], fx, fy, last, g, T, nS, v + 8);
+      any |= unblend_any<kMode, kP>(rec[q - 1], kk[q - 1], fx, fy, last, g, T, nS, v + 4, dxB);
     } else {
 #pragma unroll
-      for (int i = 8; i < 16; ++i) v[i] = 0.f;
+      for (int i = 4; i < 8; ++i) v[i] = 0.f;
     }
     if (!__any_sync(0xffffffffu, any)) continue;
-    const float tot = -warp_reduce16(v);
+    const float tot = -warp_reduce_cols(v, dxA, dxB);
     // value i sits in lanes 2i, 2i+1: lanes 0/8 collect A's 0-3 / 4-7,
     // lanes 16/24 collect B's
     const float t1 = __shfl_down_sync(0xffffffffu, tot, 2);

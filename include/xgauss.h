@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define XG_ABI_VERSION 4
+#define XG_ABI_VERSION 5
 
 typedef enum xg_status {
   XG_OK = 0,
@@ -246,6 +246,20 @@ xg_status xg_composite_fwd_batch(const xg_camera* cams, const xg_splats* sps, fl
 xg_status xg_composite_bwd(const xg_camera* cam, const xg_splats* sp, const float* t_final,
                            const int32_t* n_contrib, const float* dl_dimage, const float* image,
                            const float* target, float l1_scale, float* grad_acc, void* stream);
+
+/* The trainer's K3 + K4a pair (_kernels.pyx:23-74 forward, :77-178 backward
+ * with the fused L1 gradient l1_scale*sign(image-target)): the results of
+ * xg_composite_fwd_train followed by xg_composite_bwd(dl_dimage = NULL), as
+ * one stream segment in which the reverse replay starts on each tile as soon
+ * as that tile's forward is done (the forward publishes every finished
+ * tile's replay chunks to a device ring, the replay kernel - launched with
+ * programmatic dependent launch - consumes them).  Needs a training frame
+ * (replay_ckpt, replay_items, unit_cost); target and grad_acc are required,
+ * grad_acc is zeroed here.  Uses counters 5-7.  Falls back to the two calls
+ * when the build's tiling does not allow it (or XG_TRAIN_STREAM=0). */
+xg_status xg_composite_train_pair(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                                  int32_t* n_contrib, const float* target, double* l1_sum, float l1_scale,
+                                  float* grad_acc, void* stream);
 
 /* Reproducible K4a (the reference's single-threaded backward is bitwise
  * reproducible, pkg/tests/test_trainer.py:336-353): the same reverse replay,

@@ -37,7 +37,7 @@ XG_CTR_ACTIVE, XG_CTR_ENTRIES, XG_CTR_STATUS, XG_CTR_STICKY, XG_CTR_QUEUE = 0, 1
 XG_CTR_ITEMS = 6
 XG_CTR_L1 = 8  # words 8-9: the fused-L1 double, zeroed by xg_preprocess_fwd
 XG_NCOUNTERS = 10
-XG_ABI_VERSION = 4
+XG_ABI_VERSION = 5
 XG_REPLAY_CHUNK = 256
 XG_MAX_BATCH = 16
 PARAM_FIELDS = ("positions", "rotations", "log_scales", "raw_opacities", "features")
@@ -117,6 +117,10 @@ SIGNATURES = {
     "xg_composite_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "xg_composite_fwd_train": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_void_p]),
+    "xg_composite_train_pair": (
+        c_i32,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_f32, c_void_p, c_void_p],
+    ),
     "xg_composite_bwd": (
         c_i32,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_f32, c_void_p, c_void_p],

@@ -453,11 +453,231 @@ __global__ void __launch_bounds__(kBinThreads)
 }
 #endif
 
+// ---------------------------------------------------------------------------
+// Entry-balanced multisplit (T <= XG_BIN_BAL_TILES).  The Gaussian-chunked
+// kernels above give every warp 32 x rounds depth-sorted Gaussians, so one
+// warp of large splats walks thousands of entries while its neighbours walk
+// tens: on a trained C2 cloud (tiles touched p50 16, p99 868) the slowest
+// warp holds 14x the median and the count / emit launches run with half the
+// SMs idle.  Here the scan of tiles-touched in depth order (offN, the
+// entries' global offsets) cuts the E entries into C x 8 equal warp slices:
+// warp w of CTA c walks entries [c EC + w EC / 8, ...) in the same (depth,
+// rect row-major) order - so per-(CTA, warp, tile) counts still rank every
+// entry stably - whatever splats they belong to.  The owner of the slice's
+// first entry comes from a 32-ary search of offN (k_bin_count_bal, stored
+// per warp for k_bin_emit_bal).
+// ---------------------------------------------------------------------------
+#ifndef XG_BIN_BAL_TILES
+#define XG_BIN_BAL_TILES 1024
+#endif
+#ifndef XG_BIN_BAL_CTAS
+#define XG_BIN_BAL_CTAS 444
+#endif
+#ifndef XG_BIN_COUNT_MATCH
+#define XG_BIN_COUNT_MATCH 0
+#endif
+
+// entries per CTA: a multiple of 8 x 32, <= 65280 while E <= C x 65280
+__device__ __forceinline__ uint32_t bal_chunk(uint32_t E, int C) {
+  const uint32_t per = (uint32_t)(((unsigned long long)E + (unsigned long long)C - 1ull) / (unsigned long long)C);
+  return (per + 255u) & ~255u;
+}
+
+// first s in [0, n) with offN[s] > x (n if none): 32-ary warp search
+__device__ __forceinline__ long long upper_bound_warp(const uint32_t* __restrict__ offN, long long n, uint32_t x,
+                                                      int lane) {
+  long long a = 0, b = n;  // answer in [a, b]
+  while (b - a > 32) {
+    const long long step = (b - a + 31) / 32;
+    const long long p = a + (long long)lane * step;
+    const bool gt = p >= b || offN[p] > x;
+    const unsigned m = __ballot_sync(0xffffffffu, gt);
+    const int j = m ? __ffs(m) - 1 : 32;
+    if (j == 0) return a;  // (offN[a] > x)
+    const long long pj1 = a + (long long)(j - 1) * step;
+    b = j < 32 ? min(b, a + (long long)j * step) : b;
+    a = pj1 + 1;
+  }
+  const long long p = a + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, p < b && offN[p] > x);
+  return m ? a + (__ffs(m) - 1) : b;
+}
+
+// Walks entries [lo, hi) of the depth-ordered entry sequence with the warp,
+// 32 at a time, starting at depth-sorted Gaussian s_first (the owner of
+// entry lo): f(valid, tile, gaussian) per lane and window (every lane calls
+// f, so f may use warp collectives).
+template <class F>
+__device__ __forceinline__ void walk_entries(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
+                                             const ushort4* __restrict__ rect, const uint32_t* __restrict__ offN,
+                                             long long n, int ntx, uint32_t lo, uint32_t hi, long long s_first,
+                                             uint32_t* s_nz, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  // software pipeline: the next round's (order, offset) one round ahead
+  long long s0 = s_first;
+  uint32_t g_n = 0xffffffffu, off_n = 0;
+  {
+    const long long s = s0 + lane;
+    if (s < n) {
+      g_n = order[s];
+      off_n = offN[s];
+    }
+  }
+  while (lo < hi && s0 < n) {
+    const uint32_t g = g_n, off = off_n;
+    uint32_t cnt = 0;
+    uint2 rr = make_uint2(0u, 0u);
+    if (g != 0xffffffffu) {
+      cnt = n_tiles[g];
+      if (cnt) rr = reinterpret_cast<const uint2*>(rect)[g];
+    }
+    {
+      const long long s = s0 + 32 + lane;
+      g_n = 0xffffffffu;
+      if (s < n) {
+        g_n = order[s];
+        off_n = offN[s];
+      }
+    }
+    const uint32_t base = __shfl_sync(0xffffffffu, off, 0);
+    if (base >= hi) break;
+    const uint32_t excl = off - base;
+    // the round's entry count (lanes past n carry stale offsets: only lanes with entries count)
+    const uint32_t incl_last = __reduce_max_sync(0xffffffffu, cnt > 0 ? excl + cnt : 0u);
+    const uint32_t rs = lo - base;  // (base <= lo: base is the owner's or the previous round's end)
+    const uint32_t re = min(hi - base, incl_last);
+    const int x0 = (int)(rr.x & 0xffffu), y0 = (int)(rr.x >> 16), x1 = (int)(rr.y & 0xffffu);
+    const int wdt = cnt ? x1 - x0 + 1 : 1;
+    const uint32_t mdiv =
+        wdt > 1 ? (uint32_t)((0x100000000ull + (unsigned long long)wdt - 1ull) / (unsigned long long)wdt) : 0u;
+    const unsigned nzm = __ballot_sync(0xffffffffu, cnt > 0);
+    if (cnt > 0) s_nz[__popc(nzm & lt)] = (uint32_t)lane;
+    __syncwarp();
+    uint32_t before = __popc(__ballot_sync(0xffffffffu, cnt > 0 && excl < rs));  // starts before the first window
+    for (uint32_t e0 = rs; e0 < re; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const uint32_t bit = (cnt > 0 && excl >= e0 && excl - e0 < 32u) ? 1u << (excl - e0) : 0u;
+      const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+      const uint32_t R = before + __popc(starts & (0xffffffffu >> (31 - lane)));  // starts <= e (>= 1)
+      before += __popc(starts);
+      const int ol = (int)s_nz[R - 1u];
+      const uint32_t j = e - __shfl_sync(0xffffffffu, excl, ol);
+      const int ow = __shfl_sync(0xffffffffu, wdt, ol);
+      const uint32_t om = __shfl_sync(0xffffffffu, mdiv, ol);
+      const int ox = __shfl_sync(0xffffffffu, x0, ol);
+      const int oy = __shfl_sync(0xffffffffu, y0, ol);
+      const uint32_t og = __shfl_sync(0xffffffffu, g, ol);
+      const bool valid = e < re;
+      const uint32_t jq = om ? __umulhi(j, om) : j;
+      const int t = valid ? (oy + (int)jq) * ntx + ox + (int)(j - jq * (uint32_t)ow) : -1;
+      f(valid, t, og);
+    }
+    __syncwarp();  // (s_nz is rewritten by the next round)
+    lo = base + incl_last;
+    s0 += 32;
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads)
+    k_bin_count_bal(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
+                    const ushort4* __restrict__ rect, const uint32_t* __restrict__ offN, long long n, int ntx, int T,
+                    const uint32_t* __restrict__ n_entries, uint32_t* __restrict__ hist,
+                    uint32_t* __restrict__ wc_out, uint32_t* __restrict__ wstart) {
+  extern __shared__ uint32_t wcnt[];  // [kBinWarps][TW]
+  __shared__ uint32_t s_nz[kBinWarps][32];
+  const int TW = (T + 1) >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kBinWarps * TW; i += kBinThreads) wcnt[i] = 0;
+  const int C = gridDim.x;
+  const uint32_t E = *n_entries, EC = bal_chunk(E, C), EW = EC / kBinWarps;
+  const unsigned long long lo64 = (unsigned long long)blockIdx.x * EC + (unsigned long long)warp * EW;
+  const uint32_t lo = (uint32_t)min(lo64, (unsigned long long)E), hi = (uint32_t)min(lo64 + EW, (unsigned long long)E);
+  long long s_first = n;
+  if (lo < hi) s_first = upper_bound_warp(offN, n, lo, lane) - 1;
+  if (lane == 0) wstart[blockIdx.x * kBinWarps + warp] = (uint32_t)s_first;
+  __syncthreads();
+  uint32_t* mine = wcnt + warp * TW;
+  walk_entries(order, n_tiles, rect, offN, n, ntx, lo, hi, s_first, s_nz[warp], [&](bool valid, int t, uint32_t) {
+#if XG_BIN_COUNT_MATCH
+    const unsigned peers = __match_any_sync(0xffffffffu, t);
+    if (valid && (peers >> lane) == 1u) atomicAdd(&mine[t >> 1], (uint32_t)__popc(peers) << ((t & 1) << 4));
+#else
+    // (a window's entries mostly hit distinct tiles - one splat's rect row -
+    // so plain shared atomics beat aggregating peers first)
+    if (valid) atomicAdd(&mine[t >> 1], 1u << ((t & 1) << 4));
+#endif
+  });
+  __syncthreads();
+  uint32_t* out = wc_out + (long long)blockIdx.x * kBinWarps * TW;
+  for (int k = threadIdx.x; k < TW; k += kBinThreads) {
+    uint32_t s0 = 0, s1 = 0;
+#pragma unroll
+    for (int w = 0; w < kBinWarps; ++w) {
+      const uint32_t c = wcnt[w * TW + k];
+      out[w * TW + k] = c;
+      s0 += c & 0xffffu;
+      s1 += c >> 16;
+    }
+    hist[(long long)(2 * k) * C + blockIdx.x] = s0;
+    if (2 * k + 1 < T) hist[(long long)(2 * k + 1) * C + blockIdx.x] = s1;
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads)
+    k_bin_emit_bal(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
+                   const ushort4* __restrict__ rect, const uint32_t* __restrict__ offN, long long n, int ntx, int T,
+                   const uint32_t* __restrict__ n_entries, const uint32_t* __restrict__ offs,
+                   const uint32_t* __restrict__ wc_in, const uint32_t* __restrict__ wstart, long long cap,
+                   uint32_t* __restrict__ entry_splat) {
+  extern __shared__ uint32_t smem_bin[];
+  __shared__ uint32_t s_nz[kBinWarps][32];
+  const int TW = (T + 1) >> 1;
+  uint32_t* tbase = smem_bin;
+  uint32_t* wcnt = smem_bin + T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = gridDim.x;
+  const uint32_t* wc = wc_in + (long long)blockIdx.x * kBinWarps * TW;
+  for (int i = threadIdx.x; i < kBinWarps * TW; i += kBinThreads) wcnt[i] = wc[i];
+  __syncthreads();
+  for (int k = threadIdx.x; k < TW; k += kBinThreads) {
+    const int t0 = 2 * k, t1 = 2 * k + 1;
+    tbase[t0] = offs[(long long)t0 * C + blockIdx.x];
+    if (t1 < T) tbase[t1] = offs[(long long)t1 * C + blockIdx.x];
+    uint32_t l0 = 0, l1 = 0;
+    for (int w = 0; w < kBinWarps; ++w) {
+      const uint32_t c = wcnt[w * TW + k];
+      wcnt[w * TW + k] = l0 | (l1 << 16);
+      l0 += c & 0xffffu;
+      l1 += c >> 16;
+    }
+  }
+  __syncthreads();
+  const uint32_t E = *n_entries, EC = bal_chunk(E, C), EW = EC / kBinWarps;
+  const unsigned long long lo64 = (unsigned long long)blockIdx.x * EC + (unsigned long long)warp * EW;
+  const uint32_t lo = (uint32_t)min(lo64, (unsigned long long)E), hi = (uint32_t)min(lo64 + EW, (unsigned long long)E);
+  uint16_t* mine16 = reinterpret_cast<uint16_t*>(wcnt + warp * TW);
+  const unsigned lt = lanemask_lt();
+  const long long s_first = lo < hi ? (long long)wstart[blockIdx.x * kBinWarps + warp] : n;
+  walk_entries(order, n_tiles, rect, offN, n, ntx, lo, hi, s_first, s_nz[warp], [&](bool valid, int t, uint32_t og) {
+    const unsigned peers = __match_any_sync(0xffffffffu, t);
+    const uint32_t loc = valid ? (uint32_t)mine16[t] : 0u;
+    if (valid) {
+      const long long pos = (long long)tbase[t] + loc + __popc(peers & lt);
+      if (pos < cap) entry_splat[pos] = og;
+    }
+    __syncwarp();
+    if (valid && (peers >> lane) == 1u) mine16[t] = (uint16_t)(loc + __popc(peers));  // highest peer lane
+    __syncwarp();
+  });
+}
+
 struct BinWs {
   unsigned long long *keyN1, *keyN2;
   uint32_t *valN1, *offN, *keyE0, *keyE1, *valE1;
   uint32_t *hist, *hoff;  // multisplit path: [T][C] counts and their scan
   uint32_t* wcnt;         //   and the per-warp 16-bit counts [C][kBinWarps][ceil(T/2)]
+  uint32_t* wstart;       //   balanced path: each warp's first depth-sorted splat [C][kBinWarps]
   void* tail;
   size_t tail_bytes;
 };
@@ -471,9 +691,31 @@ bool multisplit(int n_tiles) { return n_tiles <= XG_BIN_MULTISPLIT_TILES; }
 
 int64_t bin_chunks(int64_t n, int n_tiles) { return (n + bin_chunk(n, n_tiles) - 1) / bin_chunk(n, n_tiles); }
 
-size_t bin_wcnt_bytes(int64_t n, int n_tiles) {
+// entry-balanced count / emit (XG_BIN_BALANCED=0 selects the Gaussian-chunked kernels)
+bool balanced(int n_tiles) {
+  static const int on = getenv("XG_BIN_BALANCED") ? atoi(getenv("XG_BIN_BALANCED")) : 1;
+  return on && n_tiles <= XG_BIN_BAL_TILES;
+}
+// balanced grid: XG_BIN_BAL_CTAS, more if the capacity needs it (entries per
+// CTA stay below 2^16: 16-bit local offsets)
+int64_t bal_grid(int64_t cap) {
+  const int64_t need = (cap + 65279) / 65280;
+  return need > XG_BIN_BAL_CTAS ? need : XG_BIN_BAL_CTAS;
+}
+// CTAs of the multisplit count / emit launches (the (tile, chunk) table
+// width) - workspaces are sized for either path
+int64_t ms_chunks(int64_t n, int64_t cap, int n_tiles) {
+  const int64_t a = bin_chunks(n, n_tiles);
+  if (!balanced(n_tiles)) return a;
+  const int64_t b = bal_grid(cap);
+  return a > b ? a : b;
+}
+
+size_t bin_wcnt_bytes(int64_t n, int64_t cap, int n_tiles) {
   if (!multisplit(n_tiles)) return 0;
-  return align_up(sizeof(uint32_t) * (size_t)bin_chunks(n, n_tiles) * kBinWarps * (size_t)((n_tiles + 1) / 2));
+  const int64_t C = ms_chunks(n, cap, n_tiles);
+  return align_up(sizeof(uint32_t) * (size_t)C * kBinWarps * (size_t)((n_tiles + 1) / 2)) +
+         align_up(sizeof(uint32_t) * (size_t)C * kBinWarps);  // (+ the balanced path's per-warp start splats)
 }
 
 size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
@@ -482,7 +724,8 @@ size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   if (o > a) a = o;
   const size_t bsw = bucket_sort_workspace_bytes(n);
   if (bsw > a) a = bsw;
-  size_t b = scan_workspace_bytes(multisplit(n_tiles) ? (n > n_tiles * bin_chunks(n, n_tiles) ? n : n_tiles * bin_chunks(n, n_tiles)) : n);
+  const int64_t hn = multisplit(n_tiles) ? (int64_t)n_tiles * ms_chunks(n, cap, n_tiles) : 0;
+  size_t b = scan_workspace_bytes(n > hn ? n : hn);
   return a > b ? a : b;
 }
 
@@ -491,7 +734,7 @@ bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, int n_tiles, BinWs& w
   const size_t bn = align_up(sizeof(uint32_t) * (size_t)n);
   const bool ms = multisplit(n_tiles);
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(cap > 0 ? cap : 1));
-  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles * (size_t)bin_chunks(n, n_tiles)) : 0;
+  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles * (size_t)ms_chunks(n, cap, n_tiles)) : 0;
   w.keyN1 = (unsigned long long*)p; p += 2 * bn;
   w.keyN2 = (unsigned long long*)p; p += 2 * bn;
   w.valN1 = (uint32_t*)p; p += bn;
@@ -501,7 +744,11 @@ bool carve(void* ws, size_t bytes, int64_t n, int64_t cap, int n_tiles, BinWs& w
   w.valE1 = (uint32_t*)p; p += be;
   w.hist = (uint32_t*)p; p += bh;
   w.hoff = (uint32_t*)p; p += bh;
-  w.wcnt = (uint32_t*)p; p += bin_wcnt_bytes(n, n_tiles);
+  w.wcnt = (uint32_t*)p;
+  w.wstart = ms ? (uint32_t*)(p + align_up(sizeof(uint32_t) * (size_t)ms_chunks(n, cap, n_tiles) * kBinWarps *
+                                            (size_t)((n_tiles + 1) / 2)))
+                : nullptr;
+  p += bin_wcnt_bytes(n, cap, n_tiles);
   w.tail = p;
   const size_t used = (size_t)(p - (char*)ws);
   const size_t tb = tail_bytes(n, cap, n_tiles);
@@ -521,8 +768,9 @@ size_t xg_bin_workspace_bytes(int64_t n, int64_t entry_capacity, int32_t n_tiles
   const size_t bn = align_up(sizeof(uint32_t) * (size_t)n);
   const bool ms = multisplit(n_tiles_total);
   const size_t be = ms ? 0 : align_up(sizeof(uint32_t) * (size_t)(entry_capacity > 0 ? entry_capacity : 1));
-  const size_t bh = ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)bin_chunks(n, n_tiles_total)) : 0;
-  return 6 * bn + 3 * be + 2 * bh + bin_wcnt_bytes(n, n_tiles_total) + tail_bytes(n, entry_capacity, n_tiles_total) +
+  const size_t bh =
+      ms ? align_up(sizeof(uint32_t) * (size_t)n_tiles_total * (size_t)ms_chunks(n, entry_capacity, n_tiles_total)) : 0;
+  return 6 * bn + 3 * be + 2 * bh + bin_wcnt_bytes(n, entry_capacity, n_tiles_total) + tail_bytes(n, entry_capacity, n_tiles_total) +
          256;
 }
 
@@ -566,7 +814,13 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
   if (bin_stop == 1) return XG_OK;
   if (multisplit(n_tiles)) {
     // 2-4. fused duplicate + stable tile sort + ranges
-    const int C = (int)bin_chunks(n, n_tiles);
+    // entry-balanced count / emit for training frames (those with replay
+    // checkpoints): one view at a time, so the slowest warp is the launch;
+    // sweeps keep the Gaussian-chunked kernels (fewer instructions per entry,
+    // their imbalance hidden by the views binned concurrently - measured:
+    // balanced C3 -5 %, C2 +1.6 %)
+    const bool bal = balanced(n_tiles) && sp->replay_ckpt != nullptr;
+    const int C = (int)(bal ? bal_grid(cap) : bin_chunks(n, n_tiles));
     const size_t sm_count = sizeof(uint32_t) * (size_t)kBinWarps * ((n_tiles + 1) / 2);
     const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2) +
                                                (XG_BIN_EMIT_MASKS ? (size_t)kBinWarps * (ntx + nty) : 0));
@@ -579,9 +833,28 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                            (int)(sizeof(uint32_t) * kBinWarps * (kBinMaxTiles / 2)));
       attr_set = true;
     }
-    k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                                 bin_rounds(n, n_tiles), w.hist, w.wcnt);
-    if ((st = check_launch("k_bin_count")) != XG_OK) return st;
+    if (bal) {
+      // entry offsets of the depth-sorted splats (and E) cut the entries into equal warp slices
+      if ((st = scan_u32(sp->n_tiles, sp->order, w.offN, n, nullptr, n, sp->counters + XG_CTR_ENTRIES, w.tail,
+                         w.tail_bytes, s)) != XG_OK)
+        return st;
+      static bool attr_bal = false;
+      if (!attr_bal) {
+        cudaFuncSetAttribute(k_bin_emit_bal, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(uint32_t) * (kBinMaxTiles + kBinWarps * (kBinMaxTiles / 2))));
+        cudaFuncSetAttribute(k_bin_count_bal, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(uint32_t) * kBinWarps * (kBinMaxTiles / 2)));
+        attr_bal = true;
+      }
+      k_bin_count_bal<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, w.offN, n,
+                                                       ntx, n_tiles, sp->counters + XG_CTR_ENTRIES, w.hist, w.wcnt,
+                                                       w.wstart);
+      if ((st = check_launch("k_bin_count_bal")) != XG_OK) return st;
+    } else {
+      k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
+                                                   bin_rounds(n, n_tiles), w.hist, w.wcnt);
+      if ((st = check_launch("k_bin_count")) != XG_OK) return st;
+    }
     const long long hn = (long long)n_tiles * C;
     if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
                        w.tail_bytes, s)) != XG_OK)
@@ -590,9 +863,17 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                                                       (long long*)sp->tile_ranges);
     if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
     if (bin_stop == 2) return XG_OK;
-    k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                               bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
-    if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
+    if (bal) {
+      const size_t sm_bal = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2));
+      k_bin_emit_bal<<<C, kBinThreads, sm_bal, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, w.offN, n, ntx,
+                                                    n_tiles, sp->counters + XG_CTR_ENTRIES, w.hoff, w.wcnt, w.wstart,
+                                                    cap, sp->entry_splat);
+      if ((st = check_launch("k_bin_emit_bal")) != XG_OK) return st;
+    } else {
+      k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
+                                                 bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
+      if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
+    }
     if (!sp->tile_order) return XG_OK;
     return launch_tile_order(sp->tile_ranges, n_tiles, sp->tile_order, s);
   }

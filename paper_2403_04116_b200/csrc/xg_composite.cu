@@ -31,6 +31,8 @@
 // T <- T - sigma T is a single fused multiply-add.
 #include <stdlib.h>
 
+#include <atomic>
+
 #include "xg_internal.cuh"
 #include "xg_sort.cuh"
 
@@ -232,6 +234,13 @@ struct FwdArgs {
   long long cap;              // entry capacity: an overflowed view is skipped (re-binned by the caller)
   int ntx, w, h;
   float2* ckpt;               // optional (tracking only): (T, acc) before every kCk-th entry
+  // streamed replay (xg_composite_train_pair): each finished tile publishes its
+  // reverse-replay chunks to this ring, epoch-tagged, for the concurrently
+  // running k_composite_bwd_stream
+  unsigned long long* ring;   // [ring_cap] (tile | chunk << 20 | epoch << 40), or null
+  long long ring_cap;
+  uint32_t* ring_ctr;         // counters + XG_CTR_ITEMS: [0] slots reserved, [1] tiles published
+  uint32_t epoch;             // 24 bits
 };
 
 // Checkpoint slot of entry kCk * m of the tile whose list starts at `start`:
@@ -926,9 +935,41 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack, kLite>())
   __shared__ FRec s_rec[kWarps][kRecPerWarp];
   __shared__ int s_k[kWarps][64];
   const int warp = threadIdx.x >> 5;
-  if (a.n_entries && (long long)*a.n_entries > a.cap) return;
+  // (streamed replay: the backward grid may launch once every CTA got here;
+  // it synchronises on the ring, never on this grid's completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const bool skip = a.n_entries && (long long)*a.n_entries > a.cap;
   const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
-  if (i < a.n_tiles) composite_unit<kTrack, kP, kLite>(a, a.order[i], warp % kSubs, s_rec[warp], s_k[warp]);
+  if (!skip && i < a.n_tiles) composite_unit<kTrack, kP, kLite>(a, a.order[i], warp % kSubs, s_rec[warp], s_k[warp]);
+  if (kTrack && kLite && kSubs == 4 && kWarps == 4) {  // one tile per CTA
+    if (a.ring) {
+      // publish the tile's chunks (k_replay_items' count: ceil(L / kCk), L =
+      // the longest replay of its quarters) after its pixels, checkpoints
+      // and costs are visible; an overflowed view publishes nothing
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t nch = 0;
+        const int tile = i < a.n_tiles ? a.order[i] : 0;
+        if (!skip && i < a.n_tiles) {
+          int L = 0;
+          for (int q = 0; q < 4; ++q) L = max(L, a.unit_cost[4 * tile + q]);
+          nch = (uint32_t)((L + kCk - 1) >> kCkShift);
+        }
+        if (nch) {
+          const uint32_t p = atomicAdd(&a.ring_ctr[0], nch);
+          for (uint32_t j = 0; j < nch; ++j)
+            if ((long long)(p + j) < a.ring_cap) {
+              const unsigned long long v = (unsigned long long)tile | ((unsigned long long)j << 20) |
+                                           ((unsigned long long)a.epoch << 40);
+              asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.ring + p + j), "l"(v) : "memory");
+            }
+        }
+        __threadfence();
+        atomicAdd(&a.ring_ctr[1], 1u);
+      }
+    }
+  }
 }
 
 template <bool kTrack, bool kLite = false>
@@ -1672,6 +1713,65 @@ __global__ void __launch_bounds__(kThreads, XG_BWD_CK_MIN_CTAS) k_composite_bwd_
   }
 }
 
+// Streamed replay (xg_composite_train_pair): launched behind the training
+// forward with programmatic dependent launch, so its CTAs take the SM slots
+// the forward's tail leaves idle.  Warps pop ring slots in publication order
+// (tiles whose forward has finished) and wait on the slot's epoch tag; once
+// every tile has published, slots past the reserved count end the warp.
+// Needs whole-tile chunks (kBwdPairs = 4).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct StreamArgs {
+  const unsigned long long* ring;
+  long long ring_cap;
+  uint32_t* ring_ctr;  // [0] reserved, [1] tiles published
+  uint32_t epoch;
+};
+
+template <bool kRepro>
+__global__ void __launch_bounds__(kThreads, XG_BWD_CK_MIN_CTAS) k_composite_bwd_stream(BwdArgs a, StreamArgs r) {
+  static_assert(kBwdSubs == 1, "streamed chunks are whole tiles");
+  __shared__ BRec s_rec[kWarps][32];
+  __shared__ int s_k[kWarps][32];
+  __shared__ uint32_t s_gid[kWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr unsigned long long kExit = ~0ull;
+  for (;;) {
+    unsigned long long v = 0;
+    if (lane == 0) {
+      const uint32_t k = atomicAdd(a.work, 1u);
+      for (;;) {
+        if ((long long)k < r.ring_cap) {
+          v = ld_acquire_u64(r.ring + k);
+          if ((uint32_t)(v >> 40) == r.epoch) break;
+        }
+        if (ld_acquire_u32(r.ring_ctr + 1) >= (uint32_t)a.n_tiles) {
+          const uint32_t total = *(volatile uint32_t*)r.ring_ctr;
+          if ((long long)k >= r.ring_cap || k >= total) {
+            v = kExit;
+            break;
+          }
+          continue;  // (published before the last tile's count: visible now)
+        }
+        __nanosleep(128);
+      }
+    }
+    v = __shfl_sync(0xffffffffu, v, 0);
+    if (v == kExit) break;
+    bwd_chunk<kBwdPairs, kRepro>(a, make_uint2((uint32_t)(v & 0xfffffu), (uint32_t)((v >> 20) & 0xfffffu)),
+                                 s_rec[warp], s_k[warp], s_gid[warp]);
+  }
+}
+
 // Chunk list of the checkpointed replay, one CTA: per tile (heaviest first,
 // tile_order) and sub-block, ceil(L / kCk) chunks, L = the longest replay of
 // the quarter tiles it overlaps (unit_cost, from the forward).
@@ -1952,6 +2052,78 @@ xg_status xg_composite_fwd_train(const xg_camera* cam, const xg_splats* sp, floa
     return XG_ERR_INVALID;
   }
   return composite_fwd_impl(cam, sp, image, t_final, n_contrib, target, l1_sum, stream, true);
+}
+
+// The trainer's forward + fused-L1 reverse replay as one stream segment
+// (xg_composite_fwd_train then xg_composite_bwd with dl_dimage = NULL): the
+// forward publishes each finished tile's replay chunks to a device ring and
+// the backward, launched with programmatic dependent launch, replays them
+// while the forward's heaviest tiles are still running - no k_replay_items,
+// no idle SMs in the forward's tail, no launch boundary.  Same arithmetic
+// per chunk as the sequential pair (gradients agree up to float-atomic
+// summation order, which is already run-dependent).  XG_TRAIN_STREAM=0
+// runs the sequential pair.
+xg_status xg_composite_train_pair(const xg_camera* cam, const xg_splats* sp, float* image, float* t_final,
+                                  int32_t* n_contrib, const float* target, double* l1_sum, float l1_scale,
+                                  float* grad_acc, void* stream) {
+  if (!cam || !sp || !image || !t_final || !n_contrib || !target || !grad_acc) {
+    set_error_msg("xg_composite_train_pair: invalid argument");
+    return XG_ERR_INVALID;
+  }
+  static const bool on = !(getenv("XG_TRAIN_STREAM") && atoi(getenv("XG_TRAIN_STREAM")) == 0);
+  const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
+  const bool ok = on && kBwdPairs == 4 && kFwdLitePairs == 1 && kWarps == 4 && sp->replay_ckpt &&
+                  sp->replay_items && sp->unit_cost && sp->tile_order && sp->counters && sp->entry_splat &&
+                  sp->tile_ranges && sp->mean2d && sp->coef && sp->inten &&
+                  sp->replay_slots >= xg_replay_slots(sp->entry_capacity, n_tiles);
+  if (!ok) {
+    xg_status st = xg_composite_fwd_train(cam, sp, image, t_final, n_contrib, target, l1_sum, stream);
+    if (st != XG_OK) return st;
+    return xg_composite_bwd(cam, sp, t_final, n_contrib, nullptr, image, target, l1_scale, grad_acc, stream);
+  }
+  // slot tag: 23-bit call counter with bit 23 set (a sequential-path chunk
+  // list in the same buffer never has it); the ring is cleared per call as
+  // well, so neither stale slots nor the allocation's garbage can pass as
+  // published chunks
+  static std::atomic<uint32_t> epochs{0};
+  const uint32_t epoch = ((epochs.fetch_add(1u) + 1u) & 0x7fffffu) | 0x800000u;
+  cudaStream_t s = (cudaStream_t)stream;
+  // everything the pair needs zeroed happens before the forward, so the two
+  // kernels are adjacent in the stream: queue head, ring reserved count,
+  // tiles published (counters 5-7) and the gradient accumulator
+  if (sp->n > 0) cudaMemsetAsync(grad_acc, 0, sizeof(float) * 8 * (size_t)sp->n, s);
+  cudaMemsetAsync(sp->counters + XG_CTR_QUEUE, 0, 3 * sizeof(uint32_t), s);
+  unsigned long long* ring = (unsigned long long*)sp->replay_items;
+  const long long ring_cap = 4 * (long long)sp->replay_slots;
+  cudaMemsetAsync(ring, 0, sizeof(unsigned long long) * (size_t)ring_cap, s);
+  FwdArgs a{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+            (const long long*)sp->tile_ranges, sp->tile_order, sp->counters + XG_CTR_QUEUE, n_tiles, image, t_final,
+            n_contrib, target, l1_sum, sp->unit_cost,
+            sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
+            tiles_x(*cam), cam->width, cam->height, (float2*)sp->replay_ckpt, ring, ring_cap,
+            sp->counters + XG_CTR_ITEMS, epoch};
+  k_composite_fwd_np<true, true><<<n_tiles, kThreads, 0, s>>>(a);
+  xg_status st = check_launch("k_composite_fwd_np");
+  if (st != XG_OK) return st;
+  BwdArgs b{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,
+            (const long long*)sp->tile_ranges, nullptr, sp->counters + XG_CTR_QUEUE, n_tiles, false, t_final,
+            n_contrib, nullptr, image, target, l1_scale, grad_acc,
+            sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
+            tiles_x(*cam), cam->width, cam->height, (const float2*)sp->replay_ckpt, nullptr, nullptr, nullptr,
+            nullptr, nullptr};
+  StreamArgs r{ring, ring_cap, sp->counters + XG_CTR_ITEMS, epoch};
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(persistent_grid(k_composite_bwd_stream<false>, 4 * n_tiles, "XG_BWD_CTAS_PER_SM"));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_composite_bwd_stream<false>, b, r);
+  return check_launch("k_composite_bwd_stream");
 }
 
 size_t xg_composite_batch_workspace_bytes(const xg_camera* cam, int32_t n_views) {

@@ -191,6 +191,34 @@ class Frame:
         self.has_forward = track
         self.fwd_image = img  # the image the backward (fused L1, replay restarts) reads
 
+    def train_pair(self, target: torch.Tensor, l1_sum: torch.Tensor, grad_acc: torch.Tensor, l1_scale: float,
+                   events: list | None = None) -> None:
+        """K3 + K4a of a training iteration with the fused L1 objective
+        (``xg_composite_train_pair``): the tracking forward into the frame's
+        image / t_final / n_contrib / checkpoints and the reverse replay into
+        ``grad_acc``, the replay overlapping the forward's tail.  Follow with
+        ``backward(..., replay_done=True)`` for the chain rule."""
+        if self.replay_ckpt is None:
+            self._alloc_replay()
+        sp = self.splats_struct()
+        ev = None
+        if events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+        nat.check(
+            nat.lib().xg_composite_train_pair(
+                ctypes.byref(self.cam), ctypes.byref(sp), self.image.data_ptr(), self.t_final.data_ptr(),
+                self.n_contrib.data_ptr(), nat.ptr(target, "target"), nat.ptr(l1_sum, "l1_sum"),
+                ctypes.c_float(l1_scale), grad_acc.data_ptr(), nat.stream(),
+            ),
+            "xg_composite_train_pair",
+        )
+        if ev is not None:
+            ev[1].record()
+            events.append(ev)
+        self.has_forward = True
+        self.fwd_image = self.image
+
     @property
     def l1_sum(self) -> torch.Tensor:
         """The forward's fused-L1 accumulator: a float64 view of counters
@@ -249,7 +277,7 @@ class Frame:
     def backward(self, cloud, grad_acc: torch.Tensor, grads_flat: torch.Tensor, screen_norms, visible,
                  dl_dimage: torch.Tensor | None = None, target: torch.Tensor | None = None,
                  l1_scale: float = 0.0, stats=None, kernel_grads=None, reproducible: bool = False,
-                 events: list | None = None) -> None:
+                 events: list | None = None, replay_done: bool = False) -> None:
         """K4a + K4b.  ``grad_acc`` ([N, 8] float32 scratch) is zeroed by the
         library (xg_composite_bwd) or fully written (reproducible mode).
         ``reproducible`` sums each splat's per-entry gradient
@@ -263,7 +291,9 @@ class Frame:
         args = (ctypes.byref(self.cam), ctypes.byref(sp), self.t_final.data_ptr(), self.n_contrib.data_ptr(),
                 nat.ptr(dl_dimage, "dl_dimage"), self.fwd_image.data_ptr(),
                 nat.ptr(target, "target") if dl_dimage is None else None, ctypes.c_float(l1_scale))
-        if reproducible:
+        if replay_done:  # (train_pair ran the reverse replay into grad_acc)
+            pass
+        elif reproducible:
             nb = int(nat.lib().xg_entry_grad_bytes(self.n, self.entry_capacity))
             if self.entry_grad is None or self.entry_grad.numel() < nb:
                 self.entry_grad = torch.empty(nb, dtype=torch.uint8, device=self.device)

@@ -441,17 +441,30 @@ class Trainer:
         else:
             tgt = self.targets[view]
         ke = self.kernel_events
+        # plain L1 (gamma = 0): forward and reverse replay as one overlapped
+        # pair (xg_composite_train_pair); the SSIM objective needs the whole
+        # image before its pixel gradient exists, the reproducible mode its
+        # own replay
+        pair = cfg.gamma == 0.0 and not self.reproducible
         # (the L1 accumulator lives in the frame's counters, zeroed by preprocess)
-        fr.composite(target=tgt, l1_sum=eng.l1, train=True, events=ke["fwd"] if ke is not None else None)
-        if fr.finish_bin():  # (the skipped first forward added nothing)
-            fr.composite(target=tgt, l1_sum=eng.l1, train=True)
+        if pair:
+            fr.train_pair(tgt, eng.l1, eng.acc, 1.0 / (h * w), events=ke["pair"] if ke is not None else None)
+            if fr.finish_bin():  # (the skipped first pair added nothing)
+                fr.train_pair(tgt, eng.l1, eng.acc, 1.0 / (h * w))
+        else:
+            fr.composite(target=tgt, l1_sum=eng.l1, train=True, events=ke["fwd"] if ke is not None else None)
+            if fr.finish_bin():  # (the skipped first forward added nothing)
+                fr.composite(target=tgt, l1_sum=eng.l1, train=True)
         c = fr.last_counters
         nat.raise_for_status(int(c[nat.XG_CTR_STICKY]))  # divergence of the previous step
         nat.raise_for_status(int(c[nat.XG_CTR_STATUS]) & ~nat.XG_ST_ENTRY_OVERFLOW)
         if self.targets_on_host:
             self.loss_host.copy_(eng.l1, non_blocking=True)  # the step's scalar result, to the host
         self.s_dev = None
-        if cfg.gamma == 0.0:
+        if pair:
+            fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, stats=self.stats,
+                        replay_done=True)
+        elif cfg.gamma == 0.0:
             fr.backward(self.cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, target=tgt,
                         l1_scale=1.0 / (h * w), stats=self.stats, reproducible=self.reproducible,
                         events=ke["bwd"] if ke is not None else None)

@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = _native.load_library()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.xg_abi_version() == _native.XG_ABI_VERSION == 4
+    assert lib.xg_abi_version() == _native.XG_ABI_VERSION == 5
 
 
 def test_binding_covers_header():

@@ -60,8 +60,34 @@ def _check_grads(name, eng, l1g, q, n):
     assert np.array_equal(eng.vis.cpu().numpy().astype(bool), l1g[q + "grad_visible"]), (name, q)
 
 
+def test_train_pair_matches_reference(golden, l1g):
+    """gamma = 0: Trainer.step's calls, verbatim - the overlapped forward +
+    reverse replay (xg_composite_train_pair) then the chain rule."""
+    import torch
+
+    for name in l1g["scenes"]:
+        name = str(name)
+        cloud, cam, eng, stats, h, w = _scene(golden, name)
+        tgt = torch.as_tensor(l1g[name + "/target"], device="cuda").contiguous()
+        fr = eng.frame
+        fr.preprocess(cloud, cam)
+        fr.bin_async()
+        fr.train_pair(tgt, eng.l1, eng.acc, 1.0 / (h * w))
+        if fr.finish_bin():
+            fr.train_pair(tgt, eng.l1, eng.acc, 1.0 / (h * w))
+        fr.backward(cloud, eng.acc, eng.grads.flat, eng.grads.screen_norms, eng.vis, stats=stats,
+                    replay_done=True)
+        torch.cuda.synchronize()
+        q = name + "/g0.0/"
+        value = float(eng.l1.item()) / (h * w)
+        ref = float(l1g[q + "loss"])
+        assert abs(value - ref) <= 1e-6 * abs(ref), (name, value, ref)
+        _check_grads(name, eng, l1g, q, cloud.n_points)
+
+
 def test_fused_l1_matches_reference(golden, l1g):
-    """gamma = 0: Trainer.step's fused calls, verbatim."""
+    """gamma = 0, the sequential calls: xg_composite_fwd_train's fused L1 sum,
+    then xg_composite_bwd's fused sign upstream."""
     import torch
 
     for name in l1g["scenes"]:

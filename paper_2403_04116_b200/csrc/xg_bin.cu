@@ -692,10 +692,12 @@ bool multisplit(int n_tiles) { return n_tiles <= XG_BIN_MULTISPLIT_TILES; }
 int64_t bin_chunks(int64_t n, int n_tiles) { return (n + bin_chunk(n, n_tiles) - 1) / bin_chunk(n, n_tiles); }
 
 // entry-balanced count / emit (XG_BIN_BALANCED=0 selects the Gaussian-chunked kernels)
-bool balanced(int n_tiles) {
-  static const int on = getenv("XG_BIN_BALANCED") ? atoi(getenv("XG_BIN_BALANCED")) : 1;
-  return on && n_tiles <= XG_BIN_BAL_TILES;
+// (1: training frames, 2: every frame, 0: never)
+int bal_mode() {
+  static const int m = getenv("XG_BIN_BALANCED") ? atoi(getenv("XG_BIN_BALANCED")) : 1;
+  return m;
 }
+bool balanced(int n_tiles) { return bal_mode() && n_tiles <= XG_BIN_BAL_TILES; }
 // balanced grid: XG_BIN_BAL_CTAS, more if the capacity needs it (entries per
 // CTA stay below 2^16: 16-bit local offsets)
 int64_t bal_grid(int64_t cap) {
@@ -819,7 +821,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     // sweeps keep the Gaussian-chunked kernels (fewer instructions per entry,
     // their imbalance hidden by the views binned concurrently - measured:
     // balanced C3 -5 %, C2 +1.6 %)
-    const bool bal = balanced(n_tiles) && sp->replay_ckpt != nullptr;
+    const bool bal = balanced(n_tiles) && (sp->replay_ckpt != nullptr || bal_mode() == 2);
     const int C = (int)(bal ? bal_grid(cap) : bin_chunks(n, n_tiles));
     const size_t sm_count = sizeof(uint32_t) * (size_t)kBinWarps * ((n_tiles + 1) / 2);
     const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2) +

@@ -6,6 +6,7 @@
 
 __global__ void k_step(float* buf, int n, int pdl) {
   if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (pdl == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) buf[i] = buf[i] * 1.0001f + 1.f;
 }
@@ -20,7 +21,7 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int grid : {148, 592}) {
-    for (int pdl = 0; pdl < 2; ++pdl) {
+    for (int pdl = 0; pdl < 3; ++pdl) {
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

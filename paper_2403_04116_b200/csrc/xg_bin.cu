@@ -289,6 +289,43 @@ __global__ void k_bin_ranges(const uint32_t* __restrict__ offs, int C, int T, ui
   ranges[2 * t + 1] = t + 1 < T ? (long long)offs[(long long)(t + 1) * C] : (long long)counters[XG_CTR_ENTRIES];
 }
 
+// T <= 1024: k_bin_ranges and the compositing schedule (k_tile_order's
+// heaviest-first order, same 64 log-spaced buckets) in one CTA - one launch
+// fewer per view
+__global__ void __launch_bounds__(1024) k_bin_ranges_order(const uint32_t* __restrict__ offs, int C, int T,
+                                                           uint32_t* counters, long long cap,
+                                                           long long* __restrict__ ranges, int* __restrict__ order) {
+  constexpr int NB = 64;
+  __shared__ int hist[NB];
+  __shared__ int off[NB];
+  const int t = threadIdx.x;
+  if (t < NB) hist[t] = 0;
+  const long long E = (long long)counters[XG_CTR_ENTRIES];
+  if (t == 0 && E > cap) atomicOr(&counters[XG_CTR_STATUS], XG_ST_ENTRY_OVERFLOW);
+  long long s0 = 0, s1 = 0;
+  if (t < T) {
+    s0 = offs[(long long)t * C];
+    s1 = t + 1 < T ? (long long)offs[(long long)(t + 1) * C] : E;
+    ranges[2 * t] = s0;
+    ranges[2 * t + 1] = s1;
+  }
+  const long long len = s1 - s0;
+  const int b = len > 0 ? (int)(4.f * __log2f((float)len + 1.f)) : 0;
+  const int key = NB - 1 - min(b, NB - 1);
+  __syncthreads();
+  if (t < T) atomicAdd(&hist[key], 1);
+  __syncthreads();
+  if (t == 0) {
+    int run = 0;
+    for (int k = 0; k < NB; ++k) {
+      off[k] = run;
+      run += hist[k];
+    }
+  }
+  __syncthreads();
+  if (t < T) order[atomicAdd(&off[key], 1)] = t;
+}
+
 __global__ void __launch_bounds__(kBinThreads)
     k_bin_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ n_tiles,
                const ushort4* __restrict__ rect, long long n, int ntx, int T, int rounds,
@@ -861,9 +898,16 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
                        w.tail_bytes, s)) != XG_OK)
       return st;
-    k_bin_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(w.hoff, C, n_tiles, sp->counters, cap,
-                                                      (long long*)sp->tile_ranges);
-    if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
+    const bool fused_order = sp->tile_order && n_tiles <= 1024;
+    if (fused_order) {
+      k_bin_ranges_order<<<1, 1024, 0, s>>>(w.hoff, C, n_tiles, sp->counters, cap, (long long*)sp->tile_ranges,
+                                            sp->tile_order);
+      if ((st = check_launch("k_bin_ranges_order")) != XG_OK) return st;
+    } else {
+      k_bin_ranges<<<div_up(n_tiles, 256), 256, 0, s>>>(w.hoff, C, n_tiles, sp->counters, cap,
+                                                        (long long*)sp->tile_ranges);
+      if ((st = check_launch("k_bin_ranges")) != XG_OK) return st;
+    }
     if (bin_stop == 2) return XG_OK;
     if (bal) {
       const size_t sm_bal = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2));
@@ -876,7 +920,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
                                                  bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
       if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
     }
-    if (!sp->tile_order) return XG_OK;
+    if (!sp->tile_order || fused_order) return XG_OK;
     return launch_tile_order(sp->tile_ranges, n_tiles, sp->tile_order, s);
   }
   // 2. offsets of every Gaussian's entries, in depth order

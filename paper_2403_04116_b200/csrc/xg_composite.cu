@@ -941,17 +941,20 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack, kLite>())
   const bool skip = a.n_entries && (long long)*a.n_entries > a.cap;
   const int i = blockIdx.x * (kWarps / kSubs) + warp / kSubs;
   if (!skip && i < a.n_tiles) composite_unit<kTrack, kP, kLite>(a, a.order[i], warp % kSubs, s_rec[warp], s_k[warp]);
-  if (kTrack && kLite && kSubs == 4 && kWarps == 4) {  // one tile per CTA
+  if (kTrack && kLite) {
     if (a.ring) {
-      // publish the tile's chunks (k_replay_items' count: ceil(L / kCk), L =
-      // the longest replay of its quarters) after its pixels, checkpoints
-      // and costs are visible; an overflowed view publishes nothing
+      // publish each of the CTA's tiles' chunks (k_replay_items' count:
+      // ceil(L / kCk), L = the longest replay of its quarters) after its
+      // pixels, checkpoints and costs are visible; an overflowed view
+      // publishes nothing
+      constexpr int kTpc = kWarps / kSubs;  // tiles per CTA
       __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) {
+      if (threadIdx.x < kTpc) {
         uint32_t nch = 0;
-        const int tile = i < a.n_tiles ? a.order[i] : 0;
-        if (!skip && i < a.n_tiles) {
+        const int it = blockIdx.x * kTpc + threadIdx.x;
+        const int tile = it < a.n_tiles ? a.order[it] : 0;
+        if (!skip && it < a.n_tiles) {
           int L = 0;
           for (int q = 0; q < 4; ++q) L = max(L, a.unit_cost[4 * tile + q]);
           nch = (uint32_t)((L + kCk - 1) >> kCkShift);
@@ -966,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas(fwd_pairs<kTrack, kLite>())
             }
         }
         __threadfence();
-        atomicAdd(&a.ring_ctr[1], 1u);
+        if (it < a.n_tiles) atomicAdd(&a.ring_ctr[1], 1u);  // (tiles published: exactly n_tiles in the end)
       }
     }
   }
@@ -2072,7 +2075,7 @@ xg_status xg_composite_train_pair(const xg_camera* cam, const xg_splats* sp, flo
   }
   static const bool on = !(getenv("XG_TRAIN_STREAM") && atoi(getenv("XG_TRAIN_STREAM")) == 0);
   const int n_tiles = tiles_x(*cam) * tiles_y(*cam);
-  const bool ok = on && kBwdPairs == 4 && kFwdLitePairs == 1 && kWarps == 4 && sp->replay_ckpt &&
+  const bool ok = on && kBwdPairs == 4 && sp->replay_ckpt &&
                   sp->replay_items && sp->unit_cost && sp->tile_order && sp->counters && sp->entry_splat &&
                   sp->tile_ranges && sp->mean2d && sp->coef && sp->inten &&
                   sp->replay_slots >= xg_replay_slots(sp->entry_capacity, n_tiles);
@@ -2102,7 +2105,7 @@ xg_status xg_composite_train_pair(const xg_camera* cam, const xg_splats* sp, flo
             sp->entry_capacity > 0 ? sp->counters + XG_CTR_ENTRIES : nullptr, (long long)sp->entry_capacity,
             tiles_x(*cam), cam->width, cam->height, (float2*)sp->replay_ckpt, ring, ring_cap,
             sp->counters + XG_CTR_ITEMS, epoch};
-  k_composite_fwd_np<true, true><<<n_tiles, kThreads, 0, s>>>(a);
+  k_composite_fwd_np<true, true><<<div_up(n_tiles, kWarps * kFwdLitePairs / 4), kThreads, 0, s>>>(a);
   xg_status st = check_launch("k_composite_fwd_np");
   if (st != XG_OK) return st;
   BwdArgs b{(const double2*)sp->mean2d, (const float4*)sp->coef, sp->inten, sp->entry_splat,

@@ -82,59 +82,6 @@ __global__ void k_adam(AdamArgs a) {
   }
 }
 
-// The whole buffer in one launch (xg_adam): rotations are taken a Gaussian
-// at a time - one thread updates the quaternion's 4 elements and then
-// renormalises it (normalize_rotations, gaussians.py:234-235) exactly as
-// k_renorm would after the element-wise pass, so the result is bit-identical
-// to k_adam + k_renorm without the second launch.  Virtual index: [0, 3n)
-// positions, [3n, 4n) quaternions, then the elements from 7n on.
-__device__ __forceinline__ float adam_step(const AdamArgs& a, long long e, float lr, float b1, float b2, float omb1,
-                                           float omb2, float bc1, float bc2, float eps) {
-  const float g = a.g[e];
-  float m = a.m[e], v = a.v[e];
-  m = __fmaf_rn(b1, m, __fmul_rn(omb1, g));
-  v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(omb2, g), g));
-  a.m[e] = m;
-  a.v[e] = v;
-  return __fsub_rn(a.p[e], __fmul_rn(lr, __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps))));
-}
-
-__global__ void k_adam_full(AdamArgs a, long long total) {
-  const uint32_t bad = a.status ? (a.status[0] >> XG_ST_GRAD_NONFINITE_SHIFT) & 0x1f : 0u;
-  const float b1 = (float)a.b1, b2 = (float)a.b2, omb1 = (float)(1.0 - a.b1), omb2 = (float)(1.0 - a.b2);
-  const float bc1 = (float)a.bc1, bc2 = (float)a.bc2, eps = (float)a.eps;
-  float lrf[kFields];
-#pragma unroll
-  for (int k = 0; k < kFields; ++k) lrf[k] = (float)a.lr[k];
-  const long long n = a.n;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    if (t >= 3 * n && t < 4 * n) {
-      if (bad & 3u) continue;  // positions or rotations diverged: rotations untouched, no renorm
-      const long long e0 = 3 * n + 4 * (t - 3 * n);
-      float q[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) q[c] = adam_step(a, e0 + c, lrf[1], b1, b2, omb1, omb2, bc1, bc2, eps);
-      if (bad) {  // a later field diverged: updated, not renormalised (as k_renorm skips)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a.p[e0 + c] = q[c];
-        continue;
-      }
-      const double w = q[0], x = q[1], y = q[2], z = q[3];
-      const double nrm = sqrt(((w * w + x * x) + y * y) + z * z);
-      a.p[e0 + 0] = (float)(w / nrm);
-      a.p[e0 + 1] = (float)(x / nrm);
-      a.p[e0 + 2] = (float)(y / nrm);
-      a.p[e0 + 3] = (float)(z / nrm);
-      continue;
-    }
-    const long long e = t < 3 * n ? t : t + 3 * n;
-    const int f = (e >= a.bound[0]) + (e >= a.bound[1]) + (e >= a.bound[2]) + (e >= a.bound[3]);
-    if (bad & ((2u << f) - 1u)) continue;
-    a.p[e] = adam_step(a, e, lrf[f], b1, b2, omb1, omb2, bc1, bc2, eps);
-  }
-}
-
 // normalize_rotations (gaussians.py:234-235) after the update; skipped if
 // any field diverged (the reference raises before renormalising).
 __global__ void k_renorm(float* q_all, long long n, const uint32_t* status) {
@@ -338,35 +285,10 @@ xg_status xg_adam(float* params, const float* grads, float* exp_avg, float* exp_
                   int32_t n_features, const double* lr, double beta1, double beta2, double eps,
                   double bc1, double bc2, const uint32_t* status, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (!params || !grads || !exp_avg || !exp_avg_sq || !lr || n < 1 || n_features < 0) {
-    set_error_msg("xg_adam: invalid argument");
-    return XG_ERR_INVALID;
-  }
-  // one launch: element-wise Adam with the quaternion renormalisation fused
-  AdamArgs a;
-  a.p = params;
-  a.g = grads;
-  a.m = exp_avg;
-  a.v = exp_avg_sq;
-  a.n = n;
-  a.bound[0] = 3 * n;
-  a.bound[1] = 7 * n;
-  a.bound[2] = 10 * n;
-  a.bound[3] = 11 * n;
-  a.begin = 0;
-  a.end = n * (11 + n_features);
-  for (int f = 0; f < kFields; ++f) a.lr[f] = lr[f];
-  a.b1 = beta1;
-  a.b2 = beta2;
-  a.eps = eps;
-  a.bc1 = bc1;
-  a.bc2 = bc2;
-  a.status = status;
-  const long long total = n * (11 + n_features) - 3 * n;  // (4 rotation elements per quaternion thread)
-  int grid = div_up(total, 256);
-  if (grid > 148 * 16) grid = 148 * 16;
-  k_adam_full<<<grid, 256, 0, s>>>(a, total);
-  return check_launch("k_adam_full");
+  xg_status st = adam_launch(params, grads, exp_avg, exp_avg_sq, n, n_features, lr, beta1, beta2, eps, bc1,
+                             bc2, status, 0, n * (11 + n_features), s);
+  if (st != XG_OK) return st;
+  return xg_adam_renorm(params, n, n_features, status, stream);
 }
 
 xg_status xg_adam_range(float* params, const float* grads, float* exp_avg, float* exp_avg_sq, int64_t n,

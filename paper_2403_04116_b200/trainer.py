@@ -326,6 +326,7 @@ class _IterationEngine:
         n = cloud.n_points
         cap = capacity or (getattr(self, "frame", None) and self.frame.entry_capacity) or 16 * n
         self.frame = Frame(n, self.h, self.w, cloud.device, entry_capacity=cap)
+        self.frame._alloc_replay()  # (a training frame from the first bin on: entry-balanced binning)
         self.grads = make_gradients(n, cloud.n_features, cloud.device)
         self.acc = torch.empty((n, 8), dtype=torch.float32, device=cloud.device)  # (zeroed by xg_composite_bwd)
         self.vis = torch.empty(n, dtype=torch.uint8, device=cloud.device)

@@ -18,9 +18,11 @@ Mirrors ``pkg/src/xsplat/trainer.py`` API for API:
   opacity reset, metrics.tsv and PLY checkpoints.
 
 Inside ``train`` one iteration is: preprocess -> bin (one host sync: entry
-count + status words) -> composite with the L1 sum fused -> reverse
-composite with the L1 pixel gradient computed on the fly and DensifyStats
-accumulated in the chain-rule kernel -> fused Adam.  Non-finite gradients
+count + status words) -> composite with the L1 sum fused and reverse
+composite with the L1 pixel gradient computed on the fly, as one overlapped
+pair at gamma = 0 (``xg_composite_train_pair``: the replay of each tile starts
+as soon as its forward is done) -> chain rule with DensifyStats accumulated
+-> fused Adam.  Non-finite gradients
 are flagged on the device and surface at the next iteration's sync, before
 any further update (same cloud state as the reference at the raise).
 """

@@ -260,6 +260,10 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
+// set by a caller that has already zeroed the next scan_u32's workspace
+// (host-side, per call; the library's launch paths are single-threaded per stream)
+static thread_local bool g_scan_precleared = false;
+
 size_t scan_workspace_bytes(int64_t cap) {
   const int64_t tiles = (cap + kScanTile - 1) / kScanTile + 1;
   return align_up(sizeof(unsigned long long) * (size_t)tiles) + 256;
@@ -268,6 +272,8 @@ size_t scan_workspace_bytes(int64_t cap) {
 xg_status scan_u32(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64_t cap,
                    const uint32_t* n_dev, int64_t n_host, uint32_t* total, void* ws, size_t ws_bytes,
                    cudaStream_t s) {
+  const bool precleared = g_scan_precleared;  // (one call only)
+  g_scan_precleared = false;
   if (cap <= 0) {
     if (total) cudaMemsetAsync(total, 0, sizeof(uint32_t), s);
     return XG_OK;
@@ -280,7 +286,7 @@ xg_status scan_u32(const uint32_t* in, const uint32_t* gather, uint32_t* out, in
   const int tiles = div_up(cap, kScanTile);
   unsigned long long* states = (unsigned long long*)ws;
   uint32_t* counter = (uint32_t*)((char*)ws + align_up(sizeof(unsigned long long) * (size_t)(tiles + 1)));
-  cudaMemsetAsync(ws, 0, need, s);
+  if (!precleared) cudaMemsetAsync(ws, 0, need, s);
   k_scan<<<tiles, kScanThreads, 0, s>>>(in, gather, out, n_dev, n_host, cap, states, counter, total);
   return check_launch("k_scan");
 }
@@ -587,7 +593,8 @@ struct OsWs {
 
 // carve the workspace and zero what n_passes passes use (histograms,
 // counters and their look-back status words)
-OsWs os_prepare(void* ws, int64_t cap, int n_passes, cudaStream_t s) {
+// (clear = false: the caller zeroes os_prepare_bytes(cap, n_passes) at ws itself)
+OsWs os_prepare(void* ws, int64_t cap, int n_passes, cudaStream_t s, bool clear = true) {
   OsWs w;
   w.tiles = (cap + kOsTile - 1) / kOsTile;
   char* p = (char*)ws;
@@ -600,8 +607,15 @@ OsWs os_prepare(void* ws, int64_t cap, int n_passes, cudaStream_t s) {
   p += align_up(sizeof(uint32_t) * kOsPasses);
   w.status = (uint32_t*)p;
   const int np = n_passes < kOsPasses ? n_passes : kOsPasses;
-  cudaMemsetAsync(ws, 0, (size_t)(p - (char*)ws) + sizeof(uint32_t) * (size_t)np * w.tiles * 256, s);
+  if (clear) cudaMemsetAsync(ws, 0, (size_t)(p - (char*)ws) + sizeof(uint32_t) * (size_t)np * w.tiles * 256, s);
   return w;
+}
+
+size_t os_prepare_bytes(int64_t cap, int n_passes) {
+  const int64_t tiles = (cap + kOsTile - 1) / kOsTile;
+  const int np = n_passes < kOsPasses ? n_passes : kOsPasses;
+  return align_up(sizeof(uint32_t) * kOsPasses * 256 * 2) + align_up(sizeof(int) * (kOsPasses + 1)) +
+         align_up(sizeof(uint32_t) * kOsPasses) + sizeof(uint32_t) * (size_t)np * tiles * 256;
 }
 
 xg_status os_passes(const OsWs& w, const unsigned long long* keys_in, const uint32_t* vals_in,
@@ -723,17 +737,20 @@ inline size_t bs_fixed_bytes() {
          2 * al256(sizeof(uint32_t) * kBsBuckets);
 }
 
+// Layout: the all-ones region [mm | bmin | bmax], the unset [start | large |
+// mixed], then the zero region [n_large | n_mixed | count | scan_ws | tail],
+// so one memset per value initialises the whole sort (bucket_sort_depth).
 inline bool bs_carve(void* ws, size_t bytes, BsWs& w) {
   char* p = (char*)ws;
   w.mm = (unsigned long long*)p; p += 256;
-  w.n_large = (uint32_t*)p; p += 256;
-  w.count = (uint32_t*)p; p += al256(sizeof(uint32_t) * (kBsBuckets + 1));
-  w.start = (uint32_t*)p; p += al256(sizeof(uint32_t) * (kBsBuckets + 1));
   w.bmin = (unsigned long long*)p; p += al256(sizeof(unsigned long long) * kBsBuckets);
   w.bmax = (unsigned long long*)p; p += al256(sizeof(unsigned long long) * kBsBuckets);
+  w.start = (uint32_t*)p; p += al256(sizeof(uint32_t) * (kBsBuckets + 1));
   w.large = (uint32_t*)p; p += al256(sizeof(uint32_t) * kBsBuckets);
   w.mixed = (uint32_t*)p; p += al256(sizeof(uint32_t) * kBsBuckets);
+  w.n_large = (uint32_t*)p; p += 256;
   w.n_mixed = (uint32_t*)p; p += 256;
+  w.count = (uint32_t*)p; p += al256(sizeof(uint32_t) * (kBsBuckets + 1));
   w.scan_ws = p;
   w.scan_bytes = al256(scan_workspace_bytes(kBsBuckets));
   p += w.scan_bytes;
@@ -1103,21 +1120,21 @@ xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_ti
     set_error_msg("bucket_sort_depth: workspace too small");
     return XG_ERR_WORKSPACE;
   }
-  cudaMemsetAsync(w.mm, 0xff, 2 * sizeof(unsigned long long), s);
-  cudaMemsetAsync(w.n_large, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(w.n_mixed, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(w.count, 0, sizeof(uint32_t) * kBsBuckets, s);
-  cudaMemsetAsync(w.bmin, 0xff, sizeof(unsigned long long) * kBsBuckets, s);
-  cudaMemsetAsync(w.bmax, 0xff, sizeof(unsigned long long) * kBsBuckets, s);
+  // two memsets: mm, bmin, bmax to all ones; the counts, the bucket-count
+  // scan's look-back state and the onesweep's histograms / look-back state
+  // to zero (bs_carve's layout)
+  cudaMemsetAsync(w.mm, 0xff, (size_t)((char*)w.start - (char*)w.mm), s);
+  cudaMemsetAsync(w.n_large, 0, (size_t)((char*)w.tail - (char*)w.n_large) + os_prepare_bytes(n, 2), s);
   const int g = (int)((n + 255) / 256);
   k_bs_minmax<<<g < 592 ? g : 592, 256, 0, s>>>(keys, n_tiles, n, w.mm, n_dev);
   xg_status st = check_launch("k_bs_minmax");
   if (st != XG_OK) return st;
   // bucket ids into key_b, iota into val_b (the onesweep's read-only inputs)
   // (the onesweep's histograms are accumulated by k_bs_bucket: zero them first)
-  const OsWs ow = os_prepare(w.tail, n, 2, s);
+  const OsWs ow = os_prepare(w.tail, n, 2, s, false);
   k_bs_bucket<<<g, 256, 0, s>>>(keys, n_tiles, n, w.mm, key_b, val_b, w.count, w.bmin, w.bmax, ow.ghist);
   if ((st = check_launch("k_bs_bucket")) != XG_OK) return st;
+  g_scan_precleared = w.scan_bytes >= scan_workspace_bytes(kBsBuckets);  // (zeroed above)
   if ((st = scan_u32(w.count, nullptr, w.start, kBsBuckets, nullptr, kBsBuckets, w.start + kBsBuckets, w.scan_ws,
                      w.scan_bytes, s)) != XG_OK)
     return st;

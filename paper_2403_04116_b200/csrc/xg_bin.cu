@@ -764,7 +764,8 @@ size_t tail_bytes(int64_t n, int64_t cap, int n_tiles) {
   const size_t bsw = bucket_sort_workspace_bytes(n);
   if (bsw > a) a = bsw;
   const int64_t hn = multisplit(n_tiles) ? (int64_t)n_tiles * ms_chunks(n, cap, n_tiles) : 0;
-  size_t b = scan_workspace_bytes(n > hn ? n : hn);
+  // (balanced path: the offsets scan and the (tile, chunk) scan side by side, cleared by one memset)
+  size_t b = align_up(scan_workspace_bytes(n)) + align_up(scan_workspace_bytes(hn > 0 ? hn : 1));
   return a > b ? a : b;
 }
 
@@ -860,6 +861,8 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     // balanced C3 -5 %, C2 +1.6 %)
     const bool bal = balanced(n_tiles) && (sp->replay_ckpt != nullptr || bal_mode() == 2);
     const int C = (int)(bal ? bal_grid(cap) : bin_chunks(n, n_tiles));
+    void* scan2_ws = nullptr;
+    size_t scan2_bytes = 0;
     const size_t sm_count = sizeof(uint32_t) * (size_t)kBinWarps * ((n_tiles + 1) / 2);
     const size_t sm_emit = sizeof(uint32_t) * ((size_t)n_tiles + (size_t)kBinWarps * ((n_tiles + 1) / 2) +
                                                (XG_BIN_EMIT_MASKS ? (size_t)kBinWarps * (ntx + nty) : 0));
@@ -874,8 +877,14 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     }
     if (bal) {
       // entry offsets of the depth-sorted splats (and E) cut the entries into equal warp slices
+      // both scans' look-back states zeroed by one memset (the depth sort used this space)
+      const size_t need1 = align_up(scan_workspace_bytes(n));
+      scan2_ws = (char*)w.tail + need1;
+      scan2_bytes = w.tail_bytes - need1;
+      cudaMemsetAsync(w.tail, 0, need1 + scan_workspace_bytes((long long)n_tiles * C), s);
+      scan_u32_precleared_next();
       if ((st = scan_u32(sp->n_tiles, sp->order, w.offN, n, nullptr, n, sp->counters + XG_CTR_ENTRIES, w.tail,
-                         w.tail_bytes, s)) != XG_OK)
+                         need1, s)) != XG_OK)
         return st;
       static bool attr_bal = false;
       if (!attr_bal) {
@@ -895,8 +904,9 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
       if ((st = check_launch("k_bin_count")) != XG_OK) return st;
     }
     const long long hn = (long long)n_tiles * C;
-    if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES, w.tail,
-                       w.tail_bytes, s)) != XG_OK)
+    if (bal) scan_u32_precleared_next();
+    if ((st = scan_u32(w.hist, nullptr, w.hoff, hn, nullptr, hn, sp->counters + XG_CTR_ENTRIES,
+                       bal ? scan2_ws : w.tail, bal ? scan2_bytes : w.tail_bytes, s)) != XG_OK)
       return st;
     const bool fused_order = sp->tile_order && n_tiles <= 1024;
     if (fused_order) {

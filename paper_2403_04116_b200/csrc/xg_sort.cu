@@ -264,6 +264,8 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 // (host-side, per call; the library's launch paths are single-threaded per stream)
 static thread_local bool g_scan_precleared = false;
 
+void scan_u32_precleared_next() { g_scan_precleared = true; }
+
 size_t scan_workspace_bytes(int64_t cap) {
   const int64_t tiles = (cap + kScanTile - 1) / kScanTile + 1;
   return align_up(sizeof(unsigned long long) * (size_t)tiles) + 256;

@@ -9,6 +9,9 @@ namespace xg {
 // (else n_host); grids are sized for `cap`.  If total != nullptr the sum is
 // written there (device).  Single pass, decoupled look-back.
 size_t scan_workspace_bytes(int64_t cap);
+// the next scan_u32 on this host thread finds its workspace already zeroed
+// (the caller cleared scan_workspace_bytes(cap) bytes at ws): no memset
+void scan_u32_precleared_next();
 xg_status scan_u32(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64_t cap,
                    const uint32_t* n_dev, int64_t n_host, uint32_t* total, void* ws, size_t ws_bytes,
                    cudaStream_t s);

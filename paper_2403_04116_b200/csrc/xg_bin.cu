@@ -494,9 +494,9 @@ __global__ void __launch_bounds__(kBinThreads)
 // Entry-balanced multisplit (T <= XG_BIN_BAL_TILES).  The Gaussian-chunked
 // kernels above give every warp 32 x rounds depth-sorted Gaussians, so one
 // warp of large splats walks thousands of entries while its neighbours walk
-// tens: on a trained C2 cloud (tiles touched p50 16, p99 868) the slowest
-// warp holds 14x the median and the count / emit launches run with half the
-// SMs idle.  Here the scan of tiles-touched in depth order (offN, the
+// hundreds: on a trained C2 cloud (tiles touched p50 16, p99 132, max 1,024)
+// the slowest warp holds 4.3x the median's entries and the emit ran with its
+// SMs active 56 % of the time.  Here the scan of tiles-touched in depth order (offN, the
 // entries' global offsets) cuts the E entries into C x 8 equal warp slices:
 // warp w of CTA c walks entries [c EC + w EC / 8, ...) in the same (depth,
 // rect row-major) order - so per-(CTA, warp, tile) counts still rank every

@@ -19,7 +19,7 @@ ds, _ = bench.phantom_dataset(g, sc)
 tr = Trainer(ds, GaussianCloud(**acui.init_alternative_arrays("cuboid", acui.benchmark_spec(g), 16, 0),
                                device="cuda"), TrainConfig(iterations=20000, log_interval=10**9,
                                                            eval_interval=10**9))
-for _ in range(warm):
+for _ in range(warm + 1):  # (+1: iteration warm is a density-control event; the next one rebinds the frame)
     tr.step()
 torch.cuda.synchronize()
 fr = tr.eng.frame
@@ -32,9 +32,9 @@ def pct(a, name):
           + f" sum={a.sum():.0f}")
 
 
-tt = fr.tiles_touched.cpu().numpy()[: tr.cloud.n_points]
+tt = fr.tiles_touched.cpu().numpy()[: fr.n]
 pct(tt, "tiles touched / Gaussian")
-order = fr.order.cpu().numpy()[: tr.cloud.n_points]
+order = fr.order.cpu().numpy()[: fr.n]
 tt_sorted = tt[order]
 w = tt_sorted[: (tt_sorted.size // 32) * 32].reshape(-1, 32).sum(1)
 pct(w, "entries / binning warp (32 depth-sorted Gaussians)")

@@ -177,13 +177,15 @@ inline int bin_rounds(int64_t n, int n_tiles) {
 }
 inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
-// k_bin_emit phase 3: 32-entry windows over the round's concatenated entries
-// ranked with __match_any_sync (default), or (=1) a lane per Gaussian with
-// the peers ranked by column / row lane masks - fewer instructions, but each
-// lane's walk over its rect is a serial shared-memory chain: +2 % C4 and
-// +0.3 % C3 sweeps (many views hide it), -6 % per C2 iteration (one view)
+// k_bin_emit phase 3: (=1, default) a lane per Gaussian with the round's
+// peers ranked by column / row lane masks, or (=0) 32-entry windows over the
+// round's concatenated entries ranked with __match_any_sync.  The masks take
+// 14 % fewer instructions but each lane's walk over its rect is a serial
+// shared-memory chain: measured +2.3 % C4 and +0.5 % C3 (sweeps: many views
+// hide the chains), -6 % per C2 iteration - which is why single-view
+// training frames take the entry-balanced k_bin_emit_bal instead
 #ifndef XG_BIN_EMIT_MASKS
-#define XG_BIN_EMIT_MASKS 0
+#define XG_BIN_EMIT_MASKS 1
 #endif
 
 // A warp's 32 depth-sorted Gaussians of one round, software-pipelined: the

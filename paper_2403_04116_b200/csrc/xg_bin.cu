@@ -163,8 +163,15 @@ static_assert(kBinThreads * kBinMaxRounds < 65536, "k_bin_emit keeps per-tile lo
 // T offsets), so the chunk grows with the tile count: ~3 CTAs per SM for
 // T <= 1024 (small training clouds still fill the GPU), ~2 waves of one
 // CTA per SM (128 KB of counters) at T = 4096.
+// (T <= 1024: since single-view training frames take the entry-balanced
+// kernels, the chunked ones serve concurrent sweeps, where fewer, longer
+// CTAs win - measured on C3: 444 CTAs / <= 4 rounds 2,951 fps, 222 / 8
+// 2,978, 160 / 12 2,970, 148 / 16 2,948)
 #ifndef XG_BIN_CTAS_SMALL_T
-#define XG_BIN_CTAS_SMALL_T 444
+#define XG_BIN_CTAS_SMALL_T 222
+#endif
+#ifndef XG_BIN_SMALL_T_MAX_ROUNDS
+#define XG_BIN_SMALL_T_MAX_ROUNDS 8
 #endif
 #ifndef XG_BIN_CTAS_LARGE_T
 #define XG_BIN_CTAS_LARGE_T 296
@@ -172,7 +179,7 @@ static_assert(kBinThreads * kBinMaxRounds < 65536, "k_bin_emit keeps per-tile lo
 inline int bin_rounds(int64_t n, int n_tiles) {
   const int64_t ctas = n_tiles > 1024 ? XG_BIN_CTAS_LARGE_T : XG_BIN_CTAS_SMALL_T;
   const int64_t r = (n + (int64_t)kBinThreads * ctas - 1) / ((int64_t)kBinThreads * ctas);
-  const int cap = n_tiles > 1024 ? kBinMaxRounds : 4;
+  const int cap = n_tiles > 1024 ? kBinMaxRounds : XG_BIN_SMALL_T_MAX_ROUNDS;
   return r < 1 ? 1 : (r > cap ? cap : (int)r);
 }
 inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }

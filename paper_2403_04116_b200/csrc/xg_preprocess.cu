@@ -328,14 +328,23 @@ __global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(Clo
       if (o.g_int) o.g_int[i] = 0.0;
       if (o.g_alpha) o.g_alpha[i] = 0.0;
     } else {
-      Proj p;
-      project_one(c, k, i, p);
+      // every global read this thread needs issued before the projection's
+      // float64 chain (their latency overlaps it instead of following it):
+      // the replay's accumulators, the splat's coefficients, the opacity,
+      // the features (intensity) and the DensifyStats being accumulated
       const float4 a0 = reinterpret_cast<const float4*>(acc)[2 * i];
       const float4 a1 = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+      const float4 cf = reinterpret_cast<const float4*>(sp.coef)[i];
+      const float raw_i = c.raw[i];
+      bool finite;
+      const double it = intensity_of(c, i, &finite);
+      const float ns_prev = o.norm_sum ? o.norm_sum[i] : 0.f;
+      const int32_t oc_prev = o.obs_count ? o.obs_count[i] : 0;
+      Proj p;
+      project_one(c, k, i, p);
       // kernel accumulators -> reference kernel outputs (xgauss.h, K4a):
       // sum G (2 A2 dx + B2 dy) = 2 A2 sum G dx + B2 sum G dy, and the mean
       // gradient is -ln2 times that (p2 = power * log2 e, dx = px - mx)
-      const float4 cf = reinterpret_cast<const float4*>(sp.coef)[i];
       const double sdx = a0.x, sdy = a0.y;
       const double gmx = -kLn2 * (2.0 * (double)cf.x * sdx + (double)cf.y * sdy);
       const double gmy = -kLn2 * ((double)cf.y * sdx + 2.0 * (double)cf.z * sdy);
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(Clo
       const double gcc = -0.5 * (double)a1.x;
       const double gint = (double)a1.y;
       const double gpow = (double)a1.z;
-      const double alpha = det_sigmoid((double)c.raw[i]);
+      const double alpha = det_sigmoid((double)raw_i);
       const double galpha = alpha > 0.0 ? gpow / alpha : 0.0;  // sum dsigma*dens
       if (o.g_mean) { o.g_mean[2 * i] = gmx; o.g_mean[2 * i + 1] = gmy; }
       if (o.g_conic) { o.g_conic[3 * i] = gca; o.g_conic[3 * i + 1] = gcb; o.g_conic[3 * i + 2] = gcc; }
@@ -423,8 +432,6 @@ __global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(Clo
       const double inner = qw * gu[0] + qx * gu[1] + qy * gu[2] + qz * gu[3];
       const double qv[4] = {qw, qx, qy, qz};
       // features / opacity (:112-115)
-      bool finite;
-      const double it = intensity_of(c, i, &finite);
       const double gf = gint * it * (1.0 - it);
       const double graw = gpow * (1.0 - alpha);  // = g_alpha * alpha * (1 - alpha)
 
@@ -449,8 +456,8 @@ __global__ void __launch_bounds__(128, XG_PRE_BWD_MIN_CTAS) k_preprocess_bwd(Clo
       const float sn = (float)hypot(gmx, gmy);
       if (o.screen_norms) o.screen_norms[i] = sn;
       if (o.visible) o.visible[i] = 1;
-      if (o.norm_sum) o.norm_sum[i] += sn;
-      if (o.obs_count) o.obs_count[i] += 1;
+      if (o.norm_sum) o.norm_sum[i] = ns_prev + sn;
+      if (o.obs_count) o.obs_count[i] = oc_prev + 1;
       if (o.world_grad_sum)
         for (int a = 0; a < 3; ++a) o.world_grad_sum[3 * i + a] += (float)gp[a];
     }

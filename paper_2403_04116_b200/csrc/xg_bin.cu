@@ -176,13 +176,17 @@ static_assert(kBinThreads * kBinMaxRounds < 65536, "k_bin_emit keeps per-tile lo
 #ifndef XG_BIN_CTAS_LARGE_T
 #define XG_BIN_CTAS_LARGE_T 296
 #endif
-inline int bin_rounds(int64_t n, int n_tiles) {
-  const int64_t ctas = n_tiles > 1024 ? XG_BIN_CTAS_LARGE_T : XG_BIN_CTAS_SMALL_T;
+// lat: a single-view (training) frame's chunking - round 1's 444 CTAs of
+// up to 4 rounds for T <= 1024 (sweeps take the fewer, longer CTAs above)
+inline int bin_rounds(int64_t n, int n_tiles, bool lat = false) {
+  const int64_t ctas = n_tiles > 1024 ? XG_BIN_CTAS_LARGE_T : (lat ? 444 : XG_BIN_CTAS_SMALL_T);
   const int64_t r = (n + (int64_t)kBinThreads * ctas - 1) / ((int64_t)kBinThreads * ctas);
-  const int cap = n_tiles > 1024 ? kBinMaxRounds : XG_BIN_SMALL_T_MAX_ROUNDS;
+  const int cap = n_tiles > 1024 ? kBinMaxRounds : (lat ? 4 : XG_BIN_SMALL_T_MAX_ROUNDS);
   return r < 1 ? 1 : (r > cap ? cap : (int)r);
 }
-inline int64_t bin_chunk(int64_t n, int n_tiles) { return (int64_t)kBinThreads * bin_rounds(n, n_tiles); }
+inline int64_t bin_chunk(int64_t n, int n_tiles, bool lat = false) {
+  return (int64_t)kBinThreads * bin_rounds(n, n_tiles, lat);
+}
 constexpr int kBinMaxTiles = 4096;                             // smem: 8 warps x 4096 x 4 B
 // k_bin_emit phase 3: (=1, default) a lane per Gaussian with the round's
 // peers ranked by column / row lane masks, or (=0) 32-entry windows over the
@@ -735,7 +739,9 @@ struct BinWs {
 static_assert(XG_BIN_MULTISPLIT_TILES <= 4096, "multisplit counters: 8 warps x 4096 x 4 B of shared memory");
 bool multisplit(int n_tiles) { return n_tiles <= XG_BIN_MULTISPLIT_TILES; }
 
-int64_t bin_chunks(int64_t n, int n_tiles) { return (n + bin_chunk(n, n_tiles) - 1) / bin_chunk(n, n_tiles); }
+int64_t bin_chunks(int64_t n, int n_tiles, bool lat = false) {
+  return (n + bin_chunk(n, n_tiles, lat) - 1) / bin_chunk(n, n_tiles, lat);
+}
 
 // entry-balanced count / emit (XG_BIN_BALANCED=0 selects the Gaussian-chunked kernels)
 // (1: training frames, 2: every frame, 0: never)
@@ -753,7 +759,9 @@ int64_t bal_grid(int64_t cap) {
 // CTAs of the multisplit count / emit launches (the (tile, chunk) table
 // width) - workspaces are sized for either path
 int64_t ms_chunks(int64_t n, int64_t cap, int n_tiles) {
-  const int64_t a = bin_chunks(n, n_tiles);
+  int64_t a = bin_chunks(n, n_tiles);
+  const int64_t al = bin_chunks(n, n_tiles, true);
+  if (al > a) a = al;
   if (!balanced(n_tiles)) return a;
   const int64_t b = bal_grid(cap);
   return a > b ? a : b;
@@ -868,8 +876,13 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
     // sweeps keep the Gaussian-chunked kernels (fewer instructions per entry,
     // their imbalance hidden by the views binned concurrently - measured:
     // balanced C3 -5 %, C2 +1.6 %)
-    const bool bal = balanced(n_tiles) && (sp->replay_ckpt != nullptr || bal_mode() == 2);
-    const int C = (int)(bal ? bal_grid(cap) : bin_chunks(n, n_tiles));
+    // (XG_BIN_TRAIN_CHUNKED=1, measurement: training frames on the
+    // Gaussian-chunked kernels with the latency chunking)
+    static const bool train_chunked = getenv("XG_BIN_TRAIN_CHUNKED") && atoi(getenv("XG_BIN_TRAIN_CHUNKED")) > 0;
+    const bool lat = sp->replay_ckpt != nullptr;
+    const bool bal = balanced(n_tiles) && (lat || bal_mode() == 2) && !(train_chunked && lat);
+    const int rounds = bin_rounds(n, n_tiles, lat);
+    const int C = (int)(bal ? bal_grid(cap) : bin_chunks(n, n_tiles, lat));
     void* scan2_ws = nullptr;
     size_t scan2_bytes = 0;
     const size_t sm_count = sizeof(uint32_t) * (size_t)kBinWarps * ((n_tiles + 1) / 2);
@@ -909,7 +922,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
       if ((st = check_launch("k_bin_count_bal")) != XG_OK) return st;
     } else {
       k_bin_count<<<C, kBinThreads, sm_count, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                                   bin_rounds(n, n_tiles), w.hist, w.wcnt);
+                                                   rounds, w.hist, w.wcnt);
       if ((st = check_launch("k_bin_count")) != XG_OK) return st;
     }
     const long long hn = (long long)n_tiles * C;
@@ -936,7 +949,7 @@ xg_status xg_bin_sort(const xg_camera* cam, xg_splats* sp, void* workspace, size
       if ((st = check_launch("k_bin_emit_bal")) != XG_OK) return st;
     } else {
       k_bin_emit<<<C, kBinThreads, sm_emit, s>>>(sp->order, sp->n_tiles, (const ushort4*)sp->rect, n, ntx, n_tiles,
-                                                 bin_rounds(n, n_tiles), w.hoff, w.wcnt, cap, sp->entry_splat);
+                                                 rounds, w.hoff, w.wcnt, cap, sp->entry_splat);
       if ((st = check_launch("k_bin_emit")) != XG_OK) return st;
     }
     if (!sp->tile_order || fused_order) return XG_OK;

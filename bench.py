@@ -1026,10 +1026,15 @@ def train_block(args, timed, clock_cls, local, world: int = 1, c5: bool = False)
         # the trainer's overlapped forward + reverse replay (xg_composite_train_pair):
         # one roofline over both kernels, (17 + 51) FLOP per traversed pair
         pair_ach = (FLOP_PER_PAIR + FLOP_BWD_PAIR) * ppi / (d["pair_ms"] * 1e-3) / 1e12
+        tp = ROOT / "profiles" / "ncu_train_pair.json"
+        pair_traffic = json.loads(tp.read_text())["dram_bytes_per_iteration"] if (tp.exists() and world == 1 and not c5) \
+            else None
         train_roof = {"bound": "fp32", "kernel": "k_composite_fwd_np + k_composite_bwd_stream (one overlapped pair, "
                                                  "xg_composite_train_pair)",
                       "achieved": pair_ach, "peak": peak, "unit": "TFLOP/s", "frac": pair_ach / peak,
-                      "traffic": None, "flop_per_unit": FLOP_PER_PAIR + FLOP_BWD_PAIR, "units_per_launch": ppi,
+                      "traffic": pair_traffic,
+                      "traffic_source": "profiles/ncu_train_pair.json (dram read + write of both kernels at C2, ncu)"
+                      if pair_traffic else None, "flop_per_unit": FLOP_PER_PAIR + FLOP_BWD_PAIR, "units_per_launch": ppi,
                       "kernel_ms_in_timed_region": d["pair_ms"], "peak_source": note,
                       "units_note": "traversed pairs per iteration: mean over the 50 train views, probed on "
                                     "the cloud at the start and the end of the timed window; the pair's time runs "

@@ -866,9 +866,28 @@ struct BsSorted {  // the stable pass's result: vals {a, b, in}[*sel]
   }
 };
 
+// Bucket starts from the stable pass's order: the first sorted position of
+// each non-empty bucket (a bucket's end is start + count) - in place of an
+// exclusive scan over all 65,536 bucket counts.
+__device__ __forceinline__ uint32_t bs_bucket_of(const unsigned long long* __restrict__ keys,
+                                                 const uint32_t* __restrict__ n_tiles,
+                                                 const unsigned long long* __restrict__ mm, uint32_t ix) {
+  return n_tiles[ix] ? min((uint32_t)((keys[ix] - mm[0]) >> bs_shift(mm)), kBsInactive - 1u) : kBsInactive;
+}
+
+__global__ void k_bs_bounds(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,
+                            const unsigned long long* __restrict__ mm, BsSorted srt, long long n,
+                            uint32_t* __restrict__ start) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t* __restrict__ sorted = srt.get();
+  const uint32_t b = bs_bucket_of(keys, n_tiles, mm, sorted[p]);
+  if (p == 0 || bs_bucket_of(keys, n_tiles, mm, sorted[p - 1]) != b) start[b] = (uint32_t)p;
+}
+
 __global__ void k_bs_rank(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_tiles,
                           const unsigned long long* __restrict__ mm, BsSorted srt, long long n,
-                          const uint32_t* __restrict__ start, const unsigned long long* __restrict__ bmin,
+                          const uint32_t* __restrict__ start, const uint32_t* __restrict__ count, const unsigned long long* __restrict__ bmin,
                           const unsigned long long* __restrict__ bmax, uint32_t* __restrict__ order,
                           uint32_t* __restrict__ large, uint32_t* __restrict__ n_large, uint32_t* __restrict__ mixed,
                           uint32_t* __restrict__ n_mixed) {
@@ -881,7 +900,7 @@ __global__ void k_bs_rank(const unsigned long long* __restrict__ keys, const uin
     order[p] = ix;
     return;
   }
-  const uint32_t lo = start[b], hi = start[b + 1];
+  const uint32_t lo = start[b], hi = lo + count[b];
   if (hi - lo > (uint32_t)kBsRankBrute) {  // warp (<= kBsRankMax) or CTA sort
     if (p == lo) {
       if (hi - lo > (uint32_t)kBsRankMax) large[atomicAdd(n_large, 1u)] = b;
@@ -904,7 +923,8 @@ __global__ void k_bs_rank(const unsigned long long* __restrict__ keys, const uin
 // place in global memory (scratch K / I).  Writes the bucket's order[].
 __global__ void __launch_bounds__(kBsLargeThreads)
     k_bs_large(const unsigned long long* __restrict__ keys, BsSorted srt,
-               const uint32_t* __restrict__ start, const uint32_t* __restrict__ large,
+               const uint32_t* __restrict__ start, const uint32_t* __restrict__ count,
+               const uint32_t* __restrict__ large,
                const uint32_t* __restrict__ n_large, unsigned long long* __restrict__ gk, uint32_t* __restrict__ gi,
                uint32_t* __restrict__ order) {
   extern __shared__ unsigned char bs_smem[];
@@ -912,7 +932,7 @@ __global__ void __launch_bounds__(kBsLargeThreads)
   const uint32_t nl = *n_large;
   for (uint32_t j = blockIdx.x; j < nl; j += gridDim.x) {
     const uint32_t b = large[j];
-    const uint32_t lo = start[b], s = start[b + 1] - lo;
+    const uint32_t lo = start[b], s = count[b];
     uint32_t m = 1;
     while (m < s) m <<= 1;
     const bool in_smem = s <= (uint32_t)kBsSmemMax;
@@ -1091,6 +1111,7 @@ __device__ __forceinline__ bool bs_warp_few(const unsigned long long* __restrict
 
 __global__ void __launch_bounds__(128) k_bs_mixed(const unsigned long long* __restrict__ keys, BsSorted srt,
                                                   const uint32_t* __restrict__ start,
+                                                  const uint32_t* __restrict__ count,
                                                   const uint32_t* __restrict__ mixed,
                                                   const uint32_t* __restrict__ n_mixed,
                                                   uint32_t* __restrict__ order) {
@@ -1099,7 +1120,7 @@ __global__ void __launch_bounds__(128) k_bs_mixed(const unsigned long long* __re
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < nm; j += warps) {
     const uint32_t b = mixed[j];
-    const uint32_t lo = start[b], s = start[b + 1] - lo;
+    const uint32_t lo = start[b], s = count[b];
     if (bs_warp_few(keys, sorted, lo, s, order)) continue;
     if (s <= 64) bs_warp_bucket<2>(keys, sorted, lo, s, order);
     else if (s <= 128) bs_warp_bucket<4>(keys, sorted, lo, s, order);
@@ -1136,19 +1157,18 @@ xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_ti
   const OsWs ow = os_prepare(w.tail, n, 2, s, false);
   k_bs_bucket<<<g, 256, 0, s>>>(keys, n_tiles, n, w.mm, key_b, val_b, w.count, w.bmin, w.bmax, ow.ghist);
   if ((st = check_launch("k_bs_bucket")) != XG_OK) return st;
-  g_scan_precleared = w.scan_bytes >= scan_workspace_bytes(kBsBuckets);  // (zeroed above)
-  if ((st = scan_u32(w.count, nullptr, w.start, kBsBuckets, nullptr, kBsBuckets, w.start + kBsBuckets, w.scan_ws,
-                     w.scan_bytes, s)) != XG_OK)
-    return st;
+
   // stable by 16-bit bucket id: two byte passes (ids < 2^16); no final copy
   k_os_scan<<<1, 256, 0, s>>>(ow.ghist, ow.gofs, n_dev, n, ow.sel, 2);
   if ((st = check_launch("k_os_scan")) != XG_OK) return st;
   if ((st = os_passes(ow, key_b, val_b, key_a, key_b, val_a, val_b, n, n_dev, 2, s)) != XG_OK) return st;
   BsSorted srt{{val_a, val_b, val_b}, ow.sel + kOsPasses};
-  k_bs_rank<<<g, 256, 0, s>>>(keys, n_tiles, w.mm, srt, n, w.start, w.bmin, w.bmax, order, w.large, w.n_large,
-                              w.mixed, w.n_mixed);
+  k_bs_bounds<<<g, 256, 0, s>>>(keys, n_tiles, w.mm, srt, n, w.start);
+  if ((st = check_launch("k_bs_bounds")) != XG_OK) return st;
+  k_bs_rank<<<g, 256, 0, s>>>(keys, n_tiles, w.mm, srt, n, w.start, w.count, w.bmin, w.bmax, order, w.large,
+                              w.n_large, w.mixed, w.n_mixed);
   if ((st = check_launch("k_bs_rank")) != XG_OK) return st;
-  k_bs_mixed<<<4 * 148, 128, 0, s>>>(keys, srt, w.start, w.mixed, w.n_mixed, order);
+  k_bs_mixed<<<4 * 148, 128, 0, s>>>(keys, srt, w.start, w.count, w.mixed, w.n_mixed, order);
   if ((st = check_launch("k_bs_mixed")) != XG_OK) return st;
   static bool attr = false;
   const int smem = (int)((sizeof(unsigned long long) + sizeof(uint32_t)) * kBsSmemMax);
@@ -1156,7 +1176,8 @@ xg_status bucket_sort_depth(const unsigned long long* keys, const uint32_t* n_ti
     cudaFuncSetAttribute(k_bs_large, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_bs_large<<<148, kBsLargeThreads, smem, s>>>(keys, srt, w.start, w.large, w.n_large, key_a, val_a, order);
+  k_bs_large<<<148, kBsLargeThreads, smem, s>>>(keys, srt, w.start, w.count, w.large, w.n_large, key_a, val_a,
+                                                 order);
   return check_launch("k_bs_large");
 }
 
